@@ -1,0 +1,94 @@
+/* drzg — B200-native controlled-reduction engine (arXiv 2602.24155).
+ *
+ * The drop-in boundary: a plain C ABI (no C++ or torch types) over the
+ * device kernels and the device-resident reduction engine.  Each entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj/include/drzeta/).  All functions return 0 on success;
+ * on failure they return nonzero and drzg_last_error() holds the message
+ * (the reference's contract_error text, file:line included).  Functions that
+ * return char* hand back a malloc'd JSON document (free with drzg_free); on
+ * failure they return NULL.
+ *
+ * Residue layouts at this boundary are the reference's:
+ *   ModMatrix / ModVec (linalg.hpp:94-141): `limbs` planes of base-beta
+ *   digits, plane-major then row-major, beta = p^limb_exp from StripePlan.
+ *   Hypersurface coefficients: one per degree-d monomial in the reference's
+ *   grevlex-descending order (monomial.hpp:84-149).
+ */
+#ifndef DRZG_H
+#define DRZG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* StripePlan (linalg.hpp:20-58) */
+typedef struct drzg_stripe_plan {
+  uint64_t p;
+  int32_t M;
+  int32_t limbs;
+  int32_t limb_exp;
+  int32_t pad_;
+  uint64_t beta;
+  int64_t stripe;
+} drzg_stripe_plan;
+
+const char* drzg_last_error(void);
+void drzg_free(char* s);
+int drzg_device_count(void);
+
+/* StripePlan::make(p, M)  — linalg.hpp:35-58 */
+int drzg_stripe_plan_make(uint64_t p, int32_t M, drzg_stripe_plan* out);
+
+/* linrec_eval(A, B, tmax, w, ctr) — linalg.hpp:337-410.
+ * w <- M(0) M(1) ... M(tmax) w with M(t) = t*A + B (factor t = tmax first),
+ * side x side operands; host buffers (copied to and from the device inside
+ * the call).  *matvecs += tmax + 1. */
+int drzg_linrec_eval(const drzg_stripe_plan* plan, int32_t side, const uint64_t* A, const uint64_t* B, int64_t tmax,
+                     uint64_t* w, int64_t* matvecs);
+
+/* same, all pointers in device memory, launched on `stream`
+ * (cudaStream_t or NULL); *kernel_ms receives the CUDA-event time of the
+ * stepping kernels when non-NULL */
+int drzg_linrec_eval_device(const drzg_stripe_plan* plan, int32_t side, const uint64_t* dA, const uint64_t* dB,
+                            int64_t tmax, uint64_t* dw, int64_t* matvecs, void* stream, float* kernel_ms);
+
+/* detail::sparse_steps(plan, A, B, tmax, w, ctr) — linalg.hpp:257-331.
+ * A and B in SparseOp CSC form (linalg.hpp:219-252): col_ptr[side+1],
+ * row_idx[nnz], digs[nnz*limbs] entry-major. */
+int drzg_sparse_steps(const drzg_stripe_plan* plan, int32_t side, const int64_t* a_col_ptr, const int32_t* a_row_idx,
+                      const uint64_t* a_digs, const int64_t* b_col_ptr, const int32_t* b_row_idx,
+                      const uint64_t* b_digs, int64_t tmax, uint64_t* w, int64_t* matvecs);
+
+/* reduce_chunk(C, store, st, v, k, ledger) — reduction.hpp:394-423, for one
+ * state of the hypersurface (p, n, d, coeffs) at working precision M and the
+ * default working set; w in ModVec layout, updated in place; u updated. */
+char* drzg_reduce_chunk(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int32_t* u,
+                        int32_t pole, const int32_t* v, int64_t k, uint64_t* w, int32_t device);
+
+/* frobenius_matrix(X, B, plan, policy, pep, S, only_pole, threads) —
+ * zeta.hpp:36-136.  policy: 0 p-chunk.  columns: optional subset (NULL = all)
+ * for partitioning across GPUs.  JSON: F (b*b decimal strings, row-major),
+ * charpoly residues mod p^(M+n) (all columns only), plan, ledger
+ * (matvecs/startups/combines), stage and kernel timings. */
+char* drzg_frobenius(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
+                     int32_t nm_override, int32_t only_pole, const int32_t* columns, int32_t ncolumns,
+                     int32_t device, int32_t profile);
+
+/* run_zeta(X, opts) — zeta.hpp:438-549.  JSON: Q, ambiguity, plan, slopes,
+ * invariants (p-rank, height, domino, newton height), count checks, ledger,
+ * wall time. */
+char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
+                int32_t nm_override, int32_t verify_counts, int32_t device, int32_t profile);
+
+/* charpoly + recover_Q on a given F (zeta.hpp:456-470); F as b*b decimal strings */
+char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t nm_override, int32_t b,
+                    const char* const* F);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DRZG_H */

@@ -1,0 +1,169 @@
+"""drzg: B200-native controlled-reduction engine (arXiv 2602.24155).
+
+Python view of the C ABI in include/drzg.h (libdrzg.so, built in-tree by
+`make -C paper_2602_24155_b200/csrc`).  The names and argument meanings mirror
+the reference's C++ entry points (drzeta: linrec_eval, detail::sparse_steps,
+reduce_chunk, frobenius_matrix, run_zeta).  There is no CPU fallback: if the
+library is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdrzg.so")
+POLICIES = {"p-chunk": 0, "pchunk": 0, "depth-first": 1, "depth": 1, "var-by-var": 2, "varbyvar": 2}
+
+_lib = None
+
+
+class DrzgError(RuntimeError):
+    """contract_error / singular_input / escalation_exhausted from the engine"""
+
+
+class StripePlan(ctypes.Structure):
+    """StripePlan (reference linalg.hpp:20-58)"""
+    _fields_ = [("p", ctypes.c_uint64), ("M", ctypes.c_int32), ("limbs", ctypes.c_int32),
+                ("limb_exp", ctypes.c_int32), ("pad_", ctypes.c_int32), ("beta", ctypes.c_uint64),
+                ("stripe", ctypes.c_int64)]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DrzgError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}/csrc`")
+        L = ctypes.CDLL(LIB_PATH)
+        L.drzg_last_error.restype = ctypes.c_char_p
+        for name in ("drzg_zeta", "drzg_frobenius", "drzg_reduce_chunk", "drzg_charpoly"):
+            getattr(L, name).restype = ctypes.c_void_p
+        _lib = L
+    return _lib
+
+
+def _err():
+    return lib().drzg_last_error().decode()
+
+
+def _check(rc):
+    if rc != 0:
+        raise DrzgError(_err())
+
+
+def _json(ptr):
+    if not ptr:
+        raise DrzgError(_err())
+    s = ctypes.cast(ptr, ctypes.c_char_p).value.decode()
+    lib().drzg_free(ctypes.c_void_p(ptr))
+    return json.loads(s)
+
+
+def _u64arr(xs):
+    return (ctypes.c_uint64 * len(xs))(*[int(x) for x in xs])
+
+
+_P64 = ctypes.POINTER(ctypes.c_uint64)
+
+
+def device_count():
+    return lib().drzg_device_count()
+
+
+def stripe_plan(p, M):
+    sp = StripePlan()
+    _check(lib().drzg_stripe_plan_make(ctypes.c_uint64(p), M, ctypes.byref(sp)))
+    return sp
+
+
+def linrec_eval(p, M, side, A, B, tmax, w):
+    """reference linrec_eval (linalg.hpp:337-410) on the GPU; A, B, w in the
+    reference's plane-major base-beta layout; returns (w_out, matvecs)"""
+    sp = stripe_plan(p, M)
+    A = np.ascontiguousarray(A, dtype=np.uint64)
+    B = np.ascontiguousarray(B, dtype=np.uint64)
+    w = np.array(w, dtype=np.uint64, copy=True)
+    ctr = ctypes.c_int64(0)
+    _check(lib().drzg_linrec_eval(ctypes.byref(sp), side, A.ctypes.data_as(_P64), B.ctypes.data_as(_P64),
+                                  ctypes.c_int64(tmax), w.ctypes.data_as(_P64), ctypes.byref(ctr)))
+    return w, ctr.value
+
+
+def linrec_eval_device(p, M, side, dA_ptr, dB_ptr, tmax, dw_ptr, stream_ptr=0, timed=False):
+    """device-pointer variant (torch tensors' data_ptr()); returns kernel ms if timed"""
+    sp = stripe_plan(p, M)
+    ctr = ctypes.c_int64(0)
+    ms = ctypes.c_float(0.0)
+    _check(lib().drzg_linrec_eval_device(ctypes.byref(sp), side, ctypes.c_void_p(dA_ptr), ctypes.c_void_p(dB_ptr),
+                                         ctypes.c_int64(tmax), ctypes.c_void_p(dw_ptr), ctypes.byref(ctr),
+                                         ctypes.c_void_p(stream_ptr), ctypes.byref(ms) if timed else None))
+    return ms.value if timed else None
+
+
+def sparse_steps(p, M, side, A, B, tmax, w):
+    """reference detail::sparse_steps (linalg.hpp:257-331): A, B given dense in
+    plane layout are compressed to the reference's SparseOp CSC (linalg.hpp:227-251)"""
+    sp = stripe_plan(p, M)
+    L = sp.limbs
+
+    def csc(X):
+        X = np.asarray(X, dtype=np.uint64).reshape(L, side, side)
+        nz = (X != 0).any(axis=0)  # rows x cols
+        col_ptr = [0]
+        rows, digs = [], []
+        for j in range(side):
+            idx = np.nonzero(nz[:, j])[0]
+            rows.extend(idx.tolist())
+            for i in idx:
+                digs.extend(int(X[t, i, j]) for t in range(L))
+            col_ptr.append(len(rows))
+        return (np.array(col_ptr, dtype=np.int64), np.array(rows, dtype=np.int32), np.array(digs, dtype=np.uint64))
+
+    (ac, ar, ad), (bc, br, bd) = csc(A), csc(B)
+    w = np.array(w, dtype=np.uint64, copy=True)
+    ctr = ctypes.c_int64(0)
+    P64i = ctypes.POINTER(ctypes.c_int64)
+    P32 = ctypes.POINTER(ctypes.c_int32)
+    _check(lib().drzg_sparse_steps(ctypes.byref(sp), side,
+                                   ac.ctypes.data_as(P64i), ar.ctypes.data_as(P32), ad.ctypes.data_as(_P64),
+                                   bc.ctypes.data_as(P64i), br.ctypes.data_as(P32), bd.ctypes.data_as(_P64),
+                                   ctypes.c_int64(tmax), w.ctypes.data_as(_P64), ctypes.byref(ctr)))
+    return w, ctr.value
+
+
+def reduce_chunk(p, n, d, coeffs, M, u, pole, v, k, w, device=0):
+    """reference reduce_chunk (reduction.hpp:394-423) for one state; returns
+    (w_out, u_out, info)"""
+    w = np.array(w, dtype=np.uint64, copy=True)
+    ua = (ctypes.c_int32 * (n + 1))(*u)
+    va = (ctypes.c_int32 * (n + 1))(*v)
+    info = _json(lib().drzg_reduce_chunk(ctypes.c_uint64(p), n, d, _u64arr(coeffs), M, ua, pole, va,
+                                         ctypes.c_int64(k), w.ctypes.data_as(_P64), device))
+    return w, list(ua), info
+
+
+def frobenius(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, only_pole=0, columns=None, device=0,
+              profile=False):
+    """reference frobenius_matrix (zeta.hpp:36-136)"""
+    cols = None
+    ncols = 0
+    if columns is not None:
+        cols = (ctypes.c_int32 * len(columns))(*columns)
+        ncols = len(columns)
+    return _json(lib().drzg_frobenius(ctypes.c_uint64(p), n, d, _u64arr(coeffs), POLICIES[policy], r_uniform, nm,
+                                      only_pole, cols, ncols, device, int(profile)))
+
+
+def zeta(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, verify_counts=True, device=0, profile=False):
+    """reference run_zeta (zeta.hpp:438-549)"""
+    return _json(lib().drzg_zeta(ctypes.c_uint64(p), n, d, _u64arr(coeffs), POLICIES[policy], r_uniform, nm,
+                                 int(verify_counts), device, int(profile)))
+
+
+def charpoly(p, n, d, F, b, r_uniform=0, nm=0):
+    """berkowitz_charpoly + recover_Q on a given F (zeta.hpp:456-470)"""
+    arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F])
+    return _json(lib().drzg_charpoly(ctypes.c_uint64(p), n, d, r_uniform, nm, b, arr))

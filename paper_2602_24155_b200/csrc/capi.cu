@@ -1,0 +1,343 @@
+// The C ABI (include/drzg.h): marshalling between the reference's plain
+// layouts and the engine, exceptions -> status codes + thread-local message.
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "../../include/drzg.h"
+#include "kernels/linrec.cuh"
+#include "pipeline.cuh"
+
+using namespace drzg;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard_int(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  } catch (...) {
+    g_err = "unknown error";
+    return 1;
+  }
+}
+
+template <class F>
+char* guard_str(F&& f) {
+  try {
+    std::string s = f();
+    char* out = (char*)std::malloc(s.size() + 1);
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    g_err.clear();
+    return out;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  } catch (...) {
+    g_err = "unknown error";
+    return nullptr;
+  }
+}
+
+// StripePlan::make (linalg.hpp:35-58): smallest limb count with beta =
+// p^ceil(M/limbs) <= 2^62 and limbs (beta-1)^2 <= 2^126
+drzg_stripe_plan stripe_plan(u64 p, int M) {
+  DRZG_REQUIRE(p >= 2 && M >= 1, "StripePlan: bad modulus");
+  for (int limbs = 1; limbs <= 64; ++limbs) {
+    int e = (M + limbs - 1) / limbs;
+    Z pe = Z::pow(p, (u64)e);
+    if (pe > Z::from_u64(u64(1) << 62)) continue;
+    u64 beta = pe.to_u64();
+    u128 prod = (u128)(beta - 1) * (beta - 1);
+    u128 cap = u128(1) << 126;
+    if (prod > cap / (u128)limbs) continue;
+    drzg_stripe_plan pl{};
+    pl.p = p;
+    pl.M = M;
+    pl.limbs = limbs;
+    pl.limb_exp = e;
+    pl.beta = beta;
+    u128 s = cap / (prod * (u128)limbs);
+    pl.stripe = s > (u128)((i64)1 << 40) ? ((i64)1 << 40) : (i64)s;
+    return pl;
+  }
+  DRZG_REQUIRE(false, "StripePlan: no viable limb split");
+  return {};
+}
+
+LinrecPlan linrec_plan(const drzg_stripe_plan* sp) {
+  LinrecPlan lp;
+  lp.p = sp->p;
+  lp.M = sp->M;
+  lp.limbs = sp->limbs;
+  lp.limb_exp = sp->limb_exp;
+  lp.beta = sp->beta;
+  lp.top_mod = ipow(sp->p, sp->M - sp->limb_exp * (sp->limbs - 1));
+  return lp;
+}
+
+std::string zjson(const std::vector<Z>& v) {
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < v.size(); ++i) os << (i ? "," : "") << "\"" << v[i].str() << "\"";
+  os << "]";
+  return os.str();
+}
+template <class T>
+std::string ijson(const std::vector<T>& v) {
+  std::ostringstream os;
+  os << "[";
+  for (size_t i = 0; i < v.size(); ++i) os << (i ? "," : "") << v[i];
+  os << "]";
+  return os.str();
+}
+std::string plan_json(const PrecisionPlan& P) {
+  std::ostringstream os;
+  os << "{\"M\":" << P.M << ",\"A\":" << P.A << ",\"A_sharp\":" << P.A_sharp << ",\"b\":" << P.b
+     << ",\"escalations\":" << P.escalations << ",\"r_m\":" << ijson(P.r_m) << ",\"N_m\":" << ijson(P.N_m)
+     << ",\"s_m\":" << ijson(P.s_m) << "}";
+  return os.str();
+}
+std::string frob_json_body(const FrobResult& fr) {
+  std::ostringstream os;
+  os.precision(9);
+  os << "\"b\":" << fr.b << ",\"M\":" << fr.M << ",\"digits\":{\"q\":" << fr.q << ",\"Ld\":" << fr.Ld
+     << "},\"nL\":" << fr.nL << ",\"side\":" << fr.side << ",\"terms\":" << fr.terms
+     << ",\"matvecs\":" << fr.led.matvecs << ",\"startups\":" << fr.led.startups
+     << ",\"combines\":" << fr.led.combines << ",\"computed\":" << ijson(fr.computed)
+     << ",\"times\":{\"tables\":" << fr.t.tables << ",\"seeds\":" << fr.t.seeds << ",\"device\":" << fr.t.device
+     << ",\"final\":" << fr.t.final << ",\"total\":" << fr.t.total << "}"
+     << ",\"kernels\":{\"gemm_ms\":" << fr.clk.gemm_ms << ",\"carry_ms\":" << fr.clk.carry_ms
+     << ",\"gather_ms\":" << fr.clk.gather_ms << ",\"epilogue_ms\":" << fr.clk.epi_ms
+     << ",\"other_ms\":" << fr.clk.other_ms << ",\"gemm_launches\":" << fr.clk.gemm_launches
+     << ",\"gemm_macs\":" << fr.clk.gemm_macs << "}";
+  return os.str();
+}
+Policy policy_of(int p) {
+  DRZG_REQUIRE(p >= 0 && p <= 2, "unknown policy");
+  return (Policy)p;
+}
+PlanOverrides overrides(int r_uniform, int nm) {
+  PlanOverrides ov;
+  ov.r_uniform = r_uniform;
+  if (nm > 0) ov.N_m = {nm};
+  return ov;
+}
+std::vector<u64> coeff_vec(int n, int d, const uint64_t* coeffs) {
+  size_t cnt = (size_t)mono_count(n + 1, d);
+  return std::vector<u64>(coeffs, coeffs + cnt);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* drzg_last_error(void) { return g_err.c_str(); }
+void drzg_free(char* s) { std::free(s); }
+
+int drzg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int drzg_stripe_plan_make(uint64_t p, int32_t M, drzg_stripe_plan* out) {
+  return guard_int([&] { *out = stripe_plan(p, M); });
+}
+
+int drzg_linrec_eval_device(const drzg_stripe_plan* plan, int32_t side, const uint64_t* dA, const uint64_t* dB,
+                            int64_t tmax, uint64_t* dw, int64_t* matvecs, void* stream, float* kernel_ms) {
+  return guard_int([&] {
+    linrec_device(linrec_plan(plan), side, dA, dB, tmax, dw, (cudaStream_t)stream, kernel_ms, nullptr);
+    if (matvecs) *matvecs += tmax + 1;
+  });
+}
+
+int drzg_linrec_eval(const drzg_stripe_plan* plan, int32_t side, const uint64_t* A, const uint64_t* B, int64_t tmax,
+                     uint64_t* w, int64_t* matvecs) {
+  return guard_int([&] {
+    size_t nn = (size_t)plan->limbs * side * side, nv = (size_t)plan->limbs * side;
+    DevBuf<uint64_t> dA, dB, dw;
+    dA.alloc(nn);
+    dB.alloc(nn);
+    dw.alloc(nv);
+    DRZG_CUDA(cudaMemcpy(dA.p, A, nn * 8, cudaMemcpyHostToDevice));
+    DRZG_CUDA(cudaMemcpy(dB.p, B, nn * 8, cudaMemcpyHostToDevice));
+    DRZG_CUDA(cudaMemcpy(dw.p, w, nv * 8, cudaMemcpyHostToDevice));
+    linrec_device(linrec_plan(plan), side, dA.p, dB.p, tmax, dw.p, 0, nullptr, nullptr);
+    DRZG_CUDA(cudaMemcpy(w, dw.p, nv * 8, cudaMemcpyDeviceToHost));
+    if (matvecs) *matvecs += tmax + 1;
+  });
+}
+
+int drzg_sparse_steps(const drzg_stripe_plan* plan, int32_t side, const int64_t* a_col_ptr, const int32_t* a_row_idx,
+                      const uint64_t* a_digs, const int64_t* b_col_ptr, const int32_t* b_row_idx,
+                      const uint64_t* b_digs, int64_t tmax, uint64_t* w, int64_t* matvecs) {
+  return guard_int([&] {
+    const int L = plan->limbs;
+    // CSC (SparseOp) -> CSR on the host, once per call
+    auto to_csr = [&](const int64_t* cp, const int32_t* ri, const uint64_t* dg, std::vector<int>& ptr,
+                      std::vector<int>& col, std::vector<uint64_t>& val) {
+      i64 nnz = cp[side];
+      ptr.assign(side + 1, 0);
+      for (i64 e = 0; e < nnz; ++e) ptr[ri[e] + 1]++;
+      for (int i = 0; i < side; ++i) ptr[i + 1] += ptr[i];
+      col.assign(nnz, 0);
+      val.assign((size_t)nnz * L, 0);
+      std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+      for (int j = 0; j < side; ++j)
+        for (i64 e = cp[j]; e < cp[j + 1]; ++e) {
+          int pos = fill[ri[e]]++;
+          col[pos] = j;
+          for (int t = 0; t < L; ++t) val[(size_t)pos * L + t] = dg[(size_t)e * L + t];
+        }
+    };
+    std::vector<int> ap, ac, bp, bc;
+    std::vector<uint64_t> av, bv;
+    to_csr(a_col_ptr, a_row_idx, a_digs, ap, ac, av);
+    to_csr(b_col_ptr, b_row_idx, b_digs, bp, bc, bv);
+    DevBuf<int> dap, dac, dbp, dbc;
+    DevBuf<uint64_t> dav, dbv, dw;
+    dap.upload(ap, 0);
+    dac.upload(ac, 0);
+    dbp.upload(bp, 0);
+    dbc.upload(bc, 0);
+    dav.upload(av, 0);
+    dbv.upload(bv, 0);
+    std::vector<uint64_t> hw(w, w + (size_t)L * side);
+    dw.upload(hw, 0);
+    CsrPair csr{dap.p, dac.p, dav.p, dbp.p, dbc.p, dbv.p};
+    linrec_device(linrec_plan(plan), side, nullptr, nullptr, tmax, dw.p, 0, nullptr, &csr);
+    DRZG_CUDA(cudaMemcpy(w, dw.p, hw.size() * 8, cudaMemcpyDeviceToHost));
+    if (matvecs) *matvecs += tmax + 1;
+  });
+}
+
+char* drzg_reduce_chunk(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int32_t* u,
+                        int32_t pole, const int32_t* v, int64_t k, uint64_t* w, int32_t device) {
+  return guard_str([&]() -> std::string {
+    DRZG_CUDA(cudaSetDevice(device));
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    RuvTables T = build_tables(X, M, default_S(n, d));
+    DRZG_REQUIRE(pole - k >= n, "reduce_chunk: chunk passes the floor");
+    drzg_stripe_plan sp = stripe_plan(p, M);
+    HostMod hm = HostMod::make(p, M);
+    const int nv = n + 1, Ld = T.dp.Ld;
+    // ModVec digits -> residues -> balanced base-q digit planes
+    std::vector<i8> dig((size_t)Ld * T.side);
+    std::vector<i8> tmp(Ld);
+    Z beta = Z::from_u64(sp.beta);
+    for (int g = 0; g < T.side; ++g) {
+      Z val(0);
+      for (int t = sp.limbs - 1; t >= 0; --t) val = val * beta + Z::from_u64(w[(size_t)t * T.side + g]);
+      to_digits_z(val.mod(hm.mz), T.dp, tmp.data());
+      for (int t = 0; t < Ld; ++t) dig[(size_t)t * T.side + g] = tmp[t];
+    }
+    Expo ue(nv), ve(nv);
+    for (int i = 0; i < nv; ++i) ue[i] = u[i], ve[i] = v[i];
+    cudaStream_t st;
+    DRZG_CUDA(cudaStreamCreate(&st));
+    Ledger led;
+    {
+      ReductionEngine eng(T, n, p, st);
+      eng.chunk_batch({ue}, {(int)rank_of(ve)}, {k}, dig, led);
+    }
+    DRZG_CUDA(cudaStreamDestroy(st));
+    std::vector<i64> s(Ld);
+    for (int g = 0; g < T.side; ++g) {
+      for (int t = 0; t < Ld; ++t) s[t] = dig[(size_t)t * T.side + g];
+      Z val = from_digit_sums(s.data(), T.dp, hm.mz);
+      for (int t = 0; t < sp.limbs; ++t) {
+        Z q = Z::from_u64(sp.beta);
+        Z r = val.mod(q);
+        w[(size_t)t * T.side + g] = r.to_u64();
+        val = (val - r).divexact(q);
+      }
+    }
+    for (int i = 0; i < nv; ++i) u[i] -= (int)(k * v[i]);
+    std::ostringstream os;
+    os << "{\"side\":" << T.side << ",\"nL\":" << T.nL << ",\"pole\":" << pole - k << ",\"matvecs\":" << led.matvecs
+       << ",\"startups\":" << led.startups << "}";
+    return os.str();
+  });
+}
+
+char* drzg_frobenius(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
+                     int32_t nm_override, int32_t only_pole, const int32_t* columns, int32_t ncolumns,
+                     int32_t device, int32_t profile) {
+  return guard_str([&]() -> std::string {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    Policy pol = policy_of(policy);
+    std::set<int> S = working_set_for(X, pol);
+    Basis B = compute_basis(X);
+    PrecisionPlan plan = choose_precision(p, n, d, overrides(r_uniform, nm_override));
+    FrobOptions fo;
+    fo.policy = pol;
+    fo.overrides = overrides(r_uniform, nm_override);
+    fo.only_pole = only_pole;
+    fo.profile = profile != 0;
+    if (columns)
+      for (int i = 0; i < ncolumns; ++i) fo.columns.push_back(columns[i]);
+    FrobResult fr = frobenius_matrix(X, B, plan, S, fo, device);
+    std::vector<Z> dres;
+    if (!only_pole && fo.columns.empty())
+      dres = berkowitz(fr.F, (int)fr.b, Z::pow(p, (u64)(plan.M + n)));
+    std::ostringstream os;
+    os << "{" << frob_json_body(fr) << ",\"plan\":" << plan_json(plan) << ",\"F\":" << zjson(fr.F)
+       << ",\"charpoly\":" << zjson(dres) << "}";
+    return os.str();
+  });
+}
+
+char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
+                int32_t nm_override, int32_t verify_counts, int32_t device, int32_t profile) {
+  return guard_str([&]() -> std::string {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    ZetaOptions zo;
+    zo.policy = policy_of(policy);
+    zo.overrides = overrides(r_uniform, nm_override);
+    zo.verify_counts = verify_counts != 0;
+    zo.profile = profile != 0;
+    ZetaOut r = run_zeta(X, zo, device);
+    std::ostringstream os;
+    os.precision(9);
+    os << "{\"Q\":" << zjson(r.Q) << ",\"Q_alt\":" << zjson(r.Q_alt)
+       << ",\"ambiguous\":" << (r.ambiguous ? "true" : "false") << ",\"plan\":" << plan_json(r.plan)
+       << ",\"p_rank\":" << r.inv.p_rank << ",\"height\":\"" << r.inv.height << "\",\"domino\":\"" << r.inv.domino
+       << "\",\"domino_any\":\"" << r.domino << "\",\"newton_height\":\"" << r.inv.newton_height
+       << "\",\"fsplit\":" << (r.inv.fsplit_defined ? (r.inv.fsplit ? "true" : "false") : "null") << ",\"slopes\":[";
+    for (size_t i = 0; i < r.np.slopes.size(); ++i)
+      os << (i ? "," : "") << "[\"" << r.np.slopes[i].first.str() << "\"," << r.np.slopes[i].second << "]";
+    os << "],\"counts\":[";
+    for (size_t i = 0; i < r.counts.size(); ++i)
+      os << (i ? "," : "") << "[" << r.counts[i].r << ",\"" << r.counts[i].from_zeta.str() << "\","
+         << (r.counts[i].ok ? "true" : "false") << "]";
+    os << "],\"seconds\":" << r.wall << ",\"frobenius\":{" << frob_json_body(r.last) << "}}";
+    return os.str();
+  });
+}
+
+char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t nm_override, int32_t b,
+                    const char* const* F) {
+  return guard_str([&]() -> std::string {
+    PrecisionPlan plan = choose_precision(p, n, d, overrides(r_uniform, nm_override));
+    std::vector<Z> f((size_t)b * b);
+    for (size_t i = 0; i < f.size(); ++i) f[i] = Z::from_str(F[i]);
+    auto dres = berkowitz(f, b, Z::pow(p, (u64)(plan.M + n)));
+    Recovered rec = recover_Q(dres, plan);
+    std::ostringstream os;
+    os << "{\"charpoly\":" << zjson(dres) << ",\"status\":" << rec.status << ",\"candidates\":[";
+    for (size_t i = 0; i < rec.candidates.size(); ++i) os << (i ? "," : "") << zjson(rec.candidates[i]);
+    os << "]}";
+    return os.str();
+  });
+}
+
+}  // extern "C"

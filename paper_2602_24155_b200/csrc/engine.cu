@@ -1,0 +1,411 @@
+// Device-resident reduction engine (see engine.cuh).
+#include <algorithm>
+#include <functional>
+#include <map>
+
+#include "engine.cuh"
+#include "kernels/dixon.cuh"
+
+namespace drzg {
+
+namespace {
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+}  // namespace
+
+ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t st)
+    : T_(&T), n_(n), p_(p), st_(st) {
+  DRZG_REQUIRE(T.dp.Ld <= dev::kLdMax, "engine: too many digit planes");
+  nLp_ = round_up(T.nL, 64);
+  sidep_ = round_up(T.side, 16);
+  slot_stride_ = (long long)T.dp.Ld * sidep_;
+  gsize_ = (int)mono_count(T.nv, T.D - 1);
+  // C padded to nLp x nLp
+  std::vector<int8_t> Cp((size_t)nLp_ * nLp_, 0);
+  for (int r = 0; r < T.nL; ++r)
+    for (int c = 0; c < T.nL; ++c) Cp[(size_t)r * nLp_ + c] = T.sys.Cq[(size_t)r * T.nL + c];
+  C_.upload(Cp, st_);
+  jp_ptr_.upload(T.sys.rowptr, st_);
+  jp_col_.upload(T.sys.col, st_);
+  jp_val_.upload(T.sys.val, st_);
+  gidx_.upload(T.gidx, st_);
+  const auto& dl = monos(T.nv, T.d).mons;
+  std::vector<int> dirs;
+  for (const auto& v : dl) {
+    dirs_host_.push_back(v);
+    for (int i = 0; i < T.nv; ++i) dirs.push_back(v[i]);
+  }
+  dirs_.upload(dirs, st_);
+  t_ptr_.upload(T.t_ptr, st_);
+  t_src_.upload(T.t_src, st_);
+  sol_i_.upload(T.sol_i, st_);
+  sol_mu_.upload(T.sol_mu, st_);
+  std::vector<int> mon;
+  for (const auto& e : monos(T.nv, T.D).mons)
+    for (int i = 0; i < T.nv; ++i) mon.push_back(e[i]);
+  mon_.upload(mon, st_);
+  std::vector<unsigned long long> bt(Binom::get().tab.begin(), Binom::get().tab.end());
+  btab_.upload(bt, st_);
+  DRZG_CUDA(cudaEventCreate(&ev0_));
+  DRZG_CUDA(cudaEventCreate(&ev1_));
+}
+
+ReductionEngine::~ReductionEngine() {
+  if (pool_) cudaFree(pool_);
+  cudaEventDestroy(ev0_);
+  cudaEventDestroy(ev1_);
+}
+
+void ReductionEngine::timed(double* acc, const std::function<void()>& f) {
+  if (!clock.on) {
+    f();
+    return;
+  }
+  DRZG_CUDA(cudaEventRecord(ev0_, st_));
+  f();
+  DRZG_CUDA(cudaEventRecord(ev1_, st_));
+  DRZG_CUDA(cudaEventSynchronize(ev1_));
+  float ms = 0;
+  DRZG_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+  *acc += ms;
+}
+
+void ReductionEngine::grow_pool(int need) {
+  int ncap = std::max(need, std::max(1024, cap_ * 2));
+  size_t bytes = (size_t)ncap * slot_stride_;
+  size_t fr = 0, tot = 0;
+  DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  DRZG_REQUIRE(bytes - (size_t)cap_ * slot_stride_ + (size_t)(256u << 20) < fr,
+               "engine: state pool exceeds device memory");
+  int8_t* np = nullptr;
+  DRZG_CUDA(cudaMalloc(&np, bytes));
+  if (pool_) {
+    DRZG_CUDA(cudaMemcpyAsync(np, pool_, (size_t)cap_ * slot_stride_, cudaMemcpyDeviceToDevice, st_));
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    DRZG_CUDA(cudaFree(pool_));
+  }
+  pool_ = np;
+  for (int s = ncap - 1; s >= cap_; --s) free_.push_back(s);
+  cap_ = ncap;
+}
+
+int ReductionEngine::alloc_slot() {
+  if (free_.empty()) grow_pool(cap_ + 1);
+  int s = free_.back();
+  free_.pop_back();
+  return s;
+}
+
+void ReductionEngine::ensure_batch(int B) {
+  if (B <= bcap_) return;
+  const int Ld = T_->dp.Ld;
+  size_t per = (size_t)(2 * Ld + 1) * nLp_ + sizeof(int) * T_->nL;
+  size_t fr = 0, tot = 0;
+  DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  // temporaries get at most half of what is free, in multiples of 64 states
+  size_t lim = std::max<size_t>(64, (fr / 2) / per / 64 * 64);
+  int nb = (int)std::min<size_t>(lim, (size_t)round_up(B, 64));
+  if (nb <= bcap_) return;
+  bcap_ = nb;
+  Bg_.alloc((size_t)bcap_ * Ld * nLp_);
+  Y_.alloc((size_t)bcap_ * Ld * nLp_);
+  IN_.alloc((size_t)bcap_ * nLp_);
+  Cy_.alloc((size_t)bcap_ * T_->nL);
+  // K padding of Bg / IN / Y must read as zero
+  DRZG_CUDA(cudaMemsetAsync(Bg_.p, 0, Bg_.n, st_));
+  DRZG_CUDA(cudaMemsetAsync(Y_.p, 0, Y_.n, st_));
+  DRZG_CUDA(cudaMemsetAsync(IN_.p, 0, IN_.n, st_));
+}
+
+void ReductionEngine::step(int B, int y) {
+  const RuvTables& T = *T_;
+  ensure_batch(std::min(B, 1 << 30));
+  for (int b0 = 0; b0 < B; b0 += bcap_) {
+    int nb = std::min(bcap_, B - b0);
+    dev::StepArgs a;
+    a.C = C_.p;
+    a.jp_ptr = jp_ptr_.p;
+    a.jp_col = jp_col_.p;
+    a.jp_val = jp_val_.p;
+    a.gidx = gidx_.p;
+    a.dirs = dirs_.p;
+    a.t_ptr = t_ptr_.p;
+    a.t_src = t_src_.p;
+    a.sol_i = sol_i_.p;
+    a.sol_mu = sol_mu_.p;
+    a.nv = T.nv;
+    a.nL = T.nL;
+    a.nLp = nLp_;
+    a.side = T.side;
+    a.sidep = sidep_;
+    a.Ld = T.dp.Ld;
+    a.q = T.dp.q;
+    a.pool = pool_;
+    a.slot_stride = slot_stride_;
+    a.slot = d_slot_.p + b0;
+    a.vdir = d_vdir_.p + b0;
+    a.u0 = d_u0_.p + (size_t)b0 * T.nv;
+    a.y = y;
+    a.B = nb;
+    a.Bg = Bg_.p;
+    a.IN = IN_.p;
+    a.Cy = Cy_.p;
+    a.Y = Y_.p;
+    dim3 gL((T.nL + 127) / 128, nb);
+    timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 128, 0, st_>>>(a); });
+    dim3 gG(nLp_ / 64, (nb + 63) / 64);
+    for (int k = 0; k < T.dp.Ld; ++k) {
+      timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });
+      ++clock.gemm_launches;
+      clock.gemm_macs += (double)T.nL * T.nL * nb;
+      timed(&clock.carry_ms, [&] { dev::dixon_carry_kernel<<<gL, 128, 0, st_>>>(a, k); });
+    }
+    dim3 gS((T.side + 127) / 128, nb);
+    timed(&clock.epi_ms, [&] { dev::epilogue_kernel<<<gS, 128, 0, st_>>>(a); });
+    DRZG_CUDA(cudaGetLastError());
+  }
+}
+
+void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led) {
+  const RuvTables& T = *T_;
+  const int nv = T.nv, Ld = T.dp.Ld, ncol = (int)cols.size();
+  // key packing for combine_states' (u, pole) identity, per column
+  i64 maxpole = 0;
+  size_t total_seeds = 0;
+  std::vector<int> top0(ncol, 0);
+  for (int c = 0; c < ncol; ++c) {
+    if (!cols[c].by_pole.empty()) top0[c] = cols[c].by_pole.rbegin()->first;
+    maxpole = std::max<i64>(maxpole, top0[c]);
+    for (auto& kv : cols[c].by_pole) total_seeds += kv.second.size();
+  }
+  int bits = 1;
+  while (((i64)1 << bits) <= (i64)T.d * maxpole + 1) ++bits;
+  int colbits = 1;
+  while ((1 << colbits) < ncol) ++colbits;
+  DRZG_REQUIRE(nv * bits + colbits <= 64, "engine: state key does not fit 64 bits");
+  auto key = [&](int c, const Expo& u) { return ((u64)c << (nv * bits)) | u.pack(bits); };
+
+  DevBuf<long long> dG;
+  dG.alloc((size_t)ncol * Ld * gsize_);
+  DRZG_CUDA(cudaMemsetAsync(dG.p, 0, dG.n * sizeof(long long), st_));
+  DevBuf<int> d_err;
+  d_err.alloc(1);
+  DRZG_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int), st_));
+  if (cap_ == 0) grow_pool((int)std::min<size_t>(std::max<size_t>(total_seeds / 4, 1024), 1 << 20));
+
+  std::map<int, std::vector<HS>, std::greater<int>> landed;
+  std::vector<std::unordered_set<u64>> floor_keys(ncol);
+  std::vector<i64> floor_arrivals(ncol, 0);
+  std::vector<std::map<int, SeedBucket>::reverse_iterator> sit(ncol);
+  for (int c = 0; c < ncol; ++c) sit[c] = cols[c].by_pole.rbegin();
+
+  DevBuf<int> d_a, d_b, d_c;
+  DevBuf<int8_t> d_dig;
+  for (;;) {
+    int P = -1;
+    if (!landed.empty()) P = landed.begin()->first;
+    for (int c = 0; c < ncol; ++c)
+      if (sit[c] != cols[c].by_pole.rend()) P = std::max(P, sit[c]->first);
+    if (P <= n_) break;
+    std::vector<HS> front;
+    if (!landed.empty() && landed.begin()->first == P) {
+      front = std::move(landed.begin()->second);
+      landed.erase(landed.begin());
+    }
+    // materialise the seeds whose pole is P
+    {
+      std::vector<int> ss, sg;
+      std::vector<int8_t> sd;
+      for (int c = 0; c < ncol; ++c) {
+        if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
+        SeedBucket& bk = sit[c]->second;
+        for (size_t i = 0; i < bk.size(); ++i) {
+          HS h;
+          h.col = c;
+          h.u = Expo(nv);
+          for (int j = 0; j < nv; ++j) h.u[j] = bk.u[i * nv + j];
+          h.pole = P;
+          h.slot = alloc_slot();
+          front.push_back(h);
+          ss.push_back(h.slot);
+          sg.push_back(bk.g[i]);
+        }
+        sd.insert(sd.end(), bk.dig.begin(), bk.dig.end());
+        SeedBucket().u.swap(bk.u);  // release host memory
+        ++sit[c];
+      }
+      if (!ss.empty()) {
+        d_a.upload(ss, st_);
+        d_b.upload(sg, st_);
+        d_dig.upload(sd, st_);
+        timed(&clock.other_ms, [&] {
+          dev::seed_kernel<<<(int)ss.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_dig.p,
+                                                            (int)ss.size());
+        });
+      }
+    }
+    // combine_states: merge equal (col, u) except in a column's first sweep
+    {
+      std::unordered_map<u64, int> first;
+      first.reserve(front.size() * 2);
+      std::vector<HS> keep;
+      keep.reserve(front.size());
+      std::vector<std::vector<int>> extra;  // per kept index: merged slots
+      std::vector<int> gidx_of;
+      for (auto& h : front) {
+        if (top0[h.col] == P) {
+          keep.push_back(h);
+          continue;
+        }
+        u64 k = key(h.col, h.u);
+        auto it = first.find(k);
+        if (it == first.end()) {
+          first.emplace(k, (int)keep.size());
+          keep.push_back(h);
+        } else {
+          int dst = it->second;
+          if ((int)gidx_of.size() <= dst) gidx_of.resize(keep.size(), -1);
+          if (gidx_of[dst] < 0) {
+            gidx_of[dst] = (int)extra.size();
+            extra.push_back({keep[dst].slot});
+          }
+          extra[gidx_of[dst]].push_back(h.slot);
+        }
+      }
+      if (!extra.empty()) {
+        std::vector<int> gptr{0}, mem;
+        for (auto& g : extra) {
+          mem.insert(mem.end(), g.begin(), g.end());
+          gptr.push_back((int)mem.size());
+          led.combines += (i64)g.size() - 1;
+        }
+        d_a.upload(gptr, st_);
+        d_b.upload(mem, st_);
+        dim3 gm((T.side + 127) / 128, (int)extra.size());
+        timed(&clock.other_ms, [&] {
+          dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_a.p, d_b.p);
+        });
+        for (auto& g : extra)
+          for (size_t i = 1; i < g.size(); ++i) free_slot(g[i]);
+      }
+      front.swap(keep);
+    }
+    // moves (reduction.hpp:486-496), longest chunks first
+    std::vector<int> vd(front.size());
+    std::vector<i64> kk(front.size());
+    for (size_t i = 0; i < front.size(); ++i) {
+      Expo v;
+      i64 k;
+      pchunk_move(T.d, n_, (i64)p_, front[i].u, front[i].pole, T.S, &v, &k);
+      DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
+      DRZG_REQUIRE(legal(T.d, front[i].u, v, k, T.S), "reduce_chunk: illegal move");
+      vd[i] = (int)rank_of(v);
+      kk[i] = k;
+    }
+    std::vector<int> order(front.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return kk[a] > kk[b]; });
+    std::vector<int> hslot, hvdir, hu0;
+    for (int i : order) {
+      hslot.push_back(front[i].slot);
+      hvdir.push_back(vd[i]);
+      for (int j = 0; j < nv; ++j) hu0.push_back(front[i].u[j]);
+    }
+    d_slot_.upload(hslot, st_);
+    d_vdir_.upload(hvdir, st_);
+    d_u0_.upload(hu0, st_);
+    i64 kmax = front.empty() ? 0 : kk[order[0]];
+    int B = (int)front.size();
+    for (i64 y = 1; y <= kmax; ++y) {
+      while (B > 0 && kk[order[B - 1]] < y) --B;
+      step(B, (int)y);
+      led.matvecs += B;
+    }
+    led.startups += (i64)front.size();
+    // land every state at pole P - k
+    std::vector<int> fs, fc, fu;
+    for (int i : order) {
+      HS h = front[i];
+      const Expo& v = dirs_host_[vd[i]];
+      for (int j = 0; j < nv; ++j) h.u[j] -= (int)(kk[i] * v[j]);
+      h.pole -= (int)kk[i];
+      if (h.pole == n_) {
+        fs.push_back(h.slot);
+        fc.push_back(h.col);
+        for (int j = 0; j < nv; ++j) fu.push_back(h.u[j]);
+        floor_arrivals[h.col]++;
+        floor_keys[h.col].insert(key(h.col, h.u));
+      } else {
+        landed[h.pole].push_back(h);
+      }
+    }
+    if (!fs.empty()) {
+      d_a.upload(fs, st_);
+      d_b.upload(fc, st_);
+      d_c.upload(fu, st_);
+      dim3 gf((T.side + 127) / 128, (int)fs.size());
+      timed(&clock.other_ms, [&] {
+        dev::floor_kernel<<<gf, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, nv, d_a.p, d_b.p, d_c.p,
+                                               mon_.p, btab_.p, dG.p, gsize_, d_err.p);
+      });
+      for (int s : fs) free_slot(s);
+    }
+  }
+  for (int c = 0; c < ncol; ++c) led.combines += floor_arrivals[c] - (i64)floor_keys[c].size();
+  std::vector<long long> hG(dG.n);
+  DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
+  DRZG_CUDA(cudaStreamSynchronize(st_));
+  DRZG_CUDA(cudaGetLastError());
+  G.assign(ncol, {});
+  for (int c = 0; c < ncol; ++c)
+    G[c].assign(hG.begin() + (size_t)c * Ld * gsize_, hG.begin() + (size_t)(c + 1) * Ld * gsize_);
+}
+
+void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<int>& vdir, const std::vector<i64>& k,
+                                  std::vector<i8>& w_digits, Ledger& led) {
+  const RuvTables& T = *T_;
+  const int nv = T.nv, Ld = T.dp.Ld, B = (int)u.size();
+  DRZG_REQUIRE(w_digits.size() == (size_t)B * Ld * T.side, "chunk_batch: digit array size");
+  while ((int)free_.size() < B) grow_pool(cap_ + B);
+  std::vector<int> slots(B);
+  for (int i = 0; i < B; ++i) slots[i] = alloc_slot();
+  // upload digits slot by slot (pitch sidep)
+  std::vector<int8_t> stage((size_t)slot_stride_, 0);
+  for (int i = 0; i < B; ++i) {
+    std::fill(stage.begin(), stage.end(), 0);
+    for (int t = 0; t < Ld; ++t)
+      for (int g = 0; g < T.side; ++g) stage[(size_t)t * sidep_ + g] = w_digits[((size_t)i * Ld + t) * T.side + g];
+    DRZG_CUDA(cudaMemcpy(pool_ + (size_t)slots[i] * slot_stride_, stage.data(), stage.size(), cudaMemcpyHostToDevice));
+  }
+  std::vector<int> order(B);
+  for (int i = 0; i < B; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return k[a] > k[b]; });
+  std::vector<int> hslot, hvdir, hu0;
+  for (int i : order) {
+    DRZG_REQUIRE(k[i] >= 1, "reduce_chunk: empty chunk");
+    DRZG_REQUIRE(legal(T.d, u[i], dirs_host_[vdir[i]], k[i], T.S), "reduce_chunk: illegal move");
+    hslot.push_back(slots[i]);
+    hvdir.push_back(vdir[i]);
+    for (int j = 0; j < nv; ++j) hu0.push_back(u[i][j]);
+  }
+  d_slot_.upload(hslot, st_);
+  d_vdir_.upload(hvdir, st_);
+  d_u0_.upload(hu0, st_);
+  int Bc = B;
+  i64 kmax = B ? k[order[0]] : 0;
+  for (i64 y = 1; y <= kmax; ++y) {
+    while (Bc > 0 && k[order[Bc - 1]] < y) --Bc;
+    step(Bc, (int)y);
+    led.matvecs += Bc;
+  }
+  led.startups += B;
+  for (int i = 0; i < B; ++i) {
+    DRZG_CUDA(cudaMemcpyAsync(stage.data(), pool_ + (size_t)slots[i] * slot_stride_, stage.size(),
+                              cudaMemcpyDeviceToHost, st_));
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    for (int t = 0; t < Ld; ++t)
+      for (int g = 0; g < T.side; ++g) w_digits[((size_t)i * Ld + t) * T.side + g] = stage[(size_t)t * sidep_ + g];
+    free_slot(slots[i]);
+  }
+}
+
+}  // namespace drzg

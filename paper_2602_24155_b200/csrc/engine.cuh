@@ -1,0 +1,121 @@
+// Device-resident reduction engine: state vectors live in an HBM slot pool,
+// the host-side reduction policy (reference run_policy, reduction.hpp:464-533)
+// chooses every move from (u, pole) alone, and each pole drop of a whole
+// sweep runs as one batched Dixon step on the device.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "host/final.hpp"
+namespace drzg { namespace dev { constexpr int kLdMax = 32; } }
+
+namespace drzg {
+
+#define DRZG_CUDA(x)                                                                          \
+  do {                                                                                        \
+    cudaError_t err_ = (x);                                                                   \
+    if (err_ != cudaSuccess)                                                                  \
+      throw ::drzg::contract_error(std::string("CUDA: ") + cudaGetErrorString(err_), __FILE__, \
+                                   __LINE__);                                                 \
+  } while (0)
+
+enum class Policy { p_chunk = 0, depth_first = 1, var_by_var = 2 };
+
+struct Ledger {
+  i64 matvecs = 0, startups = 0, combines = 0;
+};
+
+// kernel-time accounting for the roofline report
+struct KernelClock {
+  bool on = false;
+  double gemm_ms = 0, carry_ms = 0, gather_ms = 0, epi_ms = 0, other_ms = 0;
+  i64 gemm_launches = 0;
+  double gemm_macs = 0;  // algorithmic int8 MACs issued (nL x nL per state-digit)
+};
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t count) {
+    if (count <= n) return;
+    if (p) DRZG_CUDA(cudaFree(p));
+    p = nullptr;
+    DRZG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    n = count;
+  }
+  void upload(const std::vector<T>& v, cudaStream_t st) {
+    alloc(v.size());
+    if (!v.empty()) DRZG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+};
+
+class ReductionEngine {
+ public:
+  ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t st);
+  ~ReductionEngine();
+
+  // p-chunk policy over a group of columns; returns per column the floor
+  // numerator as Ld digit-sum planes over Homog_{dn-n-1}
+  void run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led);
+
+  // one chunk (k pole drops along v) for a batch of states supplied as
+  // digit planes (reference reduce_chunk, reduction.hpp:394-423)
+  void chunk_batch(const std::vector<Expo>& u, const std::vector<int>& vdir, const std::vector<i64>& k,
+                   std::vector<i8>& w_digits, Ledger& led);
+
+  KernelClock clock;
+  int floor_size() const { return gsize_; }
+  const RuvTables& tables() const { return *T_; }
+
+ private:
+  struct HS {
+    int col;
+    Expo u;
+    int pole;
+    int slot;
+  };
+  int alloc_slot();
+  void free_slot(int s) { free_.push_back(s); }
+  void grow_pool(int need);
+  void ensure_batch(int B);
+  // one pole drop for states [0, B) of the current sweep arrays
+  void step(int B, int y);
+  void timed(double* acc, const std::function<void()>& f);
+
+  const RuvTables* T_;
+  int n_;
+  u64 p_;
+  cudaStream_t st_;
+  int nLp_ = 0, sidep_ = 0, gsize_ = 0;
+  long long slot_stride_ = 0;
+  // tables
+  DevBuf<int8_t> C_;
+  DevBuf<int> jp_ptr_, jp_col_, jp_val_, gidx_, dirs_, t_ptr_, t_src_, sol_i_, sol_mu_, mon_;
+  DevBuf<unsigned long long> btab_;
+  // pool
+  int8_t* pool_ = nullptr;
+  int cap_ = 0;
+  std::vector<int> free_;
+  // sweep arrays
+  DevBuf<int> d_slot_, d_vdir_, d_u0_;
+  // temporaries
+  int bcap_ = 0;
+  DevBuf<int8_t> Bg_, IN_, Y_;
+  DevBuf<int> Cy_;
+  cudaEvent_t ev0_, ev1_;
+  std::vector<Expo> dirs_host_;
+};
+
+}  // namespace drzg

@@ -1,0 +1,94 @@
+// drzg: B200-native controlled-reduction engine (arXiv 2602.24155).
+// Shared integer types and the always-on contract check.  Mirrors the
+// reference's convention (common.hpp:19-27): a violated precondition throws
+// an exception carrying file:line; the C-ABI layer turns it into a status
+// code plus a thread-local message.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace drzg {
+
+using u8 = std::uint8_t;
+using i8 = std::int8_t;
+using u32 = std::uint32_t;
+using i32 = std::int32_t;
+using u64 = std::uint64_t;
+using i64 = std::int64_t;
+using u128 = unsigned __int128;
+using i128 = __int128;
+
+struct contract_error : std::logic_error {
+  contract_error(const std::string& msg, const char* file, int line)
+      : std::logic_error(std::string(file) + ":" + std::to_string(line) + ": " + msg) {}
+};
+
+// run_zeta's two non-contract failures (reference zeta.hpp:17-22)
+struct singular_input : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct escalation_exhausted : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define DRZG_REQUIRE(cond, msg)                                            \
+  do {                                                                     \
+    if (!(cond)) throw ::drzg::contract_error((msg), __FILE__, __LINE__);  \
+  } while (0)
+
+constexpr int kMaxVars = 6;
+
+// --- word arithmetic mod m (m < 2^63 unless noted) ---------------------------
+inline u64 addm(u64 a, u64 b, u64 m) {
+  u64 s = a + b;
+  return s >= m ? s - m : s;
+}
+inline u64 subm(u64 a, u64 b, u64 m) { return a >= b ? a - b : a + m - b; }
+inline u64 mulm(u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); }
+inline u64 powm(u64 a, u64 e, u64 m) {
+  u64 r = 1 % m;
+  a %= m;
+  for (; e; e >>= 1) {
+    if (e & 1) r = mulm(r, a, m);
+    a = mulm(a, a, m);
+  }
+  return r;
+}
+// inverse of a unit mod m (m need not be prime)
+inline u64 invm(u64 a, u64 m) {
+  i64 t = 0, nt = 1, r = (i64)m, nr = (i64)(a % m);
+  while (nr) {
+    i64 q = r / nr;
+    i64 tmp = t - q * nt;
+    t = nt;
+    nt = tmp;
+    tmp = r - q * nr;
+    r = nr;
+    nr = tmp;
+  }
+  DRZG_REQUIRE(r == 1, "invm: not a unit");
+  return (u64)(t < 0 ? t + (i64)m : t);
+}
+inline u64 ipow(u64 p, int e) {
+  u64 r = 1;
+  for (int i = 0; i < e; ++i) {
+    DRZG_REQUIRE(r <= ~u64(0) / p, "ipow overflow");
+    r *= p;
+  }
+  return r;
+}
+
+// 128-bit residues: values below 2^80 multiply exactly by splitting b
+inline u128 mulm128(u128 a, u128 b, u128 m) {
+  DRZG_REQUIRE((m >> 80) == 0, "mulm128: modulus above 2^80");
+  a %= m;
+  b %= m;
+  u128 hi = b >> 40, lo = b & ((u128(1) << 40) - 1);
+  u128 r = (a * hi) % m;
+  r = ((r << 40) + a * lo) % m;
+  return r;
+}
+
+}  // namespace drzg

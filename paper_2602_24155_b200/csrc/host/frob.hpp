@@ -1,0 +1,169 @@
+// Frobenius expansion of one basis column into compact seeds.
+//
+// Follows reference frobenius.hpp:121-144 (terms: exponent p(beta+alpha+1)-1,
+// pole p(m+j), scalar D_{j,m} C_{j,alpha} mod p^{s_m}), zeta.hpp:56-69 (kappa_P
+// prescale) and reduction.hpp:538-563 (seed: u = tweak(E+1, dn-n) made
+// S-honest, one-hot vector at rank(E+1-u) carrying dc * kappa_P mod p^M).
+// Seeds stay compact (exponent, one index, Ld digits) until the sweep that
+// activates their pole materialises them on the device.
+#pragma once
+
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "tables.hpp"
+
+namespace drzg {
+
+// residue arithmetic mod p^M on the host: u128 while p^M < 2^80, else GMP
+struct HostMod {
+  u64 p = 0;
+  int M = 0;
+  bool wide = false;  // true -> GMP
+  u128 m128 = 0;
+  Z mz;
+  static HostMod make(u64 p, int M) {
+    HostMod h;
+    h.p = p;
+    h.M = M;
+    h.mz = Z::pow(p, (u64)M);
+    h.wide = h.mz >= (Z(1) << 80);
+    if (!h.wide) h.m128 = h.mz.to_u128();
+    return h;
+  }
+};
+
+// balanced base-q digits of a residue (least significant first); the carry
+// out of the top digit is a multiple of q^Ld, which p^M divides
+inline void to_digits_u128(u128 v, const DigitPlan& dp, i8* out) {
+  // v < 2^127 non-negative
+  for (int t = 0; t < dp.Ld; ++t) {
+    int r = (int)(v % (u128)dp.q);
+    if (r > dp.q / 2) r -= dp.q;
+    out[t] = (i8)r;
+    v = (v - (u128)(i128)r) / (u128)dp.q;  // exact; r may be negative
+  }
+}
+inline void to_digits_z(const Z& v0, const DigitPlan& dp, i8* out) {
+  Z v = v0, q((long)dp.q);
+  for (int t = 0; t < dp.Ld; ++t) {
+    Z r = v.mod(q);
+    long ri = r.to_long();
+    if (ri > dp.q / 2) ri -= dp.q;
+    out[t] = (i8)ri;
+    v = (v - Z(ri)).divexact(q);
+  }
+}
+// sum_t q^t s_t mod p^M for arbitrary (int64) digit sums
+inline Z from_digit_sums(const i64* s, const DigitPlan& dp, const Z& mod) {
+  Z acc(0), q((long)dp.q);
+  for (int t = dp.Ld - 1; t >= 0; --t) acc = acc * q + Z((long)s[t]);
+  return acc.mod(mod);
+}
+
+struct SeedBucket {
+  std::vector<i32> u;     // nv per seed
+  std::vector<i32> g;     // side index of the one-hot entry
+  std::vector<i8> dig;    // Ld per seed
+  size_t size() const { return g.size(); }
+};
+
+struct ColumnSeeds {
+  int col = 0, m = 0;
+  i64 Pmax = 0;
+  i64 nterms = 0;
+  std::map<int, SeedBucket> by_pole;  // pole -> seeds
+};
+
+// f^0..f^{N-1} mod p^s, cached per (N, s) for one hypersurface
+struct PowerCache {
+  std::mutex mu;
+  std::map<std::pair<int, int>, std::vector<HPoly>> cache;
+  const std::vector<HPoly>& get(const Hypersurface& X, int N, int s) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(N, s);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    Z smod = Z::pow(X.p, (u64)s);
+    DRZG_REQUIRE(smod < (Z(1) << 96), "power series modulus above 2^96");
+    u128 m = smod.to_u128();
+    std::vector<HPoly> out;
+    HPoly one(X.nv(), 0);
+    one.c[0] = 1;
+    out.push_back(one);
+    HPoly fr = X.f;
+    for (auto& c : fr.c) c %= m;
+    for (int j = 1; j < N; ++j) out.push_back(poly_mul_small(out.back(), fr, m));
+    return cache.emplace(key, std::move(out)).first->second;
+  }
+};
+
+inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan,
+                                 const RuvTables& T, const HostMod& hm, PowerCache& pc, int col) {
+  ColumnSeeds out;
+  out.col = col;
+  int m = B.pole_of[col];
+  out.m = m;
+  const u64 p = X.p;
+  const int nv = X.nv();
+  int N = plan.N_m[m], s = plan.s_m[m];
+  Z smodz = Z::pow(p, (u64)s);
+  u128 smod = smodz.to_u128();
+  out.Pmax = plan.max_pole(m);
+  // D_{j,m} = (-1)^j sum_{i=j}^{N-1} C(m+i-1, i) C(i, j) mod p^s (modarith.hpp:143-182)
+  std::vector<u128> Dj(N);
+  for (int j = 0; j < N; ++j) {
+    Z acc(0);
+    for (int i = j; i < N; ++i) acc += Z::binom(m + i - 1, i) * Z::binom(i, j);
+    if (j & 1) acc = -acc;
+    Dj[j] = acc.mod(smodz).to_u128();
+  }
+  // kappa_P = prod_{t=P}^{Pmax-1} t mod p^M at poles P = p*k, k >= m (zeta.hpp:56-64)
+  std::map<int, Z> kappa;
+  kappa[(int)out.Pmax] = Z(1);
+  {
+    Z cur(1);
+    for (i64 t = out.Pmax - 1; t >= (i64)p * m; --t) {
+      cur = (cur * Z((long)t)).mod(hm.mz);
+      if (t % (i64)p == 0 && t / (i64)p >= m) kappa[(int)t] = cur;
+    }
+  }
+  const auto& powers = pc.get(X, N, s);
+  const Expo one = Expo::ones(nv);
+  const Expo& beta = B.mons[col];
+  const DigitPlan& dp = T.dp;
+  for (int j = 0; j < N; ++j) {
+    if (Dj[j] == 0) continue;
+    int P = (int)p * (m + j);
+    const Z& kap = kappa.at(P);
+    u128 kap128 = hm.wide ? 0 : kap.to_u128();
+    SeedBucket& bk = out.by_pole[P];
+    const HPoly& fj = powers[j];
+    const auto& tab = fj.table();
+    for (int a = 0; a < fj.size(); ++a) {
+      if (!fj.c[a]) continue;
+      u128 dc = mulm128(Dj[j], fj.c[a], smod);
+      if (dc == 0) continue;
+      ++out.nterms;
+      Expo full = beta + tab.mons[a] + one;
+      for (int i = 0; i < nv; ++i) full[i] *= (int)p;  // E + 1
+      Expo u;
+      DRZG_REQUIRE(seed_u(full, T.D, T.S, &u), "seed: cannot honor the working set");
+      Expo wm = full - u;
+      DRZG_REQUIRE(wm.nonneg() && wm.total() == T.D, "seed: bad split");
+      for (int i = 0; i < nv; ++i) bk.u.push_back(u[i]);
+      bk.g.push_back((i32)rank_of(wm));
+      size_t off = bk.dig.size();
+      bk.dig.resize(off + dp.Ld);
+      if (!hm.wide) {
+        to_digits_u128(mulm128(dc, kap128, hm.m128), dp, bk.dig.data() + off);
+      } else {
+        to_digits_z((Z::from_u128(dc) * kap).mod(hm.mz), dp, bk.dig.data() + off);
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace drzg

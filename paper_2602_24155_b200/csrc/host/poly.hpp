@@ -1,0 +1,76 @@
+// Dense homogeneous polynomials over Z/m, indexed by grevlex position.
+// Host-side setup only (Jacobian generators, power series f^j for the
+// Frobenius expansion, reference homog.hpp:21-142).
+#pragma once
+
+#include <vector>
+
+#include "mono.hpp"
+
+namespace drzg {
+
+struct HPoly {
+  int nv = 0, deg = 0;
+  std::vector<u128> c;  // parallel to monos(nv, deg).mons
+
+  HPoly() = default;
+  HPoly(int nvars, int degree) : nv(nvars), deg(degree), c((size_t)mono_count(nvars, degree), 0) {}
+  const MonoList& table() const { return monos(nv, deg); }
+  int size() const { return (int)c.size(); }
+  bool is_zero() const {
+    for (auto x : c)
+      if (x) return false;
+    return true;
+  }
+  struct Term {
+    u128 c;
+    Expo e;
+  };
+  std::vector<Term> terms() const {
+    std::vector<Term> out;
+    const auto& t = table();
+    for (int i = 0; i < size(); ++i)
+      if (c[i]) out.push_back({c[i], t.mons[i]});
+    return out;
+  }
+};
+
+// product reduced mod m (m < 2^100 and the second factor's coefficients
+// small enough that one row of partial products fits 128 bits)
+inline HPoly poly_mul_small(const HPoly& a, const HPoly& f, u128 m) {
+  HPoly r(a.nv, a.deg + f.deg);
+  auto ft = f.terms();
+  const auto& ta = a.table();
+  // accumulate per target without reduction: |f terms| * m * max|f coeff| < 2^128
+  std::vector<u128> acc(r.c.size(), 0);
+  for (int i = 0; i < a.size(); ++i) {
+    if (!a.c[i]) continue;
+    for (const auto& t : ft) acc[(size_t)rank_of(ta.mons[i] + t.e)] += a.c[i] * t.c;
+  }
+  for (size_t i = 0; i < acc.size(); ++i) r.c[i] = acc[i] % m;
+  return r;
+}
+
+inline HPoly poly_partial(const HPoly& f, int i) {
+  DRZG_REQUIRE(f.deg >= 1, "partial: constant input");
+  HPoly r(f.nv, f.deg - 1);
+  const auto& tf = f.table();
+  for (int k = 0; k < f.size(); ++k) {
+    if (!f.c[k] || tf.mons[k][i] == 0) continue;
+    Expo e = tf.mons[k];
+    int ei = e[i];
+    e[i] -= 1;
+    r.c[(size_t)rank_of(e)] += (u128)ei * f.c[k];
+  }
+  return r;
+}
+
+inline HPoly poly_shift(const HPoly& f, const Expo& s) {
+  HPoly r(f.nv, f.deg + s.total());
+  const auto& tf = f.table();
+  for (int k = 0; k < f.size(); ++k)
+    if (f.c[k]) r.c[(size_t)rank_of(tf.mons[k] + s)] = f.c[k];
+  return r;
+}
+
+}  // namespace drzg

@@ -1,0 +1,214 @@
+// Frobenius assembly + zeta driver (see pipeline.cuh).
+#include <chrono>
+
+#include "pipeline.cuh"
+
+namespace drzg {
+
+namespace {
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+std::set<int> working_set_for(const Hypersurface& X, Policy pol) {
+  if (pol == Policy::var_by_var) return {X.n};
+  return default_S(X.n, X.d);
+}
+
+FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan, const std::set<int>& S,
+                            const FrobOptions& opt, int device) {
+  DRZG_REQUIRE(opt.policy == Policy::p_chunk, "device engine: only the p-chunk policy is implemented");
+  double t0 = now_s();
+  DRZG_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  DRZG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  FrobResult out;
+  const int n = X.n;
+  const u64 p = X.p;
+  out.b = B.b;
+  out.F.assign((size_t)B.b * B.b, Z(0));
+  out.M = plan.M;
+
+  RuvTables T = build_tables(X, plan.M, S);
+  out.Ld = T.dp.Ld;
+  out.q = T.dp.q;
+  out.nL = T.nL;
+  out.side = T.side;
+  HostMod hm = HostMod::make(p, plan.M);
+  double t1 = now_s();
+  out.t.tables = t1 - t0;
+
+  std::vector<int> cols;
+  for (int j = 0; j < (int)B.b; ++j) {
+    if (opt.only_pole && B.pole_of[j] != opt.only_pole) continue;
+    if (!opt.columns.empty() && std::find(opt.columns.begin(), opt.columns.end(), j) == opt.columns.end()) continue;
+    cols.push_back(j);
+  }
+  out.computed = cols;
+  PowerCache pc;
+  std::vector<ColumnSeeds> seeds;
+  for (int j : cols) {
+    seeds.push_back(expand_column(X, B, plan, T, hm, pc, j));
+    out.terms += seeds.back().nterms;
+  }
+  double t2 = now_s();
+  out.t.seeds = t2 - t1;
+
+  std::vector<std::vector<i64>> G;
+  {
+    ReductionEngine eng(T, n, p, st);
+    eng.clock.on = opt.profile;
+    if (!seeds.empty()) eng.run_pchunk(seeds, G, out.led);
+    out.clk = eng.clock;
+  }
+  double t3 = now_s();
+  out.t.device = t3 - t2;
+
+  FinalReducer fin(X, B, T.dp, hm);
+  const int gsize = (int)mono_count(X.nv(), T.D - 1);
+  for (size_t ci = 0; ci < cols.size(); ++ci) {
+    int j = cols[ci];
+    int m = B.pole_of[j];
+    i64 Pmax = plan.max_pole(m);
+    std::vector<Z> g(gsize);
+    for (int r = 0; r < gsize; ++r) {
+      i64 s[dev::kLdMax];
+      for (int t = 0; t < T.dp.Ld; ++t) s[t] = G[ci][(size_t)t * gsize + r];
+      g[r] = from_digit_sums(s, T.dp, hm.mz);
+    }
+    std::vector<Z> c = fin.reduce(std::move(g), n);
+    // unscale by the unit of kappa_n = (Pmax-1)!/(n-1)! and the Mazur shift
+    // (zeta.hpp:79-106)
+    i64 v = factorial_valuation((u64)(Pmax - 1), p);
+    Z unit(1);
+    for (i64 t = n; t < Pmax; ++t) unit *= Z((long)t);
+    Z pz = Z::from_u64(p);
+    for (i64 t = 0; t < v; ++t) {
+      DRZG_REQUIRE(unit.divisible_by(p), "kappa: bad valuation");
+      unit = unit.divexact(pz);
+    }
+    Z iu = unit.mod(hm.mz).inverse_mod(hm.mz);
+    i64 req = std::min<i64>(std::max<i64>(v - m + 1, 0), plan.M);
+    Z preq = Z::pow(p, (u64)req);
+    i64 shift = (i64)(n - 1) - v;
+    Z pshift = Z::pow(p, (u64)(shift < 0 ? -shift : shift));
+    for (int i = 0; i < (int)B.b; ++i) {
+      Z Zi = (c[i] * iu).mod(hm.mz);
+      DRZG_REQUIRE(Zi.divisible_by(preq), "column fails the p-divisibility floor of its pole order");
+      Z& Fij = out.F[(size_t)i * B.b + j];
+      if (shift >= 0) {
+        Fij = Zi * pshift;
+      } else {
+        DRZG_REQUIRE(Zi.divisible_by(pshift), "column entry not integral after unscaling");
+        Fij = Zi.divexact(pshift);
+      }
+    }
+  }
+  double t4 = now_s();
+  out.t.final = t4 - t3;
+  out.t.total = t4 - t0;
+  DRZG_CUDA(cudaStreamDestroy(st));
+  return out;
+}
+
+ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
+  double t0 = now_s();
+  if (!check_smooth(X, full_set(X.nv())))
+    throw singular_input("hypersurface is singular (weighted Jacobian not surjective)");
+  std::set<int> S = working_set_for(X, opt.policy);
+  if (!check_smooth(X, S)) throw std::runtime_error("input not smooth for the requested working set");
+  Basis B = compute_basis(X);
+  PrecisionPlan plan = choose_precision(X.p, X.n, X.d, opt.overrides);
+  ZetaOut res;
+  res.hodge = hodge_numbers(X.n, X.d);
+  for (;;) {
+    FrobOptions fo;
+    fo.policy = opt.policy;
+    fo.overrides = opt.overrides;
+    fo.profile = opt.profile;
+    FrobResult fr = frobenius_matrix(X, B, plan, S, fo, device);
+    res.led = fr.led;
+    Z cp_mod = Z::pow(X.p, (u64)(plan.M + X.n));
+    std::vector<Z> dres = berkowitz(fr.F, (int)fr.b, cp_mod);
+    res.last = std::move(fr);
+    Recovered rec = recover_Q(dres, plan);
+    auto escalate_or_throw = [&](const std::string& why) {
+      if (!escalate_plan(plan)) throw escalation_exhausted("precision ladder exhausted: " + why);
+    };
+    if (rec.status == 2) {
+      escalate_or_throw(rec.reason);
+      continue;
+    }
+    auto cands = std::move(rec.candidates);
+    bool ambiguous = false;
+    if (cands.size() > 1) {
+      int rounds = 0;
+      for (int r = 1; r <= 3 && cands.size() > 1; ++r) {
+        Z pts(0);
+        for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
+        if (pts > Z((long)opt.count_budget)) break;
+        ++rounds;
+        Z truth((long)count_points(X, r, opt.count_budget));
+        std::vector<std::vector<Z>> kept;
+        for (auto& c : cands)
+          if (counts_from_zeta(c, X.p, X.n, r) == truth) kept.push_back(c);
+        if (kept.empty()) break;
+        cands = std::move(kept);
+      }
+      if (cands.empty() || (cands.size() > 1 && rounds > 0)) {
+        escalate_or_throw("sign of the functional equation undecided");
+        continue;
+      }
+      ambiguous = cands.size() > 1;
+    }
+    std::vector<Z> a = cands.front();
+    NewtonPolygon np = newton_polygon(a, X.p);
+    bool geom_ok = np.vertices.front() == std::make_pair<i64, i64>(0, 0);
+    i64 HP_end = hodge_polygon_at(res.hodge, X.n, plan.b);
+    geom_ok = geom_ok && np.vertices.back().first == plan.b && np.vertices.back().second == HP_end;
+    for (i64 x = 0; x <= plan.b && geom_ok; ++x)
+      if (np.value_at(x) < Q64::make(hodge_polygon_at(res.hodge, X.n, x), 1)) geom_ok = false;
+    if (!geom_ok) {
+      escalate_or_throw("Newton polygon escapes the Hodge bound");
+      continue;
+    }
+    std::vector<CountCheck> checks;
+    bool counts_ok = true;
+    if (opt.verify_counts && !ambiguous) {
+      for (int r = 1; r <= 2; ++r) {
+        Z pts(0);
+        for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
+        if (pts > Z((long)opt.count_budget)) break;
+        CountCheck ck;
+        ck.r = r;
+        ck.from_zeta = counts_from_zeta(a, X.p, X.n, r);
+        ck.from_count = Z((long)count_points(X, r, opt.count_budget));
+        ck.ok = ck.from_zeta == ck.from_count;
+        counts_ok = counts_ok && ck.ok;
+        checks.push_back(ck);
+      }
+    }
+    if (!counts_ok) {
+      escalate_or_throw("point counts disagree with the recovered zeta");
+      continue;
+    }
+    res.Q = a;
+    res.ambiguous = ambiguous;
+    if (ambiguous) res.Q_alt = cands.back();
+    res.np = np;
+    res.inv = classify(np, res.hodge, X.n, X.d);
+    res.domino = domino_number(np, res.hodge, X.n);
+    if (X.d <= X.nv()) {
+      res.inv.fsplit_defined = true;
+      res.inv.fsplit = fedder_is_fsplit(X);
+    }
+    res.counts = checks;
+    res.plan = plan;
+    break;
+  }
+  res.wall = now_s() - t0;
+  return res;
+}
+
+}  // namespace drzg
