@@ -83,6 +83,14 @@ char* drzg_frobenius(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, i
 char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
                 int32_t nm_override, int32_t verify_counts, int32_t device, int32_t profile);
 
+/* synthetic input by the reference CLI's generator rule (drzeta_main.cpp:112-122):
+ * std::mt19937_64(seed), coefficient rng() % p per grevlex monomial, redrawn
+ * until smooth for the full set and the policy's working set (run_zeta's two
+ * checks, zeta.hpp:440-445).  fermat != 0 returns sum x_i^d.  coeffs_out
+ * holds C(n+d, n) entries. */
+int drzg_random_hypersurface(uint64_t p, int32_t n, int32_t d, uint64_t seed, int32_t policy, int32_t fermat,
+                             uint64_t* coeffs_out, int32_t* tries_out);
+
 /* charpoly + recover_Q on a given F (zeta.hpp:456-470); F as b*b decimal strings */
 char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t nm_override, int32_t b,
                     const char* const* F);

@@ -386,6 +386,64 @@ char* ref_zeta(u64 p, int n, int d, const u64* coeffs, const char* policy, const
   });
 }
 
+// Bounded sample of the reference's own hot path for CPU-baseline timing:
+// the exact setup of frobenius_matrix (zeta.hpp:41-69: RuvContext, lazy PEP
+// store, frobenius_terms, kappa prescale, seeds) for column `col`, then the
+// reference run_policy (p-chunk) on `threads` disjoint groups of that
+// column's top-pole seeds (at most max_seeds per group), one std::thread per
+// group sharing the store exactly as the column workers do (zeta.hpp:109-133).
+// Reports wall seconds and the ledger of the sampled work.
+char* ref_policy_sample(u64 p, int n, int d, const u64* coeffs, int r_uniform, int nm_override, int col,
+                        int max_seeds, int threads) {
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    Hypersurface X = make_x(p, n, d, coeffs);
+    Basis B = compute_basis(X);
+    PrecisionPlan plan = choose_precision(p, n, d, overrides(r_uniform, nm_override));
+    StripePlan kp = StripePlan::make(p, plan.M);
+    std::set<int> S = default_S(n, d);
+    RuvContext C(X, kp, S);
+    auto store = make_pep_store("lazy", C);
+    ModulusContext mctx = ModulusContext::make(p, plan.M);
+    int m = B.pole_of[col];
+    i64 Pmax = plan.max_pole(m);
+    auto terms = frobenius_terms(X, B.mons[col], m, plan);
+    std::map<int, mpz_class> kappa;
+    kappa[(int)Pmax] = 1;
+    mpz_class cur = 1;
+    for (i64 t = Pmax - 1; t >= (i64)p * m; --t) {
+      cur = mod_reduce(cur * t, mctx.modulus);
+      if (t % (i64)p == 0 && t / (i64)p >= m) kappa[(int)t] = cur;
+    }
+    std::vector<std::vector<GameState>> groups(threads);
+    int g = 0;
+    for (const auto& t : terms) {
+      if (t.pole != (int)Pmax) continue;
+      if ((int)groups[g].size() < max_seeds) groups[g].push_back(seed_reduction_input(C, t, kappa.at(t.pole)));
+      g = (g + 1) % threads;
+    }
+    double setup = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<CostLedger> leds(threads);
+    auto t1 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int i = 0; i < threads; ++i)
+      pool.emplace_back([&, i] { run_policy(C, *store, std::move(groups[i]), Policy::p_chunk, leds[i]); });
+    for (auto& th : pool) th.join();
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+    CostLedger tot;
+    for (auto& l : leds) {
+      tot.matvecs += l.matvecs;
+      tot.startups += l.startups;
+      tot.combines += l.combines;
+    }
+    std::ostringstream os;
+    os << "{\"seconds\":" << secs << ",\"setup_seconds\":" << setup << ",\"matvecs\":" << tot.matvecs
+       << ",\"startups\":" << tot.startups << ",\"combines\":" << tot.combines << ",\"threads\":" << threads
+       << ",\"Pmax\":" << Pmax << "}";
+    return os.str();
+  });
+}
+
 // Berkowitz charpoly + recover_Q on a given F (zeta.hpp:456-470)
 char* ref_charpoly(u64 p, int n, int d, int r_uniform, int nm_override, int b, const char* const* F) {
   return guarded([&] {

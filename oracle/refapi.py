@@ -25,7 +25,7 @@ def lib():
             raise RuntimeError(f"{REF_SO} missing: run `make -C oracle` where /root/reference exists")
         L = ctypes.CDLL(REF_SO)
         for name in ("ref_mono_table", "ref_hypersurface", "ref_plan", "ref_basis", "ref_seeds",
-                     "ref_chunk", "ref_frobenius", "ref_zeta", "ref_charpoly"):
+                     "ref_chunk", "ref_frobenius", "ref_zeta", "ref_charpoly", "ref_policy_sample"):
             getattr(L, name).restype = ctypes.c_void_p
         _lib = L
     return _lib
@@ -168,3 +168,9 @@ def stripe_plan_py(p, M, capacity=1 << 126):
             continue
         return {"limbs": limbs, "limb_exp": e, "beta": beta, "stripe": min(capacity // (prod * limbs), 1 << 40)}
     raise ValueError("StripePlan: no viable limb split")
+
+
+def policy_sample(p, n, d, coeffs, col, max_seeds, threads, r_uniform=0, nm=0):
+    """reference run_policy on a bounded sample of one column's top-pole seeds"""
+    return _js(lib().ref_policy_sample(ctypes.c_uint64(p), n, d, _u64(coeffs), r_uniform, nm, col, max_seeds,
+                                       threads))

@@ -163,6 +163,17 @@ def zeta(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, verify_counts=Tru
                                  int(verify_counts), device, int(profile)))
 
 
+def random_hypersurface(p, n, d, seed=1, policy="p-chunk", fermat=False):
+    """reference generator rule (drzeta_main.cpp:112-122 + run_zeta's smoothness checks)"""
+    from math import comb
+    cnt = comb(n + d, n)
+    out = (ctypes.c_uint64 * cnt)()
+    tries = ctypes.c_int32(0)
+    _check(lib().drzg_random_hypersurface(ctypes.c_uint64(p), n, d, ctypes.c_uint64(seed), POLICIES[policy],
+                                          int(fermat), out, ctypes.byref(tries)))
+    return [int(x) for x in out]
+
+
 def charpoly(p, n, d, F, b, r_uniform=0, nm=0):
     """berkowitz_charpoly + recover_Q on a given F (zeta.hpp:456-470)"""
     arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F])

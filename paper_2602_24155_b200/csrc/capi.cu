@@ -1,6 +1,7 @@
 // The C ABI (include/drzg.h): marshalling between the reference's plain
 // layouts and the engine, exceptions -> status codes + thread-local message.
 #include <cstring>
+#include <random>
 #include <sstream>
 #include <string>
 
@@ -117,7 +118,9 @@ std::string frob_json_body(const FrobResult& fr) {
      << ",\"kernels\":{\"gemm_ms\":" << fr.clk.gemm_ms << ",\"carry_ms\":" << fr.clk.carry_ms
      << ",\"gather_ms\":" << fr.clk.gather_ms << ",\"epilogue_ms\":" << fr.clk.epi_ms
      << ",\"other_ms\":" << fr.clk.other_ms << ",\"gemm_launches\":" << fr.clk.gemm_launches
-     << ",\"gemm_macs\":" << fr.clk.gemm_macs << "}";
+     << ",\"gemm_macs\":" << fr.clk.gemm_macs << ",\"device_ms\":" << fr.clk.device_ms << "}"
+     << ",\"traffic\":{\"h2d_bytes\":" << g_traffic.h2d.load() << ",\"d2h_bytes\":" << g_traffic.d2h.load()
+     << ",\"launches\":" << g_traffic.launches.load() << "}";
   return os.str();
 }
 Policy policy_of(int p) {
@@ -285,6 +288,7 @@ char* drzg_frobenius(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, i
     fo.profile = profile != 0;
     if (columns)
       for (int i = 0; i < ncolumns; ++i) fo.columns.push_back(columns[i]);
+    g_traffic.reset();
     FrobResult fr = frobenius_matrix(X, B, plan, S, fo, device);
     std::vector<Z> dres;
     if (!only_pole && fo.columns.empty())
@@ -305,6 +309,7 @@ char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_
     zo.overrides = overrides(r_uniform, nm_override);
     zo.verify_counts = verify_counts != 0;
     zo.profile = profile != 0;
+    g_traffic.reset();
     ZetaOut r = run_zeta(X, zo, device);
     std::ostringstream os;
     os.precision(9);
@@ -321,6 +326,39 @@ char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_
          << (r.counts[i].ok ? "true" : "false") << "]";
     os << "],\"seconds\":" << r.wall << ",\"frobenius\":{" << frob_json_body(r.last) << "}}";
     return os.str();
+  });
+}
+
+int drzg_random_hypersurface(uint64_t p, int32_t n, int32_t d, uint64_t seed, int32_t policy, int32_t fermat,
+                              uint64_t* coeffs_out, int32_t* tries_out) {
+  return guard_int([&] {
+    const MonoList& tab = monos(n + 1, d);
+    std::mt19937_64 rng(seed);
+    int tries = 0;
+    for (;;) {
+      ++tries;
+      DRZG_REQUIRE(tries < 100000, "random_hypersurface: no smooth draw");
+      std::vector<u64> c(tab.size(), 0);
+      if (fermat) {
+        for (int i = 0; i <= n; ++i) {
+          Expo e(n + 1);
+          e[i] = d;
+          c[(size_t)rank_of(e)] = 1;
+        }
+      } else {
+        for (auto& x : c) x = rng() % p;
+      }
+      bool zero = true;
+      for (auto x : c) zero = zero && x == 0;
+      if (zero) continue;
+      Hypersurface X = Hypersurface::make(p, n, d, c);
+      bool ok = check_smooth(X, full_set(n + 1)) && check_smooth(X, working_set_for(X, policy_of(policy)));
+      DRZG_REQUIRE(ok || !fermat, "random_hypersurface: Fermat hypersurface not smooth");
+      if (!ok) continue;
+      std::copy(c.begin(), c.end(), coeffs_out);
+      if (tries_out) *tries_out = tries;
+      return;
+    }
   });
 }
 

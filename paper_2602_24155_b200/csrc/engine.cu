@@ -56,6 +56,7 @@ ReductionEngine::~ReductionEngine() {
 }
 
 void ReductionEngine::timed(double* acc, const std::function<void()>& f) {
+  ++g_traffic.launches;
   if (!clock.on) {
     f();
     return;
@@ -184,6 +185,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   DRZG_REQUIRE(nv * bits + colbits <= 64, "engine: state key does not fit 64 bits");
   auto key = [&](int c, const Expo& u) { return ((u64)c << (nv * bits)) | u.pack(bits); };
 
+  cudaEvent_t run0, run1;
+  DRZG_CUDA(cudaEventCreate(&run0));
+  DRZG_CUDA(cudaEventCreate(&run1));
+  DRZG_CUDA(cudaEventRecord(run0, st_));
   DevBuf<long long> dG;
   dG.alloc((size_t)ncol * Ld * gsize_);
   DRZG_CUDA(cudaMemsetAsync(dG.p, 0, dG.n * sizeof(long long), st_));
@@ -353,7 +358,16 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   for (int c = 0; c < ncol; ++c) led.combines += floor_arrivals[c] - (i64)floor_keys[c].size();
   std::vector<long long> hG(dG.n);
   DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
+  g_traffic.d2h += (long long)(dG.n * sizeof(long long));
+  DRZG_CUDA(cudaEventRecord(run1, st_));
   DRZG_CUDA(cudaStreamSynchronize(st_));
+  {
+    float ms = 0;
+    DRZG_CUDA(cudaEventElapsedTime(&ms, run0, run1));
+    clock.device_ms += ms;
+    cudaEventDestroy(run0);
+    cudaEventDestroy(run1);
+  }
   DRZG_CUDA(cudaGetLastError());
   G.assign(ncol, {});
   for (int c = 0; c < ncol; ++c)

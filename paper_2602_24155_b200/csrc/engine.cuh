@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <functional>
 #include <unordered_map>
 #include <unordered_set>
@@ -24,6 +25,14 @@ namespace drzg {
                                    __LINE__);                                                 \
   } while (0)
 
+// host<->device traffic and kernel launches of the current call (reported
+// with every result: the e2e byte counts and the launch count of the bench)
+struct Traffic {
+  std::atomic<long long> h2d{0}, d2h{0}, launches{0};
+  void reset() { h2d = 0; d2h = 0; launches = 0; }
+};
+inline Traffic g_traffic;
+
 enum class Policy { p_chunk = 0, depth_first = 1, var_by_var = 2 };
 
 struct Ledger {
@@ -35,6 +44,7 @@ struct KernelClock {
   bool on = false;
   double gemm_ms = 0, carry_ms = 0, gather_ms = 0, epi_ms = 0, other_ms = 0;
   i64 gemm_launches = 0;
+  double device_ms = 0;  // CUDA-event time of the whole device-resident run
   double gemm_macs = 0;  // algorithmic int8 MACs issued (nL x nL per state-digit)
 };
 
@@ -58,6 +68,7 @@ struct DevBuf {
   void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc(v.size());
     if (!v.empty()) DRZG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+    g_traffic.h2d += (long long)(v.size() * sizeof(T));
   }
 };
 

@@ -1,0 +1,25 @@
+"""GPU exploration: time the engine on the larger configurations."""
+import json, sys, time, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2602_24155_b200 as drzg
+
+cases = sys.argv[1:] or ["k3", "threefold", "fermat4_r1", "fermat4", "fourfold_r1"]
+for c in cases:
+    t = time.time()
+    try:
+        if c == "k3":
+            co = drzg.random_hypersurface(11, 3, 4, 1); r = drzg.frobenius(11, 3, 4, co, profile=True)
+        elif c == "threefold":
+            co = drzg.random_hypersurface(13, 4, 3, 1); r = drzg.frobenius(13, 4, 3, co, profile=True)
+        elif c == "fermat4_r1":
+            co = drzg.random_hypersurface(7, 5, 3, 1, fermat=True); r = drzg.frobenius(7, 5, 3, co, r_uniform=1, profile=True)
+        elif c == "fermat4":
+            co = drzg.random_hypersurface(7, 5, 3, 1, fermat=True); r = drzg.frobenius(7, 5, 3, co, profile=True)
+        elif c == "fourfold_r1":
+            co = drzg.random_hypersurface(7, 5, 3, 1); r = drzg.frobenius(7, 5, 3, co, r_uniform=1, columns=[1], profile=True)
+        elif c == "qsurf_r1":
+            co = drzg.random_hypersurface(7, 3, 5, 1); r = drzg.frobenius(7, 3, 5, co, r_uniform=1, nm=3, profile=True)
+        r.pop("F", None); r.pop("charpoly", None)
+        print(c, round(time.time() - t, 2), json.dumps(r), flush=True)
+    except Exception as e:
+        print(c, "ERROR", e, flush=True)
