@@ -151,16 +151,16 @@ void ReductionEngine::step(int B, int y) {
     a.IN = IN_.p;
     a.Cy = Cy_.p;
     a.Y = Y_.p;
-    dim3 gL((T.nL + 127) / 128, nb);
+    dim3 gL((unsigned)((T.nL + 127) / 128) * nb);
     timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 128, 0, st_>>>(a); });
-    dim3 gG(nLp_ / 64, (nb + 63) / 64);
+    dim3 gG((nb + 63) / 64, nLp_ / 64);
     for (int k = 0; k < T.dp.Ld; ++k) {
       timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });
       ++clock.gemm_launches;
       clock.gemm_macs += (double)T.nL * T.nL * nb;
       timed(&clock.carry_ms, [&] { dev::dixon_carry_kernel<<<gL, 128, 0, st_>>>(a, k); });
     }
-    dim3 gS((T.side + 127) / 128, nb);
+    dim3 gS((unsigned)((T.side + 127) / 128) * nb);
     timed(&clock.epi_ms, [&] { dev::epilogue_kernel<<<gS, 128, 0, st_>>>(a); });
     DRZG_CUDA(cudaGetLastError());
   }
@@ -285,7 +285,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         }
         d_a.upload(gptr, st_);
         d_b.upload(mem, st_);
-        dim3 gm((T.side + 127) / 128, (int)extra.size());
+        dim3 gm((unsigned)((T.side + 127) / 128) * extra.size());
         timed(&clock.other_ms, [&] {
           dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_a.p, d_b.p);
         });
@@ -347,7 +347,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       d_a.upload(fs, st_);
       d_b.upload(fc, st_);
       d_c.upload(fu, st_);
-      dim3 gf((T.side + 127) / 128, (int)fs.size());
+      dim3 gf((unsigned)((T.side + 127) / 128) * fs.size());
       timed(&clock.other_ms, [&] {
         dev::floor_kernel<<<gf, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, nv, d_a.p, d_b.p, d_c.p,
                                                mon_.p, btab_.p, dG.p, gsize_, d_err.p);

@@ -60,8 +60,9 @@ struct StepArgs {
 };
 
 __global__ void gather_kernel(StepArgs a) {
-  int s = blockIdx.y;
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nrb = (a.nL + blockDim.x - 1) / blockDim.x;  // flattened (state, row block)
+  int s = blockIdx.x / nrb;
+  int r = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
   if (r >= a.nL || s >= a.B) return;
   int g = a.gidx[(size_t)a.vdir[s] * a.nL + r];
   const int8_t* src = a.pool + (size_t)a.slot[s] * a.slot_stride;
@@ -76,7 +77,7 @@ __global__ void gather_kernel(StepArgs a) {
 __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
   __shared__ int Cs[64][17];
   __shared__ int Is[64][17];
-  const int r0 = blockIdx.x * 64, s0 = blockIdx.y * 64;
+  const int r0 = blockIdx.y * 64, s0 = blockIdx.x * 64;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   int acc[4][4] = {};
   const int words = a.nLp >> 2;
@@ -117,8 +118,9 @@ __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
 }
 
 __global__ void dixon_carry_kernel(StepArgs a, int k) {
-  int s = blockIdx.y;
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nrb = (a.nL + blockDim.x - 1) / blockDim.x;  // flattened (state, row block)
+  int s = blockIdx.x / nrb;
+  int r = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
   if (r >= a.nL || s >= a.B) return;
   const int8_t* y = a.Y + ((size_t)s * a.Ld + k) * a.nLp;
   int sum = 0;
@@ -131,8 +133,9 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
 }
 
 __global__ void epilogue_kernel(StepArgs a) {
-  int s = blockIdx.y;
-  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nrb = (a.side + blockDim.x - 1) / blockDim.x;
+  int s = blockIdx.x / nrb;
+  int g = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
   if (g >= a.side || s >= a.B) return;
   int x[6];
   const int* v = a.dirs + (size_t)a.vdir[s] * a.nv;
@@ -170,8 +173,9 @@ __global__ void seed_kernel(int8_t* pool, long long slot_stride, int sidep, int 
 // groups (CSR over member slots, first member receives the sum)
 __global__ void merge_kernel(int8_t* pool, long long slot_stride, int side, int sidep, int Ld, int q,
                              const int* gptr, const int* members) {
-  int grp = blockIdx.y;
-  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nrb = (side + blockDim.x - 1) / blockDim.x;
+  int grp = blockIdx.x / nrb;
+  int g = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
   if (g >= side) return;
   int acc[kLdMax];
   for (int t = 0; t < Ld; ++t) acc[t] = 0;
@@ -193,8 +197,9 @@ __global__ void merge_kernel(int8_t* pool, long long slot_stride, int side, int 
 __global__ void floor_kernel(const int8_t* pool, long long slot_stride, int side, int sidep, int Ld, int nv,
                              const int* slot, const int* col, const int* u, const int* mon, const unsigned long long* btab,
                              long long* G, int gsize, int* err) {
-  int s = blockIdx.y;
-  int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nrb = (side + blockDim.x - 1) / blockDim.x;
+  int s = blockIdx.x / nrb;
+  int g = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
   if (g >= side) return;
   const int8_t* w = pool + (size_t)slot[s] * slot_stride;
   int e[6];
