@@ -178,3 +178,15 @@ def charpoly(p, n, d, F, b, r_uniform=0, nm=0):
     """berkowitz_charpoly + recover_Q on a given F (zeta.hpp:456-470)"""
     arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F])
     return _json(lib().drzg_charpoly(ctypes.c_uint64(p), n, d, r_uniform, nm, b, arr))
+
+
+def test_tc_gemm(A, B, a_unsigned=False):
+    """D = A . B^T through the tcgen05 int8 kernel (test hook); A: M x K, B: N x K"""
+    A = np.ascontiguousarray(A, dtype=np.uint8 if a_unsigned else np.int8)
+    B = np.ascontiguousarray(B, dtype=np.int8)
+    M, K = A.shape
+    N = B.shape[0]
+    D = np.zeros((N, M), dtype=np.int32)
+    _check(lib().drzg_test_tc_gemm(M, N, K, A.ctypes.data_as(ctypes.c_void_p), B.ctypes.data_as(ctypes.c_void_p),
+                                   D.ctypes.data_as(ctypes.c_void_p), int(a_unsigned)))
+    return D

@@ -7,6 +7,7 @@
 
 #include "../../include/drzg.h"
 #include "kernels/linrec.cuh"
+#include "kernels/tc_gemm.cuh"
 #include "pipeline.cuh"
 
 using namespace drzg;
@@ -379,3 +380,30 @@ char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t
 }
 
 }  // extern "C"
+
+// test hook: raw int32 D = A . B^T through the tcgen05 kernel (host buffers)
+extern "C" int drzg_test_tc_gemm(int32_t M, int32_t N, int32_t K, const int8_t* A, const int8_t* B, int32_t* D,
+                                 int32_t a_unsigned) {
+  return guard_int([&] {
+    int ld = (K + 15) / 16 * 16;
+    DevBuf<int8_t> dA, dB;
+    DevBuf<int32_t> dD;
+    std::vector<int8_t> ha((size_t)M * ld, 0), hb((size_t)N * ld, 0);
+    for (int i = 0; i < M; ++i)
+      for (int k = 0; k < K; ++k) ha[(size_t)i * ld + k] = A[(size_t)i * K + k];
+    for (int i = 0; i < N; ++i)
+      for (int k = 0; k < K; ++k) hb[(size_t)i * ld + k] = B[(size_t)i * K + k];
+    dA.upload(ha, 0);
+    dB.upload(hb, 0);
+    dD.alloc((size_t)M * N);
+    TcEpiArgs e;
+    e.mode = (int)TcEpilogue::raw;
+    e.a_unsigned = a_unsigned;
+    e.M = M;
+    e.N = N;
+    e.out = dD.p;
+    tc_gemm_i8(dA.p, M, ld, dB.p, N, ld, ld, e, 0);
+    DRZG_CUDA(cudaDeviceSynchronize());
+    DRZG_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}

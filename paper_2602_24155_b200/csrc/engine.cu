@@ -1,10 +1,13 @@
 // Device-resident reduction engine (see engine.cuh).
 #include <algorithm>
 #include <functional>
+#include <cstdlib>
 #include <map>
+#include <string>
 
 #include "engine.cuh"
 #include "kernels/dixon.cuh"
+#include "kernels/tc_gemm.cuh"
 
 namespace drzg {
 
@@ -24,6 +27,22 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   for (int r = 0; r < T.nL; ++r)
     for (int c = 0; c < T.nL; ++c) Cp[(size_t)r * nLp_ + c] = T.sys.Cq[(size_t)r * T.nL + c];
   C_.upload(Cp, st_);
+  // dense Jp for the tensor-core carry product (entries are exact small
+  // non-negative integers; u8 operand); DRZG_GEMM=dp4a selects the CUDA-core path
+  {
+    const char* g = std::getenv("DRZG_GEMM");
+    bool want_tc = !(g && std::string(g) == "dp4a");
+    int maxv = 0;
+    for (int v : T.sys.val) maxv = std::max(maxv, v);
+    if (want_tc && maxv < 256) {
+      std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);
+      for (int r = 0; r < T.nL; ++r)
+        for (int e = T.sys.rowptr[r]; e < T.sys.rowptr[r + 1]; ++e)
+          Jd[(size_t)r * nLp_ + T.sys.col[e]] = (int8_t)(uint8_t)T.sys.val[e];
+      Jd_.upload(Jd, st_);
+      use_tc_ = true;
+    }
+  }
   jp_ptr_.upload(T.sys.rowptr, st_);
   jp_col_.upload(T.sys.col, st_);
   jp_val_.upload(T.sys.val, st_);
@@ -155,10 +174,40 @@ void ReductionEngine::step(int B, int y) {
     timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 128, 0, st_>>>(a); });
     dim3 gG((nb + 63) / 64, nLp_ / 64);
     for (int k = 0; k < T.dp.Ld; ++k) {
-      timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });
-      ++clock.gemm_launches;
-      clock.gemm_macs += (double)T.nL * T.nL * nb;
-      timed(&clock.carry_ms, [&] { dev::dixon_carry_kernel<<<gL, 128, 0, st_>>>(a, k); });
+      if (use_tc_) {
+        // y_k = bal(Cq . in_k): tcgen05 int8, digit epilogue
+        TcEpiArgs e;
+        e.mode = (int)TcEpilogue::digit;
+        e.M = T.nL;
+        e.N = nb;
+        e.q = T.dp.q;
+        e.Ld = T.dp.Ld;
+        e.k = k;
+        e.nLp = nLp_;
+        e.nL = T.nL;
+        e.Y = Y_.p;
+        timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, IN_.p, nb, nLp_, nLp_, e, st_); });
+        ++clock.gemm_launches;
+        clock.gemm_macs += (double)T.nL * T.nL * nb;
+        if (k + 1 < T.dp.Ld) {
+          // c_{k+1} = (b_k + c_k - Jp . y_k) / q, in_{k+1}: tcgen05 int8, carry epilogue
+          e.mode = (int)TcEpilogue::carry;
+          e.a_unsigned = 1;
+          e.Bg = Bg_.p;
+          e.Cy = Cy_.p;
+          e.IN = IN_.p;
+          timed(&clock.carry_ms, [&] {
+            tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_, nb, T.dp.Ld * nLp_, nLp_, e, st_);
+          });
+          ++clock.gemm_launches;
+          clock.gemm_macs += (double)T.nL * T.nL * nb;
+        }
+      } else {
+        timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });
+        ++clock.gemm_launches;
+        clock.gemm_macs += (double)T.nL * T.nL * nb;
+        timed(&clock.carry_ms, [&] { dev::dixon_carry_kernel<<<gL, 128, 0, st_>>>(a, k); });
+      }
     }
     dim3 gS((unsigned)((T.side + 127) / 128) * nb);
     timed(&clock.epi_ms, [&] { dev::epilogue_kernel<<<gS, 128, 0, st_>>>(a); });

@@ -87,6 +87,7 @@ class ReductionEngine {
                    std::vector<i8>& w_digits, Ledger& led);
 
   KernelClock clock;
+  bool tensor_cores() const { return use_tc_; }
   int floor_size() const { return gsize_; }
   const RuvTables& tables() const { return *T_; }
 
@@ -113,6 +114,8 @@ class ReductionEngine {
   long long slot_stride_ = 0;
   // tables
   DevBuf<int8_t> C_;
+  DevBuf<int8_t> Jd_;   // Jp dense (u8), nLp x nLp, for the tensor-core carry
+  bool use_tc_ = false; // tcgen05 GEMMs (else the dp4a CUDA-core kernels)
   DevBuf<int> jp_ptr_, jp_col_, jp_val_, gidx_, dirs_, t_ptr_, t_src_, sol_i_, sol_mu_, mon_;
   DevBuf<unsigned long long> btab_;
   // pool

@@ -1,0 +1,236 @@
+// int8 tcgen05 GEMM with Dixon epilogues (see tc_gemm.cuh).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <string>
+
+#include "../host/common.hpp"
+#include "tc_gemm.cuh"
+
+namespace drzg {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 128;  // bytes of K per stage (one 128B swizzle row)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;
+constexpr int B_BYTES = BN * BK;
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (spin > (1u << 24)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (ignored for swizzled K-major), canonical 1
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;            // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ int balmod(int x, int q) {
+  int r = x % q;
+  if (r < 0) r += q;
+  if (r > (q >> 1)) r -= q;
+  return r;
+}
+
+// one 128 x BN output tile per CTA; 128 threads: warp 0 = TMA producer,
+// warp 1 = MMA issuer, warp 2 = TMEM allocator; all four drain the tile
+__global__ void __launch_bounds__(128, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
+                uint32_t idesc, TcEpiArgs epi) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + STAGES * A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* done = bars + 2 * STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      int s = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(smem_u32(&empty[s]), ((kb / STAGES) - 1) & 1);
+      uint32_t fb = smem_u32(&full[s]);
+      mbar_expect_tx(fb, A_BYTES + B_BYTES);
+      tma_load_2d(smem_u32(sA + s * A_BYTES), &tmA, fb, kb * BK, m0);
+      tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      int s = kb % STAGES;
+      mbar_wait(smem_u32(&full[s]), (kb / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BK / 32; ++kk)
+        mma_i8(tmem, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+      mma_commit(smem_u32(&empty[s]));
+    }
+    mma_commit(smem_u32(done));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(done), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // epilogue: thread owns output row m = m0 + 32*warp + lane, 16 columns per load
+  const int m = m0 + warp * 32 + lane;
+  for (int c = 0; c < BN; c += 16) {
+    int v[16];
+    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
+    if (m >= epi.M) continue;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      int n = n0 + c + j;
+      if (n >= epi.N) break;
+      if (epi.mode == (int)TcEpilogue::raw) {
+        epi.out[(size_t)n * epi.M + m] = v[j];
+      } else if (epi.mode == (int)TcEpilogue::digit) {
+        epi.Y[((size_t)n * epi.Ld + epi.k) * epi.nLp + m] = (int8_t)balmod(v[j], epi.q);
+      } else {
+        const int8_t* bg = epi.Bg + (size_t)n * epi.Ld * epi.nLp;
+        int num = (int)bg[(size_t)epi.k * epi.nLp + m] + epi.Cy[(size_t)n * epi.nL + m] - v[j];
+        int cnew = num / epi.q;
+        epi.Cy[(size_t)n * epi.nL + m] = cnew;
+        if (epi.k + 1 < epi.Ld)
+          epi.IN[(size_t)n * epi.nLp + m] = (int8_t)balmod((int)bg[(size_t)(epi.k + 1) * epi.nLp + m] + cnew, epi.q);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+}
+
+}  // namespace tc
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  DRZG_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+CUtensorMap make_map(const int8_t* ptr, int rows, int ld, int K, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DRZG_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+}  // namespace
+
+void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB, int ldb, int K,
+                const TcEpiArgs& epi, cudaStream_t st) {
+  DRZG_REQUIRE(lda % 16 == 0 && ldb % 16 == 0, "tc_gemm: row pitch must be a multiple of 16 bytes");
+  DRZG_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0, "tc_gemm: operands must be 16-byte aligned");
+  CUtensorMap ma = make_map(A, rowsA, lda, K, tc::BM);
+  CUtensorMap mb = make_map(B, rowsB, ldb, K, tc::BN);
+  // kind::i8 instruction descriptor: D s32, A signed (Cq) or unsigned (Jp),
+  // B signed, both K-major, N = BN, M = 128
+  uint32_t a_signed = epi.a_unsigned ? 0u : 1u;
+  uint32_t idesc = (2u << 4) | (a_signed << 7) | (1u << 10) | ((uint32_t)(tc::BN >> 3) << 17) |
+                   ((uint32_t)(tc::BM >> 4) << 24);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    attr = true;
+  }
+  dim3 grid((epi.N + tc::BN - 1) / tc::BN, (epi.M + tc::BM - 1) / tc::BM);
+  tc::gemm_kernel<<<grid, 128, tc::SMEM_BYTES, st>>>(ma, mb, K, idesc, epi);
+  cudaError_t e = cudaGetLastError();
+  DRZG_REQUIRE(e == cudaSuccess, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
+}
+
+}  // namespace drzg

@@ -1,0 +1,44 @@
+// int8 tcgen05 GEMM with Dixon epilogues (sm_100a).
+//
+//   D[m][n] = sum_k A[m][k] * B[n][k]      (A: M x K, B: N x K, both K-major int8)
+//
+// 128 x BN CTA tile, K staged 128 bytes at a time through a 4-deep
+// TMA -> shared-memory (128B-swizzled) ring; one elected thread issues
+// tcgen05.mma.kind::i8 (M=128, N=BN, K=32) into a TMEM int32 accumulator;
+// four epilogue warps drain TMEM with tcgen05.ld and apply the Dixon step's
+// elementwise epilogue in registers:
+//   EPI_DIGIT  y_k = bal(D mod q) -> int8 Y plane          (D = Cq . in_k)
+//   EPI_CARRY  c'  = (b_k + c - D) / q,  in' = bal(b_{k+1} + c')  (D = Jp . y_k)
+//   EPI_RAW    D as int32 (tests)
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace drzg {
+
+enum class TcEpilogue : int { raw = 0, digit = 1, carry = 2 };
+
+struct TcEpiArgs {
+  int mode = 0;
+  int a_unsigned = 0;      // A operand u8 (else s8)
+  int M = 0, N = 0;        // valid output extent
+  int q = 0, Ld = 0, k = 0;
+  int nLp = 0, nL = 0;
+  // raw
+  int32_t* out = nullptr;  // N x M (row n holds the M outputs of column n)
+  // digit
+  int8_t* Y = nullptr;     // N x Ld x nLp
+  // carry
+  const int8_t* Bg = nullptr;  // N x Ld x nLp
+  int* Cy = nullptr;           // N x nL
+  int8_t* IN = nullptr;        // N x nLp
+};
+
+// host side: build tensor maps and launch; A is (rowsA x K) with row pitch
+// lda bytes, B is (rowsB x K) with row pitch ldb bytes
+void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB, int ldb, int K,
+                const TcEpiArgs& epi, cudaStream_t st);
+
+}  // namespace drzg

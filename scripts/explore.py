@@ -17,6 +17,9 @@ for c in cases:
             co = drzg.random_hypersurface(7, 5, 3, 1, fermat=True); r = drzg.frobenius(7, 5, 3, co, profile=True)
         elif c == "fourfold_r1":
             co = drzg.random_hypersurface(7, 5, 3, 1); r = drzg.frobenius(7, 5, 3, co, r_uniform=1, columns=[1], profile=True)
+        elif c.startswith("fourfold_col"):
+            col = int(c[len("fourfold_col"):])
+            co = drzg.random_hypersurface(7, 5, 3, 1); r = drzg.frobenius(7, 5, 3, co, columns=[col], profile=True)
         elif c == "qsurf_r1":
             co = drzg.random_hypersurface(7, 3, 5, 1); r = drzg.frobenius(7, 3, 5, co, r_uniform=1, nm=3, profile=True)
         r.pop("F", None); r.pop("charpoly", None)
