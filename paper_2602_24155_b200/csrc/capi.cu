@@ -119,7 +119,7 @@ std::string frob_json_body(const FrobResult& fr) {
      << ",\"kernels\":{\"gemm_ms\":" << fr.clk.gemm_ms << ",\"carry_ms\":" << fr.clk.carry_ms
      << ",\"gather_ms\":" << fr.clk.gather_ms << ",\"epilogue_ms\":" << fr.clk.epi_ms
      << ",\"other_ms\":" << fr.clk.other_ms << ",\"gemm_launches\":" << fr.clk.gemm_launches
-     << ",\"gemm_macs\":" << fr.clk.gemm_macs << ",\"device_ms\":" << fr.clk.device_ms << "}"
+     << ",\"gemm_macs\":" << fr.clk.gemm_macs << ",\"device_ms\":" << fr.clk.device_ms << ",\"peak_live_states\":" << fr.clk.peak_live << "}"
      << ",\"traffic\":{\"h2d_bytes\":" << g_traffic.h2d.load() << ",\"d2h_bytes\":" << g_traffic.d2h.load()
      << ",\"launches\":" << g_traffic.launches.load() << "}";
   return os.str();
@@ -405,5 +405,60 @@ extern "C" int drzg_test_tc_gemm(int32_t M, int32_t N, int32_t K, const int8_t* 
     tc_gemm_i8(dA.p, M, ld, dB.p, N, ld, ld, e, 0);
     DRZG_CUDA(cudaDeviceSynchronize());
     DRZG_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+// micro-benchmark hook: one Dixon digit (mode 1) or carry (mode 2) GEMM of
+// nL x nL against `states` synthetic states with the engine's layouts;
+// returns the mean CUDA-event milliseconds per launch
+extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int32_t iters, float* ms_out) {
+  return guard_int([&] {
+    const int nLp = (nL + 63) / 64 * 64, Ld = 12;
+    DevBuf<int8_t> A, IN, Y, Bg;
+    DevBuf<int32_t> Cy;
+    A.alloc((size_t)nLp * nLp);
+    IN.alloc((size_t)states * nLp);
+    Y.alloc((size_t)states * Ld * nLp);
+    Bg.alloc((size_t)states * Ld * nLp);
+    Cy.alloc((size_t)states * nL);
+    DRZG_CUDA(cudaMemset(A.p, 1, A.n));
+    DRZG_CUDA(cudaMemset(IN.p, 1, IN.n));
+    DRZG_CUDA(cudaMemset(Y.p, 0, Y.n));
+    DRZG_CUDA(cudaMemset(Bg.p, 0, Bg.n));
+    DRZG_CUDA(cudaMemset(Cy.p, 0, Cy.n * 4));
+    TcEpiArgs e;
+    e.mode = mode;
+    e.M = nL;
+    e.N = states;
+    e.q = 49;
+    e.fq = FastQ::make(49);
+    e.Ld = Ld;
+    e.k = 3;
+    e.nLp = nLp;
+    e.nL = nL;
+    e.Y = Y.p;
+    e.Bg = Bg.p;
+    e.Cy = Cy.p;
+    e.IN = IN.p;
+    e.a_unsigned = mode == 2;
+    auto run = [&] {
+      if (mode == 2)
+        tc_gemm_i8(A.p, nLp, nLp, Y.p + 3 * nLp, states, Ld * nLp, nLp, e, 0);
+      else
+        tc_gemm_i8(A.p, nLp, nLp, IN.p, states, nLp, nLp, e, 0);
+    };
+    run();
+    cudaEvent_t e0, e1;
+    DRZG_CUDA(cudaEventCreate(&e0));
+    DRZG_CUDA(cudaEventCreate(&e1));
+    DRZG_CUDA(cudaEventRecord(e0, 0));
+    for (int i = 0; i < iters; ++i) run();
+    DRZG_CUDA(cudaEventRecord(e1, 0));
+    DRZG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    DRZG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_out = ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }

@@ -90,12 +90,21 @@ void ReductionEngine::timed(double* acc, const std::function<void()>& f) {
 }
 
 void ReductionEngine::grow_pool(int need) {
-  int ncap = std::max(need, std::max(1024, cap_ * 2));
+  int ncap = std::max(need, cap_ + std::max(1024, cap_ / 2));
   size_t bytes = (size_t)ncap * slot_stride_;
   size_t fr = 0, tot = 0;
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
-  DRZG_REQUIRE(bytes - (size_t)cap_ * slot_stride_ + (size_t)(256u << 20) < fr,
-               "engine: state pool exceeds device memory");
+  if (bytes + (size_t)(1u << 30) > fr && cap_ > 0) {
+    // release the batch temporaries first; they are re-sized on demand
+    Bg_.release();
+    Y_.release();
+    IN_.release();
+    Cy_.release();
+    bcap_ = 0;
+    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  }
+  DRZG_REQUIRE(bytes + (size_t)(1u << 30) < fr, "engine: state pool exceeds device memory (" +
+                                                    std::to_string(ncap) + " slots)");
   int8_t* np = nullptr;
   DRZG_CUDA(cudaMalloc(&np, bytes));
   if (pool_) {
@@ -112,6 +121,7 @@ int ReductionEngine::alloc_slot() {
   if (free_.empty()) grow_pool(cap_ + 1);
   int s = free_.back();
   free_.pop_back();
+  peak_live_ = std::max<i64>(peak_live_, (i64)cap_ - (i64)free_.size());
   return s;
 }
 
@@ -122,7 +132,7 @@ void ReductionEngine::ensure_batch(int B) {
   size_t fr = 0, tot = 0;
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   // temporaries get at most half of what is free, in multiples of 64 states
-  size_t lim = std::max<size_t>(64, (fr / 2) / per / 64 * 64);
+  size_t lim = std::max<size_t>(64, (size_t)(fr * 0.8) / per / 64 * 64);
   int nb = (int)std::min<size_t>(lim, (size_t)round_up(B, 64));
   if (nb <= bcap_) return;
   bcap_ = nb;
@@ -159,6 +169,7 @@ void ReductionEngine::step(int B, int y) {
     a.sidep = sidep_;
     a.Ld = T.dp.Ld;
     a.q = T.dp.q;
+    a.fq = FastQ::make(T.dp.q);
     a.pool = pool_;
     a.slot_stride = slot_stride_;
     a.slot = d_slot_.p + b0;
@@ -181,6 +192,7 @@ void ReductionEngine::step(int B, int y) {
         e.M = T.nL;
         e.N = nb;
         e.q = T.dp.q;
+        e.fq = FastQ::make(T.dp.q);
         e.Ld = T.dp.Ld;
         e.k = k;
         e.nLp = nLp_;
@@ -244,7 +256,15 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   DevBuf<int> d_err;
   d_err.alloc(1);
   DRZG_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int), st_));
-  if (cap_ == 0) grow_pool((int)std::min<size_t>(std::max<size_t>(total_seeds / 4, 1024), 1 << 20));
+  if (cap_ == 0) {
+    // live states never exceed the seeds materialised so far: size the pool
+    // for all of them when that fits 60% of free HBM (the rest feeds the
+    // batch temporaries), else take the 60% and grow only if needed
+    size_t fr = 0, tot = 0;
+    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    size_t budget = (size_t)(fr * 0.60) / (size_t)slot_stride_;
+    grow_pool((int)std::max<size_t>(1024, std::min<size_t>(total_seeds, budget)));
+  }
 
   std::map<int, std::vector<HS>, std::greater<int>> landed;
   std::vector<std::unordered_set<u64>> floor_keys(ncol);

@@ -45,6 +45,7 @@ struct KernelClock {
   double gemm_ms = 0, carry_ms = 0, gather_ms = 0, epi_ms = 0, other_ms = 0;
   i64 gemm_launches = 0;
   double device_ms = 0;  // CUDA-event time of the whole device-resident run
+  i64 peak_live = 0;     // most state slots live at once
   double gemm_macs = 0;  // algorithmic int8 MACs issued (nL x nL per state-digit)
 };
 
@@ -64,6 +65,11 @@ struct DevBuf {
     p = nullptr;
     DRZG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
     n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
   }
   void upload(const std::vector<T>& v, cudaStream_t st) {
     alloc(v.size());
@@ -89,6 +95,7 @@ class ReductionEngine {
   KernelClock clock;
   bool tensor_cores() const { return use_tc_; }
   int floor_size() const { return gsize_; }
+  i64 peak_live() const { return peak_live_; }
   const RuvTables& tables() const { return *T_; }
 
  private:
@@ -121,6 +128,7 @@ class ReductionEngine {
   // pool
   int8_t* pool_ = nullptr;
   int cap_ = 0;
+  i64 peak_live_ = 0;
   std::vector<int> free_;
   // sweep arrays
   DevBuf<int> d_slot_, d_vdir_, d_u0_;

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "fastq.cuh"
+
 namespace drzg {
 namespace dev {
 
@@ -43,6 +45,7 @@ struct StepArgs {
   const int* sol_i;       // per solution index: variable i of its generator
   const int* sol_mu;      // ... and mu_i
   int nv, nL, nLp, side, sidep, Ld, q;
+  FastQ fq;
   // state pool
   int8_t* pool;           // slots x (Ld * sidep)
   long long slot_stride;  // Ld * sidep
@@ -68,7 +71,7 @@ __global__ void gather_kernel(StepArgs a) {
   const int8_t* src = a.pool + (size_t)a.slot[s] * a.slot_stride;
   int8_t* dst = a.Bg + (size_t)s * a.Ld * a.nLp;
   for (int t = 0; t < a.Ld; ++t) dst[(size_t)t * a.nLp + r] = g >= 0 ? src[(size_t)t * a.sidep + g] : 0;
-  a.IN[(size_t)s * a.nLp + r] = (int8_t)balmod(g >= 0 ? src[g] : 0, a.q);
+  a.IN[(size_t)s * a.nLp + r] = (int8_t)a.fq.bal(g >= 0 ? src[g] : 0);
   a.Cy[(size_t)s * a.nL + r] = 0;
 }
 
@@ -151,10 +154,11 @@ __global__ void epilogue_kernel(StepArgs a) {
   int8_t* out = a.pool + (size_t)a.slot[s] * a.slot_stride;
   int carry = 0;
   for (int t = 0; t < a.Ld; ++t) {
-    int v2 = acc[t] + carry;
-    int dgt = balmod(v2, a.q);
-    carry = (v2 - dgt) / a.q;
-    out[(size_t)t * a.sidep + g] = (int8_t)dgt;
+    int r;
+    int qt = a.fq.divfloor(acc[t] + carry, r);
+    if (r > (a.q >> 1)) r -= a.q, ++qt;
+    carry = qt;
+    out[(size_t)t * a.sidep + g] = (int8_t)r;
   }
 }
 

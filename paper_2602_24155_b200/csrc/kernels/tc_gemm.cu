@@ -1,6 +1,7 @@
 // int8 tcgen05 GEMM with Dixon epilogues (see tc_gemm.cuh).
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -11,7 +12,7 @@ namespace drzg {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BN = 128;
+constexpr int BN = 256;
 constexpr int BK = 128;  // bytes of K per stage (one 128B swizzle row)
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;
@@ -86,9 +87,20 @@ __device__ __forceinline__ int balmod(int x, int q) {
   return r;
 }
 
-// one 128 x BN output tile per CTA; 128 threads: warp 0 = TMA producer,
-// warp 1 = MMA issuer, warp 2 = TMEM allocator; all four drain the tile
-__global__ void __launch_bounds__(128, 1)
+// Persistent, warp-specialised: CTA c processes tiles c, c+grid, ... (M-tile
+// fastest so concurrently running CTAs share the B tile in L2).
+//   warp 0: TMA producer (4-stage smem ring)      warp 1: MMA issuer
+//   warp 2: TMEM allocator                        warps 4..11: epilogue
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap
+// the mainloop of tile i+1.
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 128 + 32 * EPI_WARPS;
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                 uint32_t idesc, TcEpiArgs epi) {
   extern __shared__ uint8_t smem_raw[];
@@ -98,26 +110,31 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + STAGES;
-  uint64_t* done = bars + 2 * STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 1);
+  uint64_t* tfull = bars + 2 * STAGES;       // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (K + BK - 1) / BK;
+  const int mt = (epi.M + BM - 1) / BM, ntl = (epi.N + BN - 1) / BN;
+  const int tiles = mt * ntl;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
-    mbar_init(smem_u32(done), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), EPI_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -125,59 +142,104 @@ __global__ void __launch_bounds__(128, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    for (int kb = 0; kb < nk; ++kb) {
-      int s = kb % STAGES;
-      if (kb >= STAGES) mbar_wait(smem_u32(&empty[s]), ((kb / STAGES) - 1) & 1);
-      uint32_t fb = smem_u32(&full[s]);
-      mbar_expect_tx(fb, A_BYTES + B_BYTES);
-      tma_load_2d(smem_u32(sA + s * A_BYTES), &tmA, fb, kb * BK, m0);
-      tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kb * BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    for (int kb = 0; kb < nk; ++kb) {
-      int s = kb % STAGES;
-      mbar_wait(smem_u32(&full[s]), (kb / STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
-#pragma unroll
-      for (int kk = 0; kk < BK / 32; ++kk)
-        mma_i8(tmem, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
-      mma_commit(smem_u32(&empty[s]));
-    }
-    mma_commit(smem_u32(done));
-  }
-  __syncwarp();
-  mbar_wait(smem_u32(done), 0);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-
-  // epilogue: thread owns output row m = m0 + 32*warp + lane, 16 columns per load
-  const int m = m0 + warp * 32 + lane;
-  for (int c = 0; c < BN; c += 16) {
-    int v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c, v);
-    if (m >= epi.M) continue;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      int n = n0 + c + j;
-      if (n >= epi.N) break;
-      if (epi.mode == (int)TcEpilogue::raw) {
-        epi.out[(size_t)n * epi.M + m] = v[j];
-      } else if (epi.mode == (int)TcEpilogue::digit) {
-        epi.Y[((size_t)n * epi.Ld + epi.k) * epi.nLp + m] = (int8_t)balmod(v[j], epi.q);
-      } else {
-        const int8_t* bg = epi.Bg + (size_t)n * epi.Ld * epi.nLp;
-        int num = (int)bg[(size_t)epi.k * epi.nLp + m] + epi.Cy[(size_t)n * epi.nL + m] - v[j];
-        int cnew = num / epi.q;
-        epi.Cy[(size_t)n * epi.nL + m] = cnew;
-        if (epi.k + 1 < epi.Ld)
-          epi.IN[(size_t)n * epi.nLp + m] = (int8_t)balmod((int)bg[(size_t)(epi.k + 1) * epi.nLp + m] + cnew, epi.q);
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          int s = it % STAGES;
+          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
+          uint32_t fb = smem_u32(&full[s]);
+          mbar_expect_tx(fb, A_BYTES + B_BYTES);
+          tma_load_2d(smem_u32(sA + s * A_BYTES), &tmA, fb, kb * BK, m0);
+          tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kb * BK, n0);
+        }
       }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const int acc = i & 1;
+        mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          int s = it % STAGES;
+          mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+          mma_commit(smem_u32(&empty[s]));
+        }
+        mma_commit(smem_u32(&tfull[acc]));
+      }
+    }
+  } else if (warp >= 4) {
+    // epilogue warp e: TMEM lane quarter e % 4, column half e / 4
+    const int e = warp - 4;
+    const int quarter = e & 3, half = e >> 2;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      const int acc = i & 1;
+      mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int m = m0 + quarter * 32 + lane;
+      const bool mok = m < epi.M;
+      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
+        int v[16];
+        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        const int nb = n0 + c;
+        if (!mok || nb >= epi.N) continue;
+        const int cnt = min(16, epi.N - nb);
+        if (epi.mode == (int)TcEpilogue::raw) {
+          for (int j = 0; j < cnt; ++j) epi.out[(size_t)(nb + j) * epi.M + m] = v[j];
+        } else if (epi.mode == (int)TcEpilogue::digit) {
+          int8_t* y = epi.Y + ((size_t)nb * epi.Ld + epi.k) * epi.nLp + m;
+          const size_t stride = (size_t)epi.Ld * epi.nLp;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < cnt) y[j * stride] = (int8_t)epi.fq.bal(v[j]);
+        } else {
+          // carry: issue every load of the 16 columns before using any
+          const size_t bstride = (size_t)epi.Ld * epi.nLp;
+          const int8_t* bg = epi.Bg + (size_t)nb * bstride + (size_t)epi.k * epi.nLp + m;
+          int* cy = epi.Cy + (size_t)nb * epi.nL + m;
+          int b0[16], b1[16], cc[16];
+          const bool last = epi.k + 1 >= epi.Ld;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < cnt) {
+              b0[j] = __ldg(bg + j * bstride);
+              b1[j] = last ? 0 : __ldg(bg + j * bstride + epi.nLp);
+              cc[j] = cy[(size_t)j * epi.nL];
+            }
+          }
+          int8_t* in = epi.IN + (size_t)nb * epi.nLp + m;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (j < cnt) {
+              int rem;
+              int cnew = epi.fq.divfloor(b0[j] + cc[j] - v[j], rem);  // exact: rem == 0
+              cy[(size_t)j * epi.nL] = cnew;
+              if (!last) in[(size_t)j * epi.nLp] = (int8_t)epi.fq.bal(b1[j] + cnew);
+            }
+          }
+        }
+      }
+      // all of this warp's TMEM reads of buffer `acc` are complete
+      __syncwarp();
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
 }
 
 }  // namespace tc
@@ -227,8 +289,15 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
     cudaFuncSetAttribute(tc::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
     attr = true;
   }
-  dim3 grid((epi.N + tc::BN - 1) / tc::BN, (epi.M + tc::BM - 1) / tc::BM);
-  tc::gemm_kernel<<<grid, 128, tc::SMEM_BYTES, st>>>(ma, mb, K, idesc, epi);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int tiles = ((epi.N + tc::BN - 1) / tc::BN) * ((epi.M + tc::BM - 1) / tc::BM);
+  dim3 grid(std::min(tiles, sms));
+  tc::gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ma, mb, K, idesc, epi);
   cudaError_t e = cudaGetLastError();
   DRZG_REQUIRE(e == cudaSuccess, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
 }

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "fastq.cuh"
+
 namespace drzg {
 
 enum class TcEpilogue : int { raw = 0, digit = 1, carry = 2 };
@@ -25,6 +27,7 @@ struct TcEpiArgs {
   int a_unsigned = 0;      // A operand u8 (else s8)
   int M = 0, N = 0;        // valid output extent
   int q = 0, Ld = 0, k = 0;
+  FastQ fq;
   int nLp = 0, nL = 0;
   // raw
   int32_t* out = nullptr;  // N x M (row n holds the M outputs of column n)

@@ -60,6 +60,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     ReductionEngine eng(T, n, p, st);
     eng.clock.on = opt.profile;
     if (!seeds.empty()) eng.run_pchunk(seeds, G, out.led);
+    eng.clock.peak_live = eng.peak_live();
     out.clk = eng.clock;
   }
   double t3 = now_s();
