@@ -190,3 +190,15 @@ def test_tc_gemm(A, B, a_unsigned=False):
     _check(lib().drzg_test_tc_gemm(M, N, K, A.ctypes.data_as(ctypes.c_void_p), B.ctypes.data_as(ctypes.c_void_p),
                                    D.ctypes.data_as(ctypes.c_void_p), int(a_unsigned)))
     return D
+
+
+def test_tc_gemm_mn(A, B, a_unsigned=False):
+    """as test_tc_gemm, with B staged K x N (MN-major operand)"""
+    A = np.ascontiguousarray(A, dtype=np.uint8 if a_unsigned else np.int8)
+    B = np.ascontiguousarray(B, dtype=np.int8)
+    M, K = A.shape
+    N = B.shape[0]
+    D = np.zeros((N, M), dtype=np.int32)
+    _check(lib().drzg_test_tc_gemm_mn(M, N, K, A.ctypes.data_as(ctypes.c_void_p), B.ctypes.data_as(ctypes.c_void_p),
+                                      D.ctypes.data_as(ctypes.c_void_p), int(a_unsigned)))
+    return D

@@ -415,17 +415,18 @@ extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int3
   return guard_int([&] {
     const int nLp = (nL + 63) / 64 * 64, Ld = 12;
     DevBuf<int8_t> A, IN, Y, Bg;
-    DevBuf<int32_t> Cy;
+    DevBuf<int16_t> Cy;
     A.alloc((size_t)nLp * nLp);
     IN.alloc((size_t)states * nLp);
     Y.alloc((size_t)states * Ld * nLp);
     Bg.alloc((size_t)states * Ld * nLp);
-    Cy.alloc((size_t)states * nL);
+    // state-contiguous layouts, pitch = states (multiple of 64)
+    Cy.alloc((size_t)states * nLp);
     DRZG_CUDA(cudaMemset(A.p, 1, A.n));
     DRZG_CUDA(cudaMemset(IN.p, 1, IN.n));
     DRZG_CUDA(cudaMemset(Y.p, 0, Y.n));
     DRZG_CUDA(cudaMemset(Bg.p, 0, Bg.n));
-    DRZG_CUDA(cudaMemset(Cy.p, 0, Cy.n * 4));
+    DRZG_CUDA(cudaMemset(Cy.p, 0, Cy.n * 2));
     TcEpiArgs e;
     e.mode = mode;
     e.M = nL;
@@ -441,11 +442,13 @@ extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int3
     e.Cy = Cy.p;
     e.IN = IN.p;
     e.a_unsigned = mode == 2;
+    e.b_mn = 1;
+    e.P = states;
     auto run = [&] {
       if (mode == 2)
-        tc_gemm_i8(A.p, nLp, nLp, Y.p + 3 * nLp, states, Ld * nLp, nLp, e, 0);
+        tc_gemm_i8(A.p, nLp, nLp, Y.p + (size_t)3 * nLp * states, states, states, nLp, e, 0);
       else
-        tc_gemm_i8(A.p, nLp, nLp, IN.p, states, nLp, nLp, e, 0);
+        tc_gemm_i8(A.p, nLp, nLp, IN.p, states, states, nLp, e, 0);
     };
     run();
     cudaEvent_t e0, e1;
@@ -460,5 +463,35 @@ extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int3
     *ms_out = ms / iters;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+  });
+}
+
+// test hook, MN-major B: D = A . B^T with B stored K x Npad (states contiguous)
+extern "C" int drzg_test_tc_gemm_mn(int32_t M, int32_t N, int32_t K, const int8_t* A, const int8_t* B, int32_t* D,
+                                    int32_t a_unsigned) {
+  return guard_int([&] {
+    int ld = (K + 15) / 16 * 16;
+    int P = (N + 63) / 64 * 64;
+    DevBuf<int8_t> dA, dB;
+    DevBuf<int32_t> dD;
+    std::vector<int8_t> ha((size_t)M * ld, 0), hb((size_t)K * P, 0);
+    for (int i = 0; i < M; ++i)
+      for (int k = 0; k < K; ++k) ha[(size_t)i * ld + k] = A[(size_t)i * K + k];
+    for (int n = 0; n < N; ++n)
+      for (int k = 0; k < K; ++k) hb[(size_t)k * P + n] = B[(size_t)n * K + k];
+    dA.upload(ha, 0);
+    dB.upload(hb, 0);
+    dD.alloc((size_t)M * N);
+    TcEpiArgs e;
+    e.mode = (int)TcEpilogue::raw;
+    e.a_unsigned = a_unsigned;
+    e.b_mn = 1;
+    e.P = P;
+    e.M = M;
+    e.N = N;
+    e.out = dD.p;
+    tc_gemm_i8(dA.p, M, ld, dB.p, N, P, K, e, 0);
+    DRZG_CUDA(cudaDeviceSynchronize());
+    DRZG_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
   });
 }

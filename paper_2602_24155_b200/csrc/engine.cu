@@ -34,6 +34,15 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     bool want_tc = !(g && std::string(g) == "dp4a");
     int maxv = 0;
     for (int v : T.sys.val) maxv = std::max(maxv, v);
+    // |c_{k+1}| <= (127 + |c_k| + R (q-1)/2) / q  =>  |c| <= (127 + R (q-1)/2) / (q-1)
+    i64 R = 0;
+    for (int r = 0; r < T.nL; ++r) {
+      i64 rs = 0;
+      for (int e2 = T.sys.rowptr[r]; e2 < T.sys.rowptr[r + 1]; ++e2) rs += std::abs(T.sys.val[e2]);
+      R = std::max(R, rs);
+    }
+    i64 cmax = (127 + R * (T.dp.q - 1) / 2) / (T.dp.q - 1) + 1;
+    DRZG_REQUIRE(cmax < 32767, "engine: Dixon carries exceed int16");
     if (want_tc && maxv < 256) {
       std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);
       for (int r = 0; r < T.nL; ++r)
@@ -100,6 +109,7 @@ void ReductionEngine::grow_pool(int need) {
     Y_.release();
     IN_.release();
     Cy_.release();
+    W_.release();
     bcap_ = 0;
     DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   }
@@ -128,103 +138,152 @@ int ReductionEngine::alloc_slot() {
 void ReductionEngine::ensure_batch(int B) {
   if (B <= bcap_) return;
   const int Ld = T_->dp.Ld;
-  size_t per = (size_t)(2 * Ld + 1) * nLp_ + sizeof(int) * T_->nL;
+  size_t per = (size_t)(2 * Ld + 1) * nLp_ + sizeof(int16_t) * nLp_ + (size_t)Ld * sidep_;
   size_t fr = 0, tot = 0;
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   // temporaries get at most half of what is free, in multiples of 64 states
   size_t lim = std::max<size_t>(64, (size_t)(fr * 0.8) / per / 64 * 64);
+  lim = std::min<size_t>(lim, (size_t)1 << 21);  // grid.y = states / 32 stays < 65536
   int nb = (int)std::min<size_t>(lim, (size_t)round_up(B, 64));
   if (nb <= bcap_) return;
   bcap_ = nb;
+  // state-contiguous layouts with pitch bcap_: Bg/Y Ld x nLp x P, IN/Cy nLp x P
   Bg_.alloc((size_t)bcap_ * Ld * nLp_);
   Y_.alloc((size_t)bcap_ * Ld * nLp_);
   IN_.alloc((size_t)bcap_ * nLp_);
-  Cy_.alloc((size_t)bcap_ * T_->nL);
+  Cy_.alloc((size_t)bcap_ * nLp_);
+  W_.alloc((size_t)bcap_ * Ld * sidep_);
   // K padding of Bg / IN / Y must read as zero
   DRZG_CUDA(cudaMemsetAsync(Bg_.p, 0, Bg_.n, st_));
   DRZG_CUDA(cudaMemsetAsync(Y_.p, 0, Y_.n, st_));
   DRZG_CUDA(cudaMemsetAsync(IN_.p, 0, IN_.n, st_));
+  DRZG_CUDA(cudaMemsetAsync(Cy_.p, 0, Cy_.n * sizeof(int16_t), st_));
 }
 
-void ReductionEngine::step(int B, int y) {
+dev::StepArgs ReductionEngine::make_args(int b0, int nb, int y) {
   const RuvTables& T = *T_;
-  ensure_batch(std::min(B, 1 << 30));
-  for (int b0 = 0; b0 < B; b0 += bcap_) {
-    int nb = std::min(bcap_, B - b0);
-    dev::StepArgs a;
-    a.C = C_.p;
-    a.jp_ptr = jp_ptr_.p;
-    a.jp_col = jp_col_.p;
-    a.jp_val = jp_val_.p;
-    a.gidx = gidx_.p;
-    a.dirs = dirs_.p;
-    a.t_ptr = t_ptr_.p;
-    a.t_src = t_src_.p;
-    a.sol_i = sol_i_.p;
-    a.sol_mu = sol_mu_.p;
-    a.nv = T.nv;
-    a.nL = T.nL;
-    a.nLp = nLp_;
-    a.side = T.side;
-    a.sidep = sidep_;
-    a.Ld = T.dp.Ld;
-    a.q = T.dp.q;
-    a.fq = FastQ::make(T.dp.q);
-    a.pool = pool_;
-    a.slot_stride = slot_stride_;
-    a.slot = d_slot_.p + b0;
-    a.vdir = d_vdir_.p + b0;
-    a.u0 = d_u0_.p + (size_t)b0 * T.nv;
-    a.y = y;
-    a.B = nb;
-    a.Bg = Bg_.p;
-    a.IN = IN_.p;
-    a.Cy = Cy_.p;
-    a.Y = Y_.p;
-    dim3 gL((unsigned)((T.nL + 127) / 128) * nb);
-    timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 128, 0, st_>>>(a); });
-    dim3 gG((nb + 63) / 64, nLp_ / 64);
-    for (int k = 0; k < T.dp.Ld; ++k) {
-      if (use_tc_) {
-        // y_k = bal(Cq . in_k): tcgen05 int8, digit epilogue
-        TcEpiArgs e;
-        e.mode = (int)TcEpilogue::digit;
-        e.M = T.nL;
-        e.N = nb;
-        e.q = T.dp.q;
-        e.fq = FastQ::make(T.dp.q);
-        e.Ld = T.dp.Ld;
-        e.k = k;
-        e.nLp = nLp_;
-        e.nL = T.nL;
-        e.Y = Y_.p;
-        timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, IN_.p, nb, nLp_, nLp_, e, st_); });
+  dev::StepArgs a;
+  a.C = C_.p;
+  a.jp_ptr = jp_ptr_.p;
+  a.jp_col = jp_col_.p;
+  a.jp_val = jp_val_.p;
+  a.gidx = gidx_.p;
+  a.dirs = dirs_.p;
+  a.t_ptr = t_ptr_.p;
+  a.t_src = t_src_.p;
+  a.sol_i = sol_i_.p;
+  a.sol_mu = sol_mu_.p;
+  a.nv = T.nv;
+  a.nL = T.nL;
+  a.nLp = nLp_;
+  a.side = T.side;
+  a.sidep = sidep_;
+  a.Ld = T.dp.Ld;
+  a.q = T.dp.q;
+  a.fq = FastQ::make(T.dp.q);
+  a.pool = pool_;
+  a.slot_stride = slot_stride_;
+  a.slot = d_slot_.p + b0;
+  a.vdir = d_vdir_.p + b0;
+  a.u0 = d_u0_.p + (size_t)b0 * T.nv;
+  a.y = y;
+  a.B = nb;
+  a.P = bcap_;
+  a.Bg = Bg_.p;
+  a.IN = IN_.p;
+  a.Cy = Cy_.p;
+  a.Y = Y_.p;
+  a.W = W_.p;
+  return a;
+}
+
+// Dixon solve of the batch's gathered digits (Bg, in_0, c_0 = 0) into Y
+void ReductionEngine::dixon(dev::StepArgs& a) {
+  const RuvTables& T = *T_;
+  const int nb = a.B;
+  dim3 gG((nb + 63) / 64, nLp_ / 64);
+  dim3 gC((nb + 127) / 128, T.nL);
+  for (int k = 0; k < T.dp.Ld; ++k) {
+    if (use_tc_) {
+      // y_k = bal(Cq . in_k): tcgen05 int8, digit epilogue
+      TcEpiArgs e;
+      e.mode = (int)TcEpilogue::digit;
+      e.M = T.nL;
+      e.N = nb;
+      e.q = T.dp.q;
+      e.fq = FastQ::make(T.dp.q);
+      e.Ld = T.dp.Ld;
+      e.k = k;
+      e.nLp = nLp_;
+      e.nL = T.nL;
+      e.Y = Y_.p;
+      e.b_mn = 1;
+      e.P = bcap_;
+      timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, IN_.p, nb, bcap_, nLp_, e, st_); });
+      ++clock.gemm_launches;
+      clock.gemm_macs += (double)T.nL * T.nL * nb;
+      if (k + 1 < T.dp.Ld) {
+        // c_{k+1} = (b_k + c_k - Jp . y_k) / q, in_{k+1}: tcgen05 int8 (u8 Jp), carry epilogue
+        e.mode = (int)TcEpilogue::carry;
+        e.a_unsigned = 1;
+        e.Bg = Bg_.p;
+        e.Cy = Cy_.p;
+        e.IN = IN_.p;
+        timed(&clock.carry_ms, [&] {
+          tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
+        });
         ++clock.gemm_launches;
         clock.gemm_macs += (double)T.nL * T.nL * nb;
-        if (k + 1 < T.dp.Ld) {
-          // c_{k+1} = (b_k + c_k - Jp . y_k) / q, in_{k+1}: tcgen05 int8, carry epilogue
-          e.mode = (int)TcEpilogue::carry;
-          e.a_unsigned = 1;
-          e.Bg = Bg_.p;
-          e.Cy = Cy_.p;
-          e.IN = IN_.p;
-          timed(&clock.carry_ms, [&] {
-            tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_, nb, T.dp.Ld * nLp_, nLp_, e, st_);
-          });
-          ++clock.gemm_launches;
-          clock.gemm_macs += (double)T.nL * T.nL * nb;
-        }
-      } else {
-        timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });
-        ++clock.gemm_launches;
-        clock.gemm_macs += (double)T.nL * T.nL * nb;
-        timed(&clock.carry_ms, [&] { dev::dixon_carry_kernel<<<gL, 128, 0, st_>>>(a, k); });
       }
+    } else {
+      timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });
+      ++clock.gemm_launches;
+      clock.gemm_macs += (double)T.nL * T.nL * nb;
+      timed(&clock.carry_ms, [&] { dev::dixon_carry_kernel<<<gC, 128, 0, st_>>>(a, k); });
     }
-    dim3 gS((unsigned)((T.side + 127) / 128) * nb);
-    timed(&clock.epi_ms, [&] { dev::epilogue_kernel<<<gS, 128, 0, st_>>>(a); });
-    DRZG_CUDA(cudaGetLastError());
   }
+}
+
+i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
+  const RuvTables& T = *T_;
+  const int B = (int)ks.size();
+  if (B == 0) return 0;
+  ensure_batch(B);
+  i64 mv = 0;
+  for (int b0 = 0; b0 < B; b0 += bcap_) {
+    const int nb = std::min(bcap_, B - b0);
+    // prefix sizes: states of this sub-batch still stepping at y
+    auto count_ge = [&](i64 y) {
+      int c = 0;
+      while (c < nb && ks[b0 + c] >= y) ++c;
+      return c;
+    };
+    const i64 kmax = ks[b0];
+    int By = nb;
+    for (i64 y = 1; y <= kmax; ++y) {
+      dev::StepArgs a = make_args(b0, By, (int)y);
+      if (y == 1) {
+        dim3 gL((T.nL + dev::kGatherRows - 1) / dev::kGatherRows, (By + dev::kGatherStates - 1) / dev::kGatherStates);
+        timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 256, 0, st_>>>(a); });
+      } else {
+        dim3 gW((By + 31) / 32, (T.nL + 63) / 64);
+        timed(&clock.gather_ms, [&] { dev::gather_w_kernel<<<gW, 256, 0, st_>>>(a); });
+      }
+      dixon(a);
+      dim3 gE((By + 31) / 32, (T.side + 63) / 64);
+      timed(&clock.epi_ms, [&] { dev::epilogue_kernel<<<gE, 256, 0, st_>>>(a); });
+      mv += By;
+      const int Bn = count_ge(y + 1);
+      if (Bn < By) {
+        dim3 gF((By - Bn + dev::kFlushStates - 1) / dev::kFlushStates, (T.side + dev::kFlushRows - 1) / dev::kFlushRows);
+        size_t fsm = (size_t)T.dp.Ld * dev::kFlushRows * dev::kFlushStates;
+        timed(&clock.epi_ms, [&] { dev::flush_kernel<<<gF, 256, fsm, st_>>>(a, Bn, By); });
+      }
+      By = Bn;
+      DRZG_CUDA(cudaGetLastError());
+    }
+  }
+  return mv;
 }
 
 void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led) {
@@ -377,23 +436,20 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
     std::vector<int> order(front.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return kk[a] > kk[b]; });
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int a, int b) { return kk[a] != kk[b] ? kk[a] > kk[b] : vd[a] < vd[b]; });
     std::vector<int> hslot, hvdir, hu0;
+    std::vector<i64> ks;
     for (int i : order) {
       hslot.push_back(front[i].slot);
       hvdir.push_back(vd[i]);
+      ks.push_back(kk[i]);
       for (int j = 0; j < nv; ++j) hu0.push_back(front[i].u[j]);
     }
     d_slot_.upload(hslot, st_);
     d_vdir_.upload(hvdir, st_);
     d_u0_.upload(hu0, st_);
-    i64 kmax = front.empty() ? 0 : kk[order[0]];
-    int B = (int)front.size();
-    for (i64 y = 1; y <= kmax; ++y) {
-      while (B > 0 && kk[order[B - 1]] < y) --B;
-      step(B, (int)y);
-      led.matvecs += B;
-    }
+    led.matvecs += run_sweep(ks);
     led.startups += (i64)front.size();
     // land every state at pole P - k
     std::vector<int> fs, fc, fu;
@@ -461,9 +517,12 @@ void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<
   }
   std::vector<int> order(B);
   for (int i = 0; i < B; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return k[a] > k[b]; });
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return k[a] != k[b] ? k[a] > k[b] : vdir[a] < vdir[b]; });
   std::vector<int> hslot, hvdir, hu0;
+  std::vector<i64> ks;
   for (int i : order) {
+    ks.push_back(k[i]);
     DRZG_REQUIRE(k[i] >= 1, "reduce_chunk: empty chunk");
     DRZG_REQUIRE(legal(T.d, u[i], dirs_host_[vdir[i]], k[i], T.S), "reduce_chunk: illegal move");
     hslot.push_back(slots[i]);
@@ -473,13 +532,7 @@ void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<
   d_slot_.upload(hslot, st_);
   d_vdir_.upload(hvdir, st_);
   d_u0_.upload(hu0, st_);
-  int Bc = B;
-  i64 kmax = B ? k[order[0]] : 0;
-  for (i64 y = 1; y <= kmax; ++y) {
-    while (Bc > 0 && k[order[Bc - 1]] < y) --Bc;
-    step(Bc, (int)y);
-    led.matvecs += Bc;
-  }
+  led.matvecs += run_sweep(ks);
   led.startups += B;
   for (int i = 0; i < B; ++i) {
     DRZG_CUDA(cudaMemcpyAsync(stage.data(), pool_ + (size_t)slots[i] * slot_stride_, stage.size(),

@@ -13,7 +13,7 @@
 #include <vector>
 
 #include "host/final.hpp"
-namespace drzg { namespace dev { constexpr int kLdMax = 32; } }
+#include "kernels/step_args.cuh"
 
 namespace drzg {
 
@@ -109,8 +109,12 @@ class ReductionEngine {
   void free_slot(int s) { free_.push_back(s); }
   void grow_pool(int need);
   void ensure_batch(int B);
-  // one pole drop for states [0, B) of the current sweep arrays
-  void step(int B, int y);
+  // all chunk steps of the uploaded sweep (states sorted by k desc, then v):
+  // per sub-batch, gather once from the pool, keep the state in W between
+  // steps, flush to the pool where each chunk ends; returns matvecs
+  i64 run_sweep(const std::vector<i64>& k_sorted);
+  dev::StepArgs make_args(int b0, int nb, int y);
+  void dixon(dev::StepArgs& a);
   void timed(double* acc, const std::function<void()>& f);
 
   const RuvTables* T_;
@@ -135,7 +139,8 @@ class ReductionEngine {
   // temporaries
   int bcap_ = 0;
   DevBuf<int8_t> Bg_, IN_, Y_;
-  DevBuf<int> Cy_;
+  DevBuf<int16_t> Cy_;
+  DevBuf<int8_t> W_;
   cudaEvent_t ev0_, ev1_;
   std::vector<Expo> dirs_host_;
 };

@@ -18,12 +18,10 @@
 #include <stdint.h>
 
 #include "fastq.cuh"
+#include "step_args.cuh"
 
 namespace drzg {
 namespace dev {
-
-constexpr int kLdMaxK = 32;
-static_assert(kLdMaxK == kLdMax, "digit plane bound");
 
 __device__ __forceinline__ int balmod(int x, int q) {
   int r = x % q;
@@ -32,133 +30,183 @@ __device__ __forceinline__ int balmod(int x, int q) {
   return r;
 }
 
-struct StepArgs {
-  // tables
-  const int8_t* C;        // nLp x nLp (row-major), Jp^{-1} mod q
-  const int* jp_ptr;      // nL + 1
-  const int* jp_col;
-  const int* jp_val;
-  const int* gidx;        // ndir x nL
-  const int* dirs;        // ndir x nv exponents of each v
-  const int* t_ptr;       // side + 1
-  const int* t_src;       // solution index feeding each side row
-  const int* sol_i;       // per solution index: variable i of its generator
-  const int* sol_mu;      // ... and mu_i
-  int nv, nL, nLp, side, sidep, Ld, q;
-  FastQ fq;
-  // state pool
-  int8_t* pool;           // slots x (Ld * sidep)
-  long long slot_stride;  // Ld * sidep
-  // batch
-  const int* slot;        // B
-  const int* vdir;        // B
-  const int* u0;          // B x nv (exponent at sweep start)
-  int y;                  // step index within the chunk: x = u0 - y v
-  int B;
-  // temporaries
-  int8_t* Bg;             // B x Ld x nLp
-  int8_t* IN;             // B x nLp
-  int* Cy;                // B x nL
-  int8_t* Y;              // B x Ld x nLp
-};
-
-__global__ void gather_kernel(StepArgs a) {
-  const int nrb = (a.nL + blockDim.x - 1) / blockDim.x;  // flattened (state, row block)
-  int s = blockIdx.x / nrb;
-  int r = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
-  if (r >= a.nL || s >= a.B) return;
-  int g = a.gidx[(size_t)a.vdir[s] * a.nL + r];
-  const int8_t* src = a.pool + (size_t)a.slot[s] * a.slot_stride;
-  int8_t* dst = a.Bg + (size_t)s * a.Ld * a.nLp;
-  for (int t = 0; t < a.Ld; ++t) dst[(size_t)t * a.nLp + r] = g >= 0 ? src[(size_t)t * a.sidep + g] : 0;
-  a.IN[(size_t)s * a.nLp + r] = (int8_t)a.fq.bal(g >= 0 ? src[g] : 0);
-  a.Cy[(size_t)s * a.nL + r] = 0;
+// b = P_v w for 32 states x 256 rows per block, transposed through shared
+// memory so the Bg / IN / Cy writes are state-contiguous
+__global__ void __launch_bounds__(256) gather_kernel(StepArgs a) {
+  __shared__ int8_t tile[kGatherRows][kGatherStates + 4];
+  __shared__ int vd[kGatherStates];
+  __shared__ long long base[kGatherStates];
+  const int r0 = blockIdx.x * kGatherRows, s0 = blockIdx.y * kGatherStates;
+  const int tid = threadIdx.x, r = r0 + tid;
+  if (tid < kGatherStates) {
+    int s = s0 + tid;
+    vd[tid] = s < a.B ? a.vdir[s] : -1;
+    base[tid] = s < a.B ? (long long)a.slot[s] * a.slot_stride : 0;
+  }
+  __syncthreads();
+  int g[kGatherStates];
+#pragma unroll
+  for (int i = 0; i < kGatherStates; ++i) g[i] = (r < a.nL && vd[i] >= 0) ? a.gidx[(size_t)vd[i] * a.nL + r] : -1;
+  for (int t = 0; t < a.Ld; ++t) {
+#pragma unroll
+    for (int i = 0; i < kGatherStates; ++i)
+      tile[tid][i] = g[i] >= 0 ? a.pool[base[i] + (size_t)t * a.sidep + g[i]] : (int8_t)0;
+    __syncthreads();
+    // 256 rows x 32 bytes = 2048 words; 8 per thread, row-contiguous
+    for (int e = tid; e < kGatherRows * kGatherStates / 4; e += 256) {
+      int row = e >> 3, w = e & 7;
+      int rr = r0 + row;
+      if (rr >= a.nL) continue;
+      uint32_t word = *reinterpret_cast<const uint32_t*>(&tile[row][w * 4]);
+      size_t off = (size_t)rr * a.P + s0 + w * 4;
+      *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * a.nLp * a.P + off) = word;
+      if (t == 0) {
+        uint32_t inw = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          inw |= (uint32_t)(uint8_t)(int8_t)a.fq.bal((int8_t)(word >> (8 * b))) << (8 * b);
+        *reinterpret_cast<uint32_t*>(a.IN + off) = inw;
+        *reinterpret_cast<uint2*>(a.Cy + off) = make_uint2(0, 0);
+      }
+    }
+    __syncthreads();
+  }
 }
 
-// Y[s][k][r] = bal( sum_j C[r][j] * IN[s][j] ), 64x64 tile, K step 64 bytes,
-// 256 threads each owning a 4x4 block, int8 dot products via dp4a
+// CUDA-core fallback (DRZG_GEMM=dp4a, or Jp entries >= 256):
+// Y[k][r][s] = bal( sum_j C[r][j] * IN[j][s] ), 64 x 64 tiles
 __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
-  __shared__ int Cs[64][17];
-  __shared__ int Is[64][17];
+  __shared__ int8_t Cs[64][68];
+  __shared__ int8_t Is[64][68];  // [j][s]
   const int r0 = blockIdx.y * 64, s0 = blockIdx.x * 64;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   int acc[4][4] = {};
-  const int words = a.nLp >> 2;
-  for (int kw = 0; kw < words; kw += 16) {
-    // load 64 rows x 16 words of each operand: 1024 words, 4 per thread
-    for (int l = tid; l < 1024; l += 256) {
-      int row = l >> 4, w = l & 15;
-      Cs[row][w] = reinterpret_cast<const int*>(a.C + (size_t)(r0 + row) * a.nLp)[kw + w];
-      int s = s0 + row;
-      Is[row][w] = s < a.B ? reinterpret_cast<const int*>(a.IN + (size_t)s * a.nLp)[kw + w] : 0;
+  for (int j0 = 0; j0 < a.nLp; j0 += 64) {
+    for (int l = tid; l < 64 * 64; l += 256) {
+      int rr = l >> 6, cc = l & 63;
+      Cs[rr][cc] = a.C[(size_t)(r0 + rr) * a.nLp + j0 + cc];
+      Is[rr][cc] = s0 + cc < a.P ? a.IN[(size_t)(j0 + rr) * a.P + s0 + cc] : (int8_t)0;
     }
     __syncthreads();
+    for (int j = 0; j < 64; ++j) {
+      int cv[4], iv[4];
 #pragma unroll
-    for (int w = 0; w < 16; ++w) {
-      int ca[4], ib[4];
+      for (int i = 0; i < 4; ++i) cv[i] = Cs[ty * 4 + i][j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) ca[i] = Cs[ty * 4 + i][w];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) ib[j] = Is[tx * 4 + j][w];
+      for (int i = 0; i < 4; ++i) iv[i] = Is[j][tx * 4 + i];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = __dp4a(ca[i], ib[j], acc[i][j]);
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] += cv[i] * iv[jj];
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    int s = s0 + tx * 4 + j;
-    if (s >= a.B) continue;
-    int8_t* yrow = a.Y + ((size_t)s * a.Ld + k) * a.nLp;
+  for (int i = 0; i < 4; ++i) {
+    int r = r0 + ty * 4 + i;
+    if (r >= a.nL) continue;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      int r = r0 + ty * 4 + i;
-      if (r < a.nL) yrow[r] = (int8_t)balmod(acc[i][j], a.q);
+    for (int jj = 0; jj < 4; ++jj) {
+      int s = s0 + tx * 4 + jj;
+      if (s < a.B) a.Y[((size_t)k * a.nLp + r) * a.P + s] = (int8_t)a.fq.bal(acc[i][jj]);
     }
   }
 }
 
 __global__ void dixon_carry_kernel(StepArgs a, int k) {
-  const int nrb = (a.nL + blockDim.x - 1) / blockDim.x;  // flattened (state, row block)
-  int s = blockIdx.x / nrb;
-  int r = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
-  if (r >= a.nL || s >= a.B) return;
-  const int8_t* y = a.Y + ((size_t)s * a.Ld + k) * a.nLp;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (s >= a.B || r >= a.nL) return;
+  const int8_t* y = a.Y + (size_t)k * a.nLp * a.P;
   int sum = 0;
-  for (int e = a.jp_ptr[r]; e < a.jp_ptr[r + 1]; ++e) sum += a.jp_val[e] * (int)y[a.jp_col[e]];
-  const int8_t* bg = a.Bg + (size_t)s * a.Ld * a.nLp;
-  int num = (int)bg[(size_t)k * a.nLp + r] + a.Cy[(size_t)s * a.nL + r] - sum;
-  int c = num / a.q;  // exact
-  a.Cy[(size_t)s * a.nL + r] = c;
-  if (k + 1 < a.Ld) a.IN[(size_t)s * a.nLp + r] = (int8_t)balmod((int)bg[(size_t)(k + 1) * a.nLp + r] + c, a.q);
+  for (int e = a.jp_ptr[r]; e < a.jp_ptr[r + 1]; ++e) sum += a.jp_val[e] * (int)y[(size_t)a.jp_col[e] * a.P + s];
+  size_t off = (size_t)r * a.P + s;
+  int rem;
+  int c = a.fq.divfloor((int)a.Bg[(size_t)k * a.nLp * a.P + off] + (int)a.Cy[off] - sum, rem);
+  a.Cy[off] = (int16_t)c;
+  if (k + 1 < a.Ld) a.IN[off] = (int8_t)a.fq.bal((int)a.Bg[(size_t)(k + 1) * a.nLp * a.P + off] + c);
 }
 
-__global__ void epilogue_kernel(StepArgs a) {
-  const int nrb = (a.side + blockDim.x - 1) / blockDim.x;
-  int s = blockIdx.x / nrb;
-  int g = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
-  if (g >= a.side || s >= a.B) return;
-  int x[6];
-  const int* v = a.dirs + (size_t)a.vdir[s] * a.nv;
-  for (int i = 0; i < a.nv; ++i) x[i] = a.u0[(size_t)s * a.nv + i] - a.y * v[i];
-  int acc[kLdMax];
-  for (int t = 0; t < a.Ld; ++t) acc[t] = 0;
-  const int8_t* ys = a.Y + (size_t)s * a.Ld * a.nLp;
-  for (int e = a.t_ptr[g]; e < a.t_ptr[g + 1]; ++e) {
-    int r = a.t_src[e];
-    int wgt = x[a.sol_i[r]] + a.sol_mu[r];
-    for (int t = 0; t < a.Ld; ++t) acc[t] += wgt * (int)ys[(size_t)t * a.nLp + r];
+// b = P_v W for the second and later steps of a chunk: lanes are states of
+// one (k, v)-sorted batch, so neighbouring lanes usually share v and read the
+// same W row: both sides state-contiguous
+__global__ void __launch_bounds__(256) gather_w_kernel(StepArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * 32 + lane;
+  if (s >= a.B) return;
+  const int vd = a.vdir[s];
+  const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
+  for (int r = blockIdx.y * 64 + warp; r < min(a.nL, (int)(blockIdx.y + 1) * 64); r += 8) {
+    const int g = a.gidx[(size_t)vd * a.nL + r];
+    const size_t off = (size_t)r * a.P + s;
+    int8_t b0 = 0;
+    for (int t = 0; t < a.Ld; ++t) {
+      int8_t bt = g >= 0 ? a.W[(size_t)t * wplane + (size_t)g * a.P + s] : (int8_t)0;
+      a.Bg[(size_t)t * plane + off] = bt;
+      if (t == 0) b0 = bt;
+    }
+    a.IN[off] = (int8_t)a.fq.bal(b0);
+    a.Cy[off] = 0;
   }
-  int8_t* out = a.pool + (size_t)a.slot[s] * a.slot_stride;
-  int carry = 0;
-  for (int t = 0; t < a.Ld; ++t) {
-    int r;
-    int qt = a.fq.divfloor(acc[t] + carry, r);
-    if (r > (a.q >> 1)) r -= a.q, ++qt;
-    carry = qt;
-    out[(size_t)t * a.sidep + g] = (int8_t)r;
+}
+
+// w' = T_x y into W (Ld x sidep x P), carry-normalised digits; lanes = states
+__global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * 32 + lane;
+  if (s >= a.B) return;
+  int x[6] = {0, 0, 0, 0, 0, 0};
+  {
+    const int* v = a.dirs + (size_t)a.vdir[s] * a.nv;
+    for (int i = 0; i < a.nv; ++i) x[i] = a.u0[(size_t)s * a.nv + i] - a.y * v[i];
+  }
+  const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
+  for (int g = blockIdx.y * 64 + warp; g < min(a.side, (int)(blockIdx.y + 1) * 64); g += 8) {
+    int acc[kLdMax];
+    for (int t = 0; t < a.Ld; ++t) acc[t] = 0;
+    for (int e = a.t_ptr[g]; e < a.t_ptr[g + 1]; ++e) {
+      int r = a.t_src[e];
+      int wgt = x[a.sol_i[r]] + a.sol_mu[r];
+      const int8_t* yr = a.Y + (size_t)r * a.P + s;
+      for (int t = 0; t < a.Ld; ++t) acc[t] += wgt * (int)yr[(size_t)t * plane];
+    }
+    int carry = 0;
+    for (int t = 0; t < a.Ld; ++t) {
+      int rr;
+      int qt = a.fq.divfloor(acc[t] + carry, rr);
+      if (rr > (a.q >> 1)) rr -= a.q, ++qt;
+      carry = qt;
+      a.W[(size_t)t * wplane + (size_t)g * a.P + s] = (int8_t)rr;
+    }
+  }
+}
+
+// W -> slot pool for the batch columns [s_lo, s_hi) whose chunk ends here:
+// 32 states x 64 side rows per block, transposed through shared memory
+__global__ void __launch_bounds__(256) flush_kernel(StepArgs a, int s_lo, int s_hi) {
+  extern __shared__ int8_t ft[];  // Ld x kFlushRows x kFlushStates
+  const int g0 = blockIdx.y * kFlushRows, s0 = s_lo + blockIdx.x * kFlushStates;
+  const size_t wplane = (size_t)a.sidep * a.P;
+  for (int e = threadIdx.x; e < a.Ld * kFlushRows * kFlushStates; e += 256) {
+    int sl = e % kFlushStates, gl = (e / kFlushStates) % kFlushRows, t = e / (kFlushStates * kFlushRows);
+    int g = g0 + gl, s = s0 + sl;
+    ft[e] = (g < a.side && s < s_hi) ? a.W[(size_t)t * wplane + (size_t)g * a.P + s] : (int8_t)0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;  // lane = state
+  const int s = s0 + lane;
+  if (s >= s_hi) return;
+  int8_t* dst = a.pool + (size_t)a.slot[s] * a.slot_stride;
+  for (int t = grp; t < a.Ld; t += 8) {
+    for (int w = 0; w < kFlushRows / 4; ++w) {
+      int g = g0 + w * 4;
+      if (g >= a.side) break;
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        word |= (uint32_t)(uint8_t)ft[((size_t)t * kFlushRows + w * 4 + b) * kFlushStates + lane] << (8 * b);
+      *reinterpret_cast<uint32_t*>(dst + (size_t)t * a.sidep + g) = word;
+    }
   }
 }
 

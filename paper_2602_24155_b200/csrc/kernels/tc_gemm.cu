@@ -60,6 +60,18 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
   d |= (uint64_t)2 << 61;            // SWIZZLE_128B
   return d;
 }
+// MN-major 128B-swizzled operand: rows of 128 B along N, 8-row K groups 1 KB
+// apart (SBO), 128-wide N atoms 16 KB apart (LBO); one MMA (K = 32) spans
+// four K groups
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((BN / 2 * BK) >> 4) << 16;  // LBO: next N atom
+  d |= (uint64_t)(1024 >> 4) << 32;           // SBO: next 8-row K group
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accumulate) {
   asm volatile(
@@ -153,7 +165,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t fb = smem_u32(&full[s]);
           mbar_expect_tx(fb, A_BYTES + B_BYTES);
           tma_load_2d(smem_u32(sA + s * A_BYTES), &tmA, fb, kb * BK, m0);
-          tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kb * BK, n0);
+          if (epi.b_mn) {
+            // K x N operand: two 128-state-wide swizzle atoms per stage
+            tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, n0, kb * BK);
+            tma_load_2d(smem_u32(sB + s * B_BYTES + BN / 2 * BK), &tmB, fb, n0 + BN / 2, kb * BK);
+          } else {
+            tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kb * BK, n0);
+          }
         }
       }
     }
@@ -172,7 +190,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 32; ++kk)
-            mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
+            mma_i8(d, sw128_desc(a0 + kk * 32),
+                   epi.b_mn ? sw128_mn_desc(b0 + kk * 4096) : sw128_desc(b0 + kk * 32), idesc, (kb | kk) != 0);
           mma_commit(smem_u32(&empty[s]));
         }
         mma_commit(smem_u32(&tfull[acc]));
@@ -198,37 +217,42 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int cnt = min(16, epi.N - nb);
         if (epi.mode == (int)TcEpilogue::raw) {
           for (int j = 0; j < cnt; ++j) epi.out[(size_t)(nb + j) * epi.M + m] = v[j];
-        } else if (epi.mode == (int)TcEpilogue::digit) {
-          int8_t* y = epi.Y + ((size_t)nb * epi.Ld + epi.k) * epi.nLp + m;
-          const size_t stride = (size_t)epi.Ld * epi.nLp;
+        } else if (epi.b_mn && epi.mode == (int)TcEpilogue::digit) {
+          // Y[k][m][n0..n0+15]: one 16-byte store
+          uint32_t w4[4];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (j < cnt) y[j * stride] = (int8_t)epi.fq.bal(v[j]);
-        } else {
-          // carry: issue every load of the 16 columns before using any
-          const size_t bstride = (size_t)epi.Ld * epi.nLp;
-          const int8_t* bg = epi.Bg + (size_t)nb * bstride + (size_t)epi.k * epi.nLp + m;
-          int* cy = epi.Cy + (size_t)nb * epi.nL + m;
-          int b0[16], b1[16], cc[16];
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) word |= (uint32_t)(uint8_t)(int8_t)epi.fq.bal(v[q4 * 4 + b]) << (8 * b);
+            w4[q4] = word;
+          }
+          *reinterpret_cast<uint4*>(epi.Y + ((size_t)epi.k * epi.nLp + m) * epi.P + nb) =
+              make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        } else if (epi.b_mn) {
+          // carry on state-contiguous rows: 16-byte vector loads and stores
+          const size_t P = (size_t)epi.P;
           const bool last = epi.k + 1 >= epi.Ld;
+          uint4 bk = __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)epi.k * epi.nLp + m) * P + nb));
+          uint4 bk1 = last ? make_uint4(0, 0, 0, 0)
+                           : __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P + nb));
+          uint4* cyp = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
+          uint4 c4[2] = {cyp[0], cyp[1]};
+          const int8_t* b0 = reinterpret_cast<const int8_t*>(&bk);
+          const int8_t* b1 = reinterpret_cast<const int8_t*>(&bk1);
+          int16_t* cc = reinterpret_cast<int16_t*>(c4);
+          uint32_t in4[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            if (j < cnt) {
-              b0[j] = __ldg(bg + j * bstride);
-              b1[j] = last ? 0 : __ldg(bg + j * bstride + epi.nLp);
-              cc[j] = cy[(size_t)j * epi.nL];
-            }
+            int rem;
+            int cnew = epi.fq.divfloor((int)b0[j] + (int)cc[j] - v[j], rem);  // exact
+            cc[j] = (int16_t)cnew;
+            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)epi.fq.bal((int)b1[j] + cnew) << (8 * (j & 3));
           }
-          int8_t* in = epi.IN + (size_t)nb * epi.nLp + m;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j < cnt) {
-              int rem;
-              int cnew = epi.fq.divfloor(b0[j] + cc[j] - v[j], rem);  // exact: rem == 0
-              cy[(size_t)j * epi.nL] = cnew;
-              if (!last) in[(size_t)j * epi.nLp] = (int8_t)epi.fq.bal(b1[j] + cnew);
-            }
-          }
+          cyp[0] = c4[0];
+          cyp[1] = c4[1];
+          if (!last)
+            *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
         }
       }
       // all of this warp's TMEM reads of buffer `acc` are complete
@@ -278,11 +302,13 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
   DRZG_REQUIRE(lda % 16 == 0 && ldb % 16 == 0, "tc_gemm: row pitch must be a multiple of 16 bytes");
   DRZG_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0, "tc_gemm: operands must be 16-byte aligned");
   CUtensorMap ma = make_map(A, rowsA, lda, K, tc::BM);
-  CUtensorMap mb = make_map(B, rowsB, ldb, K, tc::BN);
+  CUtensorMap mb = epi.b_mn ? make_map(B, K, ldb, ldb, tc::BK)  // K rows x ldb states, box 128 x 128
+                            : make_map(B, rowsB, ldb, K, tc::BN);
   // kind::i8 instruction descriptor: D s32, A signed (Cq) or unsigned (Jp),
   // B signed, both K-major, N = BN, M = 128
   uint32_t a_signed = epi.a_unsigned ? 0u : 1u;
-  uint32_t idesc = (2u << 4) | (a_signed << 7) | (1u << 10) | ((uint32_t)(tc::BN >> 3) << 17) |
+  uint32_t idesc = (2u << 4) | (a_signed << 7) | (1u << 10) | ((uint32_t)(epi.b_mn ? 1u : 0u) << 16) |
+                   ((uint32_t)(tc::BN >> 3) << 17) |
                    ((uint32_t)(tc::BM >> 4) << 24);
   static bool attr = false;
   if (!attr) {

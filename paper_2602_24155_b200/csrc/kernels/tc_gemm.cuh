@@ -25,6 +25,8 @@ enum class TcEpilogue : int { raw = 0, digit = 1, carry = 2 };
 struct TcEpiArgs {
   int mode = 0;
   int a_unsigned = 0;      // A operand u8 (else s8)
+  int b_mn = 0;            // B stored K x N (states contiguous, "MN-major"); else N x K
+  int P = 0;               // b_mn: state pitch of every per-state array (elements)
   int M = 0, N = 0;        // valid output extent
   int q = 0, Ld = 0, k = 0;
   FastQ fq;
@@ -35,12 +37,13 @@ struct TcEpiArgs {
   int8_t* Y = nullptr;     // N x Ld x nLp
   // carry
   const int8_t* Bg = nullptr;  // N x Ld x nLp
-  int* Cy = nullptr;           // N x nL
+  int16_t* Cy = nullptr;       // (b_mn) nLp x P carries
   int8_t* IN = nullptr;        // N x nLp
 };
 
 // host side: build tensor maps and launch; A is (rowsA x K) with row pitch
-// lda bytes, B is (rowsB x K) with row pitch ldb bytes
+// lda bytes; B is (rowsB x K) with row pitch ldb bytes, or with epi.b_mn a
+// K x ldb matrix (row pitch ldb bytes, N = epi.N valid columns)
 void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB, int ldb, int K,
                 const TcEpiArgs& epi, cudaStream_t st);
 

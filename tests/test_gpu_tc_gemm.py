@@ -24,3 +24,12 @@ def test_tc_gemm_unsigned_a():
     B = rng.integers(-127, 128, size=(200, 400), dtype=np.int64)
     D = drzg.test_tc_gemm(A.astype(np.uint8), B.astype(np.int8), a_unsigned=True)
     assert (D.astype(np.int64) == B.dot(A.T)).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 128), (220, 300, 220), (3003, 513, 3003), (130, 17, 48)])
+def test_tc_gemm_mn_major_b(M, N, K):
+    rng = np.random.default_rng(M + N * 3)
+    A = rng.integers(-127, 128, size=(M, K), dtype=np.int64)
+    B = rng.integers(-127, 128, size=(N, K), dtype=np.int64)
+    D = drzg.test_tc_gemm_mn(A.astype(np.int8), B.astype(np.int8))
+    assert (D.astype(np.int64) == B.dot(A.T)).all()
