@@ -56,6 +56,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   jp_col_.upload(T.sys.col, st_);
   jp_val_.upload(T.sys.val, st_);
   gidx_.upload(T.gidx, st_);
+  ginv_.upload(T.ginv, st_);
   const auto& dl = monos(T.nv, T.d).mons;
   std::vector<int> dirs;
   for (const auto& v : dl) {
@@ -168,6 +169,8 @@ dev::StepArgs ReductionEngine::make_args(int b0, int nb, int y) {
   a.jp_col = jp_col_.p;
   a.jp_val = jp_val_.p;
   a.gidx = gidx_.p;
+  a.ginv = ginv_.p;
+  a.ks = d_k_.p + b0;
   a.dirs = dirs_.p;
   a.t_ptr = t_ptr_.p;
   a.t_src = t_src_.p;
@@ -219,7 +222,9 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
       e.Y = Y_.p;
       e.b_mn = 1;
       e.P = bcap_;
-      timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, IN_.p, nb, bcap_, nLp_, e, st_); });
+      // in_0 = bal(b_0 + 0) = b_0: digit 0 reads the gathered plane directly
+      const int8_t* in = k ? IN_.p : Bg_.p;
+      timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, in, nb, bcap_, nLp_, e, st_); });
       ++clock.gemm_launches;
       clock.gemm_macs += (double)T.nL * T.nL * nb;
       if (k + 1 < T.dp.Ld) {
@@ -265,10 +270,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
       if (y == 1) {
         dim3 gL((T.nL + dev::kGatherRows - 1) / dev::kGatherRows, (By + dev::kGatherStates - 1) / dev::kGatherStates);
         timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 256, 0, st_>>>(a); });
-      } else {
-        dim3 gW((By + 31) / 32, (T.nL + 63) / 64);
-        timed(&clock.gather_ms, [&] { dev::gather_w_kernel<<<gW, 256, 0, st_>>>(a); });
-      }
+      }  // later steps: the previous epilogue already wrote this step's operand
       dixon(a);
       dim3 gE((By + 31) / 32, (T.side + 63) / 64);
       timed(&clock.epi_ms, [&] { dev::epilogue_kernel<<<gE, 256, 0, st_>>>(a); });
@@ -449,6 +451,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     d_slot_.upload(hslot, st_);
     d_vdir_.upload(hvdir, st_);
     d_u0_.upload(hu0, st_);
+    d_k_.upload(ks, st_);
     led.matvecs += run_sweep(ks);
     led.startups += (i64)front.size();
     // land every state at pole P - k
@@ -532,6 +535,7 @@ void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<
   d_slot_.upload(hslot, st_);
   d_vdir_.upload(hvdir, st_);
   d_u0_.upload(hu0, st_);
+  d_k_.upload(ks, st_);
   led.matvecs += run_sweep(ks);
   led.startups += B;
   for (int i = 0; i < B; ++i) {

@@ -108,6 +108,7 @@ struct RuvTables {
   // per direction v (rank in Homog_d): gather table over Homog_L
   int ndir = 0;
   std::vector<i32> gidx;  // ndir x nL, rank in Homog_D or -1
+  std::vector<i32> ginv;  // ndir x side: the L-row each side row feeds, or -1
 };
 
 inline RuvTables build_tables(const Hypersurface& X, int M, const std::set<int>& Sset) {
@@ -187,6 +188,12 @@ inline RuvTables build_tables(const Hypersurface& X, int M, const std::set<int>&
     for (int r = 0; r < T.nL; ++r) {
       Expo g = Lm[r] - dirs[vi] + T.sexp;
       if (g.nonneg()) T.gidx[(size_t)vi * T.nL + r] = (i32)rank_of(g);
+    }
+  T.ginv.assign((size_t)T.ndir * T.side, -1);
+  for (int vi = 0; vi < T.ndir; ++vi)
+    for (int r = 0; r < T.nL; ++r) {
+      i32 g = T.gidx[(size_t)vi * T.nL + r];
+      if (g >= 0) T.ginv[(size_t)vi * T.side + g] = r;
     }
   return T;
 }

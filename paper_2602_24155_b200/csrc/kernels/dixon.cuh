@@ -85,7 +85,9 @@ __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
     for (int l = tid; l < 64 * 64; l += 256) {
       int rr = l >> 6, cc = l & 63;
       Cs[rr][cc] = a.C[(size_t)(r0 + rr) * a.nLp + j0 + cc];
-      Is[rr][cc] = s0 + cc < a.P ? a.IN[(size_t)(j0 + rr) * a.P + s0 + cc] : (int8_t)0;
+      // digit 0 reads b_0 itself (balanced digits, c_0 = 0)
+      const int8_t* src = k ? a.IN : a.Bg;
+      Is[rr][cc] = s0 + cc < a.P ? src[(size_t)(j0 + rr) * a.P + s0 + cc] : (int8_t)0;
     }
     __syncthreads();
     for (int j = 0; j < 64; ++j) {
@@ -122,7 +124,7 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
   for (int e = a.jp_ptr[r]; e < a.jp_ptr[r + 1]; ++e) sum += a.jp_val[e] * (int)y[(size_t)a.jp_col[e] * a.P + s];
   size_t off = (size_t)r * a.P + s;
   int rem;
-  int c = a.fq.divfloor((int)a.Bg[(size_t)k * a.nLp * a.P + off] + (int)a.Cy[off] - sum, rem);
+  int c = a.fq.divfloor((int)a.Bg[(size_t)k * a.nLp * a.P + off] + (k ? (int)a.Cy[off] : 0) - sum, rem);
   a.Cy[off] = (int16_t)c;
   if (k + 1 < a.Ld) a.IN[off] = (int8_t)a.fq.bal((int)a.Bg[(size_t)(k + 1) * a.nLp * a.P + off] + c);
 }
@@ -156,8 +158,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
   const int s = blockIdx.x * 32 + lane;
   if (s >= a.B) return;
   int x[6] = {0, 0, 0, 0, 0, 0};
+  const int vd = a.vdir[s];
+  const bool cont = a.y < a.ks[s];
   {
-    const int* v = a.dirs + (size_t)a.vdir[s] * a.nv;
+    const int* v = a.dirs + (size_t)vd * a.nv;
     for (int i = 0; i < a.nv; ++i) x[i] = a.u0[(size_t)s * a.nv + i] - a.y * v[i];
   }
   const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
@@ -170,13 +174,20 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
       const int8_t* yr = a.Y + (size_t)r * a.P + s;
       for (int t = 0; t < a.Ld; ++t) acc[t] += wgt * (int)yr[(size_t)t * plane];
     }
+    // the next step of this chunk reads row ginv[v][g] of its operand: write
+    // it there directly (lanes of a (k, v)-sorted batch share v); a state
+    // whose chunk ends here goes to W for the flush into the slot pool
+    const int rn = cont ? a.ginv[(size_t)vd * a.side + g] : -1;
     int carry = 0;
     for (int t = 0; t < a.Ld; ++t) {
       int rr;
       int qt = a.fq.divfloor(acc[t] + carry, rr);
       if (rr > (a.q >> 1)) rr -= a.q, ++qt;
       carry = qt;
-      a.W[(size_t)t * wplane + (size_t)g * a.P + s] = (int8_t)rr;
+      if (!cont)
+        a.W[(size_t)t * wplane + (size_t)g * a.P + s] = (int8_t)rr;
+      else if (rn >= 0)
+        a.Bg[(size_t)t * plane + (size_t)rn * a.P + s] = (int8_t)rr;
     }
   }
 }

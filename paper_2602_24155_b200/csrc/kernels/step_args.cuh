@@ -19,6 +19,8 @@ struct StepArgs {
   const int* jp_col;
   const int* jp_val;
   const int* gidx;        // ndir x nL
+  const int* ginv;        // ndir x side (next step's row of each side row, or -1)
+  const int64_t* ks;      // B: chunk length of each batch state
   const int* dirs;        // ndir x nv exponents of each v
   const int* t_ptr;       // side + 1
   const int* t_src;       // solution index feeding each side row

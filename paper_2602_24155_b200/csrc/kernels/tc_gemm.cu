@@ -237,7 +237,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint4 bk1 = last ? make_uint4(0, 0, 0, 0)
                            : __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P + nb));
           uint4* cyp = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
-          uint4 c4[2] = {cyp[0], cyp[1]};
+          // c_0 = 0: digit 0 ignores whatever the previous step left in Cy
+          uint4 c4[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+          if (epi.k) {
+            c4[0] = cyp[0];
+            c4[1] = cyp[1];
+          }
           const int8_t* b0 = reinterpret_cast<const int8_t*>(&bk);
           const int8_t* b1 = reinterpret_cast<const int8_t*>(&bk1);
           int16_t* cc = reinterpret_cast<int16_t*>(c4);
