@@ -111,7 +111,7 @@ std::string frob_json_body(const FrobResult& fr) {
   std::ostringstream os;
   os.precision(9);
   os << "\"b\":" << fr.b << ",\"M\":" << fr.M << ",\"digits\":{\"q\":" << fr.q << ",\"Ld\":" << fr.Ld
-     << "},\"nL\":" << fr.nL << ",\"side\":" << fr.side << ",\"terms\":" << fr.terms
+     << "},\"nL\":" << fr.nL << ",\"side\":" << fr.side << ",\"terms\":" << fr.terms << ",\"groups\":" << fr.groups
      << ",\"matvecs\":" << fr.led.matvecs << ",\"startups\":" << fr.led.startups
      << ",\"combines\":" << fr.led.combines << ",\"computed\":" << ijson(fr.computed)
      << ",\"times\":{\"tables\":" << fr.t.tables << ",\"seeds\":" << fr.t.seeds << ",\"device\":" << fr.t.device

@@ -51,12 +51,18 @@ class FinalReducer {
   FinalReducer(const Hypersurface& X, const Basis& B, const DigitPlan& dp, const HostMod& hm)
       : X_(&X), B_(&B), dp_(dp), hm_(hm) {}
 
+  // build every level up front; afterwards reduce() only reads shared state
+  // and may run concurrently on many columns
+  void prepare() {
+    for (int m = 1; m <= X_->n; ++m) level(m);
+  }
+
   // g over monos(nv, dm-n-1) as residues mod p^M; returns the b-vector
-  std::vector<Z> reduce(std::vector<Z> g, int m) {
+  std::vector<Z> reduce(std::vector<Z> g, int m) const {
     DRZG_REQUIRE(m >= 1 && m <= X_->n, "FinalReducer: pole order out of range");
     std::vector<Z> out((size_t)B_->b, Z(0));
     for (; m >= 1; --m) {
-      Level& L = level(m);
+      const Level& L = levels_.at(m);
       DRZG_REQUIRE((int)g.size() == L.rows, "FinalReducer: bad coeff size");
       std::vector<Z> sol(L.ncols, Z(0));
       if (L.rows > 0) {

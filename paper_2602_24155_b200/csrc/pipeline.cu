@@ -1,5 +1,8 @@
 // Frobenius assembly + zeta driver (see pipeline.cuh).
+#include <atomic>
 #include <chrono>
+#include <exception>
+#include <thread>
 
 #include "pipeline.cuh"
 
@@ -46,39 +49,101 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     cols.push_back(j);
   }
   out.computed = cols;
+  // column expansions in parallel host threads (the reference threads over
+  // columns too, zeta.hpp:109-133); the final reducer's levels are built
+  // meanwhile on this thread
   PowerCache pc;
-  std::vector<ColumnSeeds> seeds;
-  for (int j : cols) {
-    seeds.push_back(expand_column(X, B, plan, T, hm, pc, j));
-    out.terms += seeds.back().nterms;
+  std::vector<ColumnSeeds> seeds(cols.size());
+  FinalReducer fin(X, B, T.dp, hm);
+  {
+    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)std::thread::hardware_concurrency()));
+    std::atomic<size_t> next{0};
+    std::vector<std::exception_ptr> errs(nth);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          for (size_t i = next++; i < cols.size(); i = next++) seeds[i] = expand_column(X, B, plan, T, hm, pc, cols[i]);
+        } catch (...) {
+          errs[t] = std::current_exception();
+        }
+      });
+    fin.prepare();
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
   }
+  for (auto& s : seeds) out.terms += s.nterms;
   double t2 = now_s();
   out.t.seeds = t2 - t1;
 
-  std::vector<std::vector<i64>> G;
+  // columns run through the device engine in groups whose states fit HBM:
+  // live states stay below ~60% of a group's seeds (SURVEY 8a peaks), and a
+  // group may use half of the free memory
+  std::vector<std::vector<i64>> G(cols.size());
   {
     ReductionEngine eng(T, n, p, st);
     eng.clock.on = opt.profile;
-    if (!seeds.empty()) eng.run_pchunk(seeds, G, out.led);
+    size_t fr = 0, tot = 0;
+    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    const double slot_bytes = (double)T.dp.Ld * ((T.side + 15) / 16 * 16);
+    const double budget = 0.5 * (double)fr;
+    size_t c0 = 0;
+    while (c0 < cols.size()) {
+      size_t c1 = c0;
+      double need = 0;
+      while (c1 < cols.size()) {
+        double add = 0.6 * (double)seeds[c1].nterms * slot_bytes;
+        if (c1 > c0 && need + add > budget) break;
+        need += add;
+        ++c1;
+      }
+      std::vector<ColumnSeeds> grp(std::make_move_iterator(seeds.begin() + c0),
+                                   std::make_move_iterator(seeds.begin() + c1));
+      std::vector<std::vector<i64>> Gg;
+      eng.run_pchunk(grp, Gg, out.led);
+      for (size_t i = c0; i < c1; ++i) G[i] = std::move(Gg[i - c0]);
+      c0 = c1;
+      ++out.groups;
+    }
     eng.clock.peak_live = eng.peak_live();
     out.clk = eng.clock;
   }
   double t3 = now_s();
   out.t.device = t3 - t2;
 
-  FinalReducer fin(X, B, T.dp, hm);
   const int gsize = (int)mono_count(X.nv(), T.D - 1);
+  std::vector<std::vector<Z>> colres(cols.size());
+  {
+    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)std::thread::hardware_concurrency()));
+    std::atomic<size_t> next{0};
+    std::vector<std::exception_ptr> errs(nth);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          for (size_t ci = next++; ci < cols.size(); ci = next++) {
+            std::vector<Z> g(gsize);
+            for (int r = 0; r < gsize; ++r) {
+              i64 s[dev::kLdMax];
+              for (int tt = 0; tt < T.dp.Ld; ++tt) s[tt] = G[ci][(size_t)tt * gsize + r];
+              g[r] = from_digit_sums(s, T.dp, hm.mz);
+            }
+            colres[ci] = fin.reduce(std::move(g), n);
+          }
+        } catch (...) {
+          errs[t] = std::current_exception();
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  }
   for (size_t ci = 0; ci < cols.size(); ++ci) {
     int j = cols[ci];
     int m = B.pole_of[j];
     i64 Pmax = plan.max_pole(m);
-    std::vector<Z> g(gsize);
-    for (int r = 0; r < gsize; ++r) {
-      i64 s[dev::kLdMax];
-      for (int t = 0; t < T.dp.Ld; ++t) s[t] = G[ci][(size_t)t * gsize + r];
-      g[r] = from_digit_sums(s, T.dp, hm.mz);
-    }
-    std::vector<Z> c = fin.reduce(std::move(g), n);
+    const std::vector<Z>& c = colres[ci];
     // unscale by the unit of kappa_n = (Pmax-1)!/(n-1)! and the Mazur shift
     // (zeta.hpp:79-106)
     i64 v = factorial_valuation((u64)(Pmax - 1), p);

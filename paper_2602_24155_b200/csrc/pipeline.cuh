@@ -34,6 +34,7 @@ struct FrobResult {
   KernelClock clk;
   int M = 0, Ld = 0, q = 0, nL = 0, side = 0;
   i64 terms = 0;
+  int groups = 0;            // device passes (memory-bounded column groups)
 };
 
 FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan, const std::set<int>& S,
