@@ -346,35 +346,97 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       front = std::move(landed.begin()->second);
       landed.erase(landed.begin());
     }
-    // materialise the seeds whose pole is P
+    // materialise the seeds whose pole is P.  Seeds sharing (column, u) are
+    // combined here on the host (the reference's combine_states of those
+    // seeds, counted in the ledger) so each distinct state takes one slot;
+    // a column's first sweep keeps its seeds apart, as the reference does
     {
-      std::vector<int> ss, sg;
-      std::vector<int8_t> sd;
+      std::vector<int> ss, eptr{0}, eg;
+      std::vector<int> accd;  // Ld per entry (int sums, normalised below)
       for (int c = 0; c < ncol; ++c) {
         if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
         SeedBucket& bk = sit[c]->second;
+        const bool first_sweep = top0[c] == P;
+        std::unordered_map<u64, int> grp;  // key -> index into ss
+        std::vector<std::unordered_map<int, int>> ent;  // per new state: g -> entry
+        const size_t base_state = ss.size();
         for (size_t i = 0; i < bk.size(); ++i) {
-          HS h;
-          h.col = c;
-          h.u = Expo(nv);
-          for (int j = 0; j < nv; ++j) h.u[j] = bk.u[i * nv + j];
-          h.pole = P;
-          h.slot = alloc_slot();
-          front.push_back(h);
-          ss.push_back(h.slot);
-          sg.push_back(bk.g[i]);
+          Expo u(nv);
+          for (int j = 0; j < nv; ++j) u[j] = bk.u[i * nv + j];
+          int st;
+          auto it = first_sweep ? grp.end() : grp.find(key(c, u));
+          if (it == grp.end()) {
+            HS h;
+            h.col = c;
+            h.u = u;
+            h.pole = P;
+            h.slot = alloc_slot();
+            front.push_back(h);
+            st = (int)(ss.size() - base_state);
+            ss.push_back(h.slot);
+            ent.emplace_back();
+            if (!first_sweep) grp.emplace(key(c, u), st);
+          } else {
+            st = it->second;
+            led.combines += 1;
+          }
+          auto& em = ent[st];
+          auto eit = em.find(bk.g[i]);
+          int e;
+          if (eit == em.end()) {
+            e = (int)(eg.size());
+            em.emplace(bk.g[i], e);
+            eg.push_back(bk.g[i]);
+            accd.resize(accd.size() + Ld, 0);
+          } else {
+            e = eit->second;
+          }
+          for (int t = 0; t < Ld; ++t) accd[(size_t)e * Ld + t] += bk.dig[i * Ld + t];
         }
-        sd.insert(sd.end(), bk.dig.begin(), bk.dig.end());
+        // entries grouped by state in ss order
+        std::vector<int> order_e;
+        for (auto& em : ent) {
+          std::vector<int> es;
+          for (auto& kv : em) es.push_back(kv.second);
+          std::sort(es.begin(), es.end());
+          order_e.insert(order_e.end(), es.begin(), es.end());
+          eptr.push_back(eptr.back() + (int)es.size());
+        }
+        // permute this column's entries into state order
+        const size_t e0 = eg.size() - order_e.size();
+        std::vector<int> eg2(order_e.size()), ac2(order_e.size() * Ld);
+        for (size_t k = 0; k < order_e.size(); ++k) {
+          eg2[k] = eg[order_e[k]];
+          for (int t = 0; t < Ld; ++t) ac2[k * Ld + t] = accd[(size_t)order_e[k] * Ld + t];
+        }
+        std::copy(eg2.begin(), eg2.end(), eg.begin() + e0);
+        std::copy(ac2.begin(), ac2.end(), accd.begin() + e0 * Ld);
         SeedBucket().u.swap(bk.u);  // release host memory
+        SeedBucket().g.swap(bk.g);
+        SeedBucket().dig.swap(bk.dig);
         ++sit[c];
       }
       if (!ss.empty()) {
+        // normalise summed digits (balanced base q, top carry dropped)
+        std::vector<int8_t> ed(accd.size());
+        const int q = T.dp.q;
+        for (size_t e = 0; e < eg.size(); ++e) {
+          int carry = 0;
+          for (int t = 0; t < Ld; ++t) {
+            int v = accd[e * Ld + t] + carry;
+            int r = ((v % q) + q) % q;
+            if (r > q / 2) r -= q;
+            carry = (v - r) / q;
+            ed[e * Ld + t] = (int8_t)r;
+          }
+        }
         d_a.upload(ss, st_);
-        d_b.upload(sg, st_);
-        d_dig.upload(sd, st_);
+        d_b.upload(eptr, st_);
+        d_c.upload(eg, st_);
+        d_dig.upload(ed, st_);
         timed(&clock.other_ms, [&] {
-          dev::seed_kernel<<<(int)ss.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_dig.p,
-                                                            (int)ss.size());
+          dev::seed_kernel<<<(int)ss.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p,
+                                                            d_dig.p, (int)ss.size());
         });
       }
     }

@@ -221,16 +221,20 @@ __global__ void __launch_bounds__(256) flush_kernel(StepArgs a, int s_lo, int s_
   }
 }
 
-// one block per seed: zero its slot, then write the one-hot digits
-__global__ void seed_kernel(int8_t* pool, long long slot_stride, int sidep, int Ld, const int* slot, const int* g,
-                            const int8_t* dig, int nseeds) {
+// one block per new state: zero its slot, then write its entries (distinct
+// side rows g, Ld balanced digits each)
+__global__ void seed_kernel(int8_t* pool, long long slot_stride, int sidep, int Ld, const int* slot, const int* eptr,
+                            const int* eg, const int8_t* edig, int nstates) {
   int i = blockIdx.x;
-  if (i >= nseeds) return;
+  if (i >= nstates) return;
   int8_t* w = pool + (size_t)slot[i] * slot_stride;
   int4* w4 = reinterpret_cast<int4*>(w);
   for (long long j = threadIdx.x; j < slot_stride / 16; j += blockDim.x) w4[j] = make_int4(0, 0, 0, 0);
   __syncthreads();
-  if (threadIdx.x < Ld) w[(size_t)threadIdx.x * sidep + g[i]] = dig[(size_t)i * Ld + threadIdx.x];
+  for (int e = eptr[i] + (int)threadIdx.x / Ld; e < eptr[i + 1]; e += (int)blockDim.x / Ld) {
+    int t = (int)threadIdx.x % Ld;
+    if ((int)threadIdx.x < (int)(blockDim.x / Ld) * Ld) w[(size_t)t * sidep + eg[e]] = edig[(size_t)e * Ld + t];
+  }
 }
 
 // groups (CSR over member slots, first member receives the sum)
