@@ -328,6 +328,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   }
 
   std::map<int, std::vector<HS>, std::greater<int>> landed;
+  // per pole: key -> position in landed[pole]; a state landing on a key that
+  // is already there is combined at once (the reference combines after every
+  // sweep, reduction.hpp:502, so the ledger is unchanged)
+  std::map<int, std::unordered_map<u64, int>> landed_idx;
   std::vector<std::unordered_set<u64>> floor_keys(ncol);
   std::vector<i64> floor_arrivals(ncol, 0);
   std::vector<std::map<int, SeedBucket>::reverse_iterator> sit(ncol);
@@ -346,6 +350,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       front = std::move(landed.begin()->second);
       landed.erase(landed.begin());
     }
+    landed_idx.erase(P);
     // materialise the seeds whose pole is P.  Seeds sharing (column, u) are
     // combined here on the host (the reference's combine_states of those
     // seeds, counted in the ledger) so each distinct state takes one slot;
@@ -518,6 +523,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     led.startups += (i64)front.size();
     // land every state at pole P - k
     std::vector<int> fs, fc, fu;
+    std::unordered_map<int, std::vector<int>> merges;  // dst slot -> merged slots
     for (int i : order) {
       HS h = front[i];
       const Expo& v = dirs_host_[vd[i]];
@@ -530,8 +536,34 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         floor_arrivals[h.col]++;
         floor_keys[h.col].insert(key(h.col, h.u));
       } else {
-        landed[h.pole].push_back(h);
+        auto& idx = landed_idx[h.pole];
+        auto& lst = landed[h.pole];
+        u64 kh = key(h.col, h.u);
+        auto it = idx.find(kh);
+        if (it == idx.end()) {
+          idx.emplace(kh, (int)lst.size());
+          lst.push_back(h);
+        } else {
+          merges[lst[it->second].slot].push_back(h.slot);
+          led.combines += 1;
+        }
       }
+    }
+    if (!merges.empty()) {
+      std::vector<int> gptr{0}, mem;
+      for (auto& kv : merges) {
+        mem.push_back(kv.first);
+        mem.insert(mem.end(), kv.second.begin(), kv.second.end());
+        gptr.push_back((int)mem.size());
+      }
+      d_b.upload(gptr, st_);
+      d_c.upload(mem, st_);
+      dim3 gm((unsigned)((T.side + 127) / 128) * merges.size());
+      timed(&clock.other_ms, [&] {
+        dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_b.p, d_c.p);
+      });
+      for (auto& kv : merges)
+        for (int s : kv.second) free_slot(s);
     }
     if (!fs.empty()) {
       d_a.upload(fs, st_);
