@@ -350,13 +350,19 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       front = std::move(landed.begin()->second);
       landed.erase(landed.begin());
     }
-    landed_idx.erase(P);
+    std::unordered_map<u64, int> front_idx;  // key -> position in front (landed at P)
+    {
+      auto li = landed_idx.find(P);
+      if (li != landed_idx.end()) front_idx.swap(li->second);
+      landed_idx.erase(P);
+    }
     // materialise the seeds whose pole is P.  Seeds sharing (column, u) are
     // combined here on the host (the reference's combine_states of those
     // seeds, counted in the ledger) so each distinct state takes one slot;
     // a column's first sweep keeps its seeds apart, as the reference does
     {
       std::vector<int> ss, eptr{0}, eg;
+      std::vector<int> add_slots;  // per new group: -1 = fresh slot, else absorbed in place
       std::vector<int> accd;  // Ld per entry (int sums, normalised below)
       for (int c = 0; c < ncol; ++c) {
         if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
@@ -369,18 +375,29 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
           Expo u(nv);
           for (int j = 0; j < nv; ++j) u[j] = bk.u[i * nv + j];
           int st;
-          auto it = first_sweep ? grp.end() : grp.find(key(c, u));
+          const u64 ku = key(c, u);
+          auto it = first_sweep ? grp.end() : grp.find(ku);
           if (it == grp.end()) {
-            HS h;
-            h.col = c;
-            h.u = u;
-            h.pole = P;
-            h.slot = alloc_slot();
-            front.push_back(h);
+            // a state already landed at this pole absorbs the seed in place
+            auto fit = first_sweep ? front_idx.end() : front_idx.find(ku);
+            int slot;
+            if (fit != front_idx.end()) {
+              slot = front[fit->second].slot;
+              led.combines += 1;
+              add_slots.push_back(slot);
+            } else {
+              HS h;
+              h.col = c;
+              h.u = u;
+              h.pole = P;
+              h.slot = slot = alloc_slot();
+              front.push_back(h);
+              add_slots.push_back(-1);
+            }
             st = (int)(ss.size() - base_state);
-            ss.push_back(h.slot);
+            ss.push_back(slot);
             ent.emplace_back();
-            if (!first_sweep) grp.emplace(key(c, u), st);
+            if (!first_sweep) grp.emplace(ku, st);
           } else {
             st = it->second;
             led.combines += 1;
@@ -435,14 +452,35 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
             ed[e * Ld + t] = (int8_t)r;
           }
         }
-        d_a.upload(ss, st_);
-        d_b.upload(eptr, st_);
-        d_c.upload(eg, st_);
-        d_dig.upload(ed, st_);
-        timed(&clock.other_ms, [&] {
-          dev::seed_kernel<<<(int)ss.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p,
-                                                            d_dig.p, (int)ss.size());
-        });
+        // fresh slots are zeroed and written; absorbed groups add in place
+        for (int pass = 0; pass < 2; ++pass) {
+          std::vector<int> s2, p2{0}, g2;
+          std::vector<int8_t> d2;
+          for (size_t i = 0; i < ss.size(); ++i) {
+            if ((add_slots[i] >= 0) != (pass == 1)) continue;
+            s2.push_back(ss[i]);
+            for (int e2 = eptr[i]; e2 < eptr[i + 1]; ++e2) {
+              g2.push_back(eg[e2]);
+              d2.insert(d2.end(), ed.begin() + (size_t)e2 * Ld, ed.begin() + (size_t)(e2 + 1) * Ld);
+            }
+            p2.push_back((int)g2.size());
+          }
+          if (s2.empty()) continue;
+          d_a.upload(s2, st_);
+          d_b.upload(p2, st_);
+          d_c.upload(g2, st_);
+          d_dig.upload(d2, st_);
+          if (pass == 0)
+            timed(&clock.other_ms, [&] {
+              dev::seed_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p,
+                                                                d_dig.p, (int)s2.size());
+            });
+          else
+            timed(&clock.other_ms, [&] {
+              dev::add_entries_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, T.dp.q,
+                                                                      d_a.p, d_b.p, d_c.p, d_dig.p, (int)s2.size());
+            });
+        }
       }
     }
     // combine_states: merge equal (col, u) except in a column's first sweep

@@ -237,6 +237,25 @@ __global__ void seed_kernel(int8_t* pool, long long slot_stride, int sidep, int 
   }
 }
 
+// seeds absorbed by a state already at their pole: w[t][g] += digits, with
+// the carry normalised along t for each touched g
+__global__ void add_entries_kernel(int8_t* pool, long long slot_stride, int sidep, int Ld, int q, const int* slot,
+                                   const int* eptr, const int* eg, const int8_t* edig, int nstates) {
+  int i = blockIdx.x;
+  if (i >= nstates) return;
+  int8_t* w = pool + (size_t)slot[i] * slot_stride;
+  for (int e = eptr[i] + (int)threadIdx.x; e < eptr[i + 1]; e += blockDim.x) {
+    const int g = eg[e];
+    int carry = 0;
+    for (int t = 0; t < Ld; ++t) {
+      int v = (int)w[(size_t)t * sidep + g] + (int)edig[(size_t)e * Ld + t] + carry;
+      int r = balmod(v, q);
+      carry = (v - r) / q;
+      w[(size_t)t * sidep + g] = (int8_t)r;
+    }
+  }
+}
+
 // groups (CSR over member slots, first member receives the sum)
 __global__ void merge_kernel(int8_t* pool, long long slot_stride, int side, int sidep, int Ld, int q,
                              const int* gptr, const int* members) {
