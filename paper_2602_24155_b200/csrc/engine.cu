@@ -1,6 +1,9 @@
 // Device-resident reduction engine (see engine.cuh).
 #include <algorithm>
 #include <functional>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdlib>
 #include <map>
 #include <string>
@@ -79,7 +82,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
 }
 
 ReductionEngine::~ReductionEngine() {
-  if (pool_) cudaFree(pool_);
+  release_pool();
   cudaEventDestroy(ev0_);
   cudaEventDestroy(ev1_);
 }
@@ -99,13 +102,75 @@ void ReductionEngine::timed(double* acc, const std::function<void()>& f) {
   *acc += ms;
 }
 
+// The state pool lives in one reserved virtual range; growth maps more
+// physical memory behind it (CUDA VMM), so existing slots never move and no
+// copy (old + new pool at once) is needed
+namespace {
+struct Vmm {
+  PFN_cuMemAddressReserve_v10020 reserve = nullptr;
+  PFN_cuMemCreate_v10020 create = nullptr;
+  PFN_cuMemMap_v10020 map = nullptr;
+  PFN_cuMemSetAccess_v10020 access = nullptr;
+  PFN_cuMemGetAllocationGranularity_v10020 gran = nullptr;
+  PFN_cuMemUnmap_v10020 unmap = nullptr;
+  PFN_cuMemRelease_v10020 release = nullptr;
+  PFN_cuMemAddressFree_v10020 addr_free = nullptr;
+  static const Vmm& get() {
+    static Vmm v = [] {
+      Vmm x;
+      auto load = [](const char* name, void** fn) {
+        cudaDriverEntryPointQueryResult q;
+        DRZG_CUDA(cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q));
+        DRZG_REQUIRE(q == cudaDriverEntryPointSuccess, std::string("driver entry point ") + name);
+      };
+      load("cuMemAddressReserve", (void**)&x.reserve);
+      load("cuMemCreate", (void**)&x.create);
+      load("cuMemMap", (void**)&x.map);
+      load("cuMemSetAccess", (void**)&x.access);
+      load("cuMemGetAllocationGranularity", (void**)&x.gran);
+      load("cuMemUnmap", (void**)&x.unmap);
+      load("cuMemRelease", (void**)&x.release);
+      load("cuMemAddressFree", (void**)&x.addr_free);
+      return x;
+    }();
+    return v;
+  }
+};
+#define DRZG_CU(x)                                                                             \
+  do {                                                                                         \
+    CUresult r_ = (x);                                                                         \
+    if (r_ != CUDA_SUCCESS)                                                                    \
+      throw ::drzg::contract_error("CUDA driver error " + std::to_string((int)r_), __FILE__, __LINE__); \
+  } while (0)
+}  // namespace
+
 void ReductionEngine::grow_pool(int need) {
-  int ncap = std::max(need, cap_ + std::max(1024, cap_ / 2));
-  size_t bytes = (size_t)ncap * slot_stride_;
+  const Vmm& V = Vmm::get();
+  int dev = 0;
+  DRZG_CUDA(cudaGetDevice(&dev));
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = dev;
+  size_t gran = 0;
+  DRZG_CU(V.gran(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
   size_t fr = 0, tot = 0;
+  if (!pool_) {
+    // reserve address space for the whole device once
+    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    vmm_reserved_ = (tot + gran - 1) / gran * gran;
+    CUdeviceptr base = 0;
+    DRZG_CU(V.reserve(&base, vmm_reserved_, gran, 0, 0));
+    pool_ = reinterpret_cast<int8_t*>(base);
+    vmm_mapped_ = 0;
+  }
+  int ncap = std::max(need, cap_ + std::max(1024, cap_ / 2));
+  size_t want = (size_t)ncap * slot_stride_;
+  DRZG_CUDA(cudaStreamSynchronize(st_));
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
-  if (bytes + (size_t)(1u << 30) > fr && cap_ > 0) {
-    // release the batch temporaries first; they are re-sized on demand
+  size_t margin = (size_t)2 << 30;
+  if (want > vmm_mapped_ + (fr > margin ? fr - margin : 0) && bcap_ > 0) {
+    // give the batch temporaries back first; they are re-sized on demand
     Bg_.release();
     Y_.release();
     IN_.release();
@@ -114,18 +179,42 @@ void ReductionEngine::grow_pool(int need) {
     bcap_ = 0;
     DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   }
-  DRZG_REQUIRE(bytes + (size_t)(1u << 30) < fr, "engine: state pool exceeds device memory (" +
-                                                    std::to_string(ncap) + " slots)");
-  int8_t* np = nullptr;
-  DRZG_CUDA(cudaMalloc(&np, bytes));
-  if (pool_) {
-    DRZG_CUDA(cudaMemcpyAsync(np, pool_, (size_t)cap_ * slot_stride_, cudaMemcpyDeviceToDevice, st_));
-    DRZG_CUDA(cudaStreamSynchronize(st_));
-    DRZG_CUDA(cudaFree(pool_));
+  size_t room = vmm_mapped_ + (fr > margin ? fr - margin : 0);
+  if (want > room) want = std::max<size_t>(room, (size_t)need * (size_t)slot_stride_);  // settle for what fits
+  DRZG_REQUIRE(want <= room && want <= vmm_reserved_,
+               "engine: state pool exceeds device memory (" + std::to_string(need) + " slots)");
+  size_t target = (want + gran - 1) / gran * gran;
+  target = std::min(target, vmm_reserved_);
+  while (vmm_mapped_ < target) {
+    size_t chunk = std::min<size_t>(target - vmm_mapped_, (size_t)4 << 30);
+    chunk = (chunk + gran - 1) / gran * gran;
+    CUmemGenericAllocationHandle h;
+    DRZG_CU(V.create(&h, chunk, &prop, 0));
+    CUdeviceptr at = reinterpret_cast<CUdeviceptr>(pool_) + vmm_mapped_;
+    DRZG_CU(V.map(at, chunk, 0, h, 0));
+    CUmemAccessDesc acc = {};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    DRZG_CU(V.access(at, chunk, &acc, 1));
+    vmm_chunks_.push_back({vmm_mapped_, chunk, (unsigned long long)h});
+    vmm_mapped_ += chunk;
   }
-  pool_ = np;
-  for (int s = ncap - 1; s >= cap_; --s) free_.push_back(s);
-  cap_ = ncap;
+  int ncap2 = (int)std::min<size_t>(vmm_mapped_ / (size_t)slot_stride_, (size_t)INT32_MAX);
+  for (int s = ncap2 - 1; s >= cap_; --s) free_.push_back(s);
+  cap_ = ncap2;
+}
+
+void ReductionEngine::release_pool() {
+  if (!pool_) return;
+  cudaStreamSynchronize(st_);
+  const Vmm& V = Vmm::get();
+  for (auto& c : vmm_chunks_) {
+    V.unmap(reinterpret_cast<CUdeviceptr>(pool_) + c.off, c.bytes);
+    V.release((CUmemGenericAllocationHandle)c.handle);
+  }
+  V.addr_free(reinterpret_cast<CUdeviceptr>(pool_), vmm_reserved_);
+  vmm_chunks_.clear();
+  pool_ = nullptr;
 }
 
 int ReductionEngine::alloc_slot() {
@@ -143,7 +232,9 @@ void ReductionEngine::ensure_batch(int B) {
   size_t fr = 0, tot = 0;
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   // temporaries get at most half of what is free, in multiples of 64 states
-  size_t lim = std::max<size_t>(64, (size_t)(fr * 0.8) / per / 64 * 64);
+  // temporaries: at most 80% of what is free and 12% of the device, so the
+  // state pool keeps room to grow
+  size_t lim = std::max<size_t>(64, std::min<size_t>((size_t)(fr * 0.8), (size_t)(tot * 0.12)) / per / 64 * 64);
   lim = std::min<size_t>(lim, (size_t)1 << 21);  // grid.y = states / 32 stays < 65536
   int nb = (int)std::min<size_t>(lim, (size_t)round_up(B, 64));
   if (nb <= bcap_) return;
@@ -323,8 +414,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     // batch temporaries), else take the 60% and grow only if needed
     size_t fr = 0, tot = 0;
     DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
-    size_t budget = (size_t)(fr * 0.60) / (size_t)slot_stride_;
-    grow_pool((int)std::max<size_t>(1024, std::min<size_t>(total_seeds, budget)));
+    size_t budget = (size_t)(fr * 0.40) / (size_t)slot_stride_;
+    grow_pool((int)std::max<size_t>(1024, std::min<size_t>(total_seeds / 3 + 1, budget)));
   }
 
   std::map<int, std::vector<HS>, std::greater<int>> landed;

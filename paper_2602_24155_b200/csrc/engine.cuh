@@ -132,6 +132,13 @@ class ReductionEngine {
   DevBuf<unsigned long long> btab_;
   // pool
   int8_t* pool_ = nullptr;
+  size_t vmm_reserved_ = 0, vmm_mapped_ = 0;
+  struct VmmChunk {
+    size_t off, bytes;
+    unsigned long long handle;
+  };
+  std::vector<VmmChunk> vmm_chunks_;
+  void release_pool();
   int cap_ = 0;
   i64 peak_live_ = 0;
   std::vector<int> free_;

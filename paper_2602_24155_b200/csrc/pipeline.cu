@@ -1,6 +1,8 @@
 // Frobenius assembly + zeta driver (see pipeline.cuh).
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <thread>
 
@@ -101,7 +103,12 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       std::vector<ColumnSeeds> grp(std::make_move_iterator(seeds.begin() + c0),
                                    std::make_move_iterator(seeds.begin() + c1));
       std::vector<std::vector<i64>> Gg;
+      const double tg = now_s();
+      const i64 mv0 = out.led.matvecs;
       eng.run_pchunk(grp, Gg, out.led);
+      if (std::getenv("DRZG_VERBOSE"))
+        std::fprintf(stderr, "[drzg] group %d: columns %zu-%zu, %lld matvecs, %.2f s, peak live %lld\n", out.groups,
+                     c0, c1 - 1, (long long)(out.led.matvecs - mv0), now_s() - tg, (long long)eng.peak_live());
       for (size_t i = c0; i < c1; ++i) G[i] = std::move(Gg[i - c0]);
       c0 = c1;
       ++out.groups;
