@@ -91,6 +91,10 @@ char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_
 int drzg_random_hypersurface(uint64_t p, int32_t n, int32_t d, uint64_t seed, int32_t policy, int32_t fermat,
                              uint64_t* coeffs_out, int32_t* tries_out);
 
+/* brute-force #X(F_{p^r}) — oracle.hpp:190-245 (the driver's count checks) */
+int drzg_count_points(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r, int64_t budget,
+                      int64_t* out);
+
 /* charpoly + recover_Q on a given F (zeta.hpp:456-470); F as b*b decimal strings */
 char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t nm_override, int32_t b,
                     const char* const* F);

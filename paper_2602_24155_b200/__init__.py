@@ -174,6 +174,14 @@ def random_hypersurface(p, n, d, seed=1, policy="p-chunk", fermat=False):
     return [int(x) for x in out]
 
 
+def count_points(p, n, d, coeffs, r, budget=200_000_000):
+    """brute-force #X(F_{p^r}) (reference oracle.hpp:190-245)"""
+    out = ctypes.c_int64()
+    _check(lib().drzg_count_points(ctypes.c_uint64(p), n, d, _u64arr(coeffs), r, ctypes.c_int64(budget),
+                                   ctypes.byref(out)))
+    return out.value
+
+
 def charpoly(p, n, d, F, b, r_uniform=0, nm=0):
     """berkowitz_charpoly + recover_Q on a given F (zeta.hpp:456-470)"""
     arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F])

@@ -325,6 +325,8 @@ char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_
     for (size_t i = 0; i < r.counts.size(); ++i)
       os << (i ? "," : "") << "[" << r.counts[i].r << ",\"" << r.counts[i].from_zeta.str() << "\","
          << (r.counts[i].ok ? "true" : "false") << "]";
+    os << "],\"escalations\":[";
+    for (size_t i = 0; i < r.reasons.size(); ++i) os << (i ? "," : "") << "\"" << r.reasons[i] << "\"";
     os << "],\"seconds\":" << r.wall << ",\"frobenius\":{" << frob_json_body(r.last) << "}}";
     return os.str();
   });
@@ -360,6 +362,15 @@ int drzg_random_hypersurface(uint64_t p, int32_t n, int32_t d, uint64_t seed, in
       if (tries_out) *tries_out = tries;
       return;
     }
+  });
+}
+
+// brute-force #X(F_{p^r}) (reference count_points, oracle.hpp:190-245)
+int drzg_count_points(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r, int64_t budget,
+                      int64_t* out) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    *out = count_points(X, r, budget);
   });
 }
 

@@ -207,6 +207,8 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
     res.last = std::move(fr);
     Recovered rec = recover_Q(dres, plan);
     auto escalate_or_throw = [&](const std::string& why) {
+      res.reasons.push_back(why);
+      if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] escalate: %s\n", why.c_str());
       if (!escalate_plan(plan)) throw escalation_exhausted("precision ladder exhausted: " + why);
     };
     if (rec.status == 2) {

@@ -66,6 +66,7 @@ struct ZetaOut {
   Ledger led;
   FrobResult last;
   double wall = 0;
+  std::vector<std::string> reasons;  // escalation ladder steps taken
 };
 
 ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device);
