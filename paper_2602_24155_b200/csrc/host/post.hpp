@@ -170,9 +170,16 @@ inline NewtonPolygon newton_polygon(const std::vector<Z>& a, u64 p) {
   return np;
 }
 
+// Hodge polygon at integer x: slope m-1 with multiplicity h_m (SPEC.md:327,
+// 878).  Deliberate deviation: the reference (zeta.hpp:275-284) stops at the
+// first empty slot (`take <= 0` also when h_m == 0), so for h_1 = 0 (cubic
+// threefolds and fourfolds) its polygon is identically 0, the Newton >= Hodge
+// check with equal endpoints always fails and run_zeta escalates until it
+// throws.  Empty slots are skipped here; nonempty ones behave identically.
 inline i64 hodge_polygon_at(const std::vector<i64>& h, int n, i64 x) {
   i64 acc = 0, used = 0;
   for (int m = 1; m <= n; ++m) {
+    if (h[m] == 0) continue;
     i64 take = std::min<i64>(h[m], x - used);
     if (take <= 0) break;
     acc += take * (m - 1);

@@ -22,7 +22,10 @@ for c in cases:
             co = drzg.random_hypersurface(7, 5, 3, 1); r = drzg.frobenius(7, 5, 3, co, columns=[col], profile=True)
         elif c == "fourfold_zeta":
             co = drzg.random_hypersurface(7, 5, 3, 1); r = drzg.zeta(7, 5, 3, co, profile=False)
-            r = {k: r[k] for k in ("Q", "ambiguous", "slopes", "newton_height", "p_rank", "counts", "seconds", "frobenius")}
+            r = {k: r[k] for k in ("Q", "ambiguous", "slopes", "newton_height", "p_rank", "counts", "escalations", "seconds", "frobenius")}
+        elif c == "threefold_zeta":
+            co = drzg.random_hypersurface(13, 4, 3, 1); r = drzg.zeta(13, 4, 3, co)
+            r.pop("frobenius", None)
         elif c == "qsurf_r1":
             co = drzg.random_hypersurface(7, 3, 5, 1); r = drzg.frobenius(7, 3, 5, co, r_uniform=1, nm=3, profile=True)
         r.pop("F", None); r.pop("charpoly", None)
