@@ -199,9 +199,10 @@ def main():
     coeffs = drzg.random_hypersurface(p, n, d, seed=seed, fermat=fermat)
     h = hodge_counts(n, d)
     b = sum(h)
-    # columns partitioned across ranks, heavier pole orders dealt first
-    cols = list(range(b))
-    mine = cols[rank::world] if world > 1 else None
+    # columns partitioned across ranks (longest-processing-time by pole order)
+    from paper_2602_24155_b200 import parallel
+    all_cols = [parallel.partition_columns(n, d, world, r) for r in range(world)]
+    mine = all_cols[rank] if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step(profile=False):
@@ -211,27 +212,9 @@ def main():
                           verify_counts=True)
             return z["frobenius"]["kernels"]["device_ms"] / 1e3, z, z["frobenius"]
         fr = drzg.frobenius(p, n, d, coeffs, r_uniform=r_uniform, columns=mine, device=local, profile=profile)
-        # gather F column blocks over NCCL: fixed-width 64-bit limbs, each
-        # entry owned by exactly one rank (NCCL integer Sum would wrap mod
-        # 2^64, so entries travel as limbs and are combined on the host)
-        W = 6
-        flat = []
-        for x in fr["F"]:
-            v = int(x)
-            flat.extend((v >> (62 * i)) & ((1 << 62) - 1) for i in range(W))
-        t = torch.tensor(flat, dtype=torch.int64, device="cuda")
-        outs = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(outs, t)
-        z = None
-        if rank == 0:
-            F = [0] * (b * b)
-            for o in outs:
-                vals = o.view(-1, W).tolist()
-                for i, limbs in enumerate(vals):
-                    v = sum(l << (62 * k) for k, l in enumerate(limbs))
-                    if v:
-                        F[i] = v
-            z = drzg.charpoly(p, n, d, [str(x) for x in F], b, r_uniform=r_uniform)
+        # one NCCL all_gather of the column blocks (62-bit limbs; see parallel.py)
+        F = parallel.gather_frobenius(fr["F"], b, mine, world, all_cols, device=torch.device("cuda", local))
+        z = drzg.charpoly(p, n, d, [str(x) for x in F], b, r_uniform=r_uniform) if rank == 0 else None
         return fr["kernels"]["device_ms"] / 1e3, z, fr
 
     for _ in range(args.warmup):

@@ -89,7 +89,8 @@ def test_reduce_chunk_matches_reference(case):
 
 FROB_CASES = ["fermat_cubic_curve_f7.json", "random_cubic_curve_f11_s3.json", "random_quartic_curve_f7_s2.json",
               "quintic_f7_s1.json", "fermat_quartic_surface_f7.json", "k3_f11_s1_r1.json",
-              "quintic_surface_f7_s1_r1.json", "threefold_f13_s1_r1.json", "fermat_fourfold_f7_r1.json"]
+              "quintic_surface_f7_s1_r1.json", "threefold_f13_s1_r1.json", "fermat_fourfold_f7_r1.json",
+              "k3_f11_s1.json", "threefold_f13_s1.json"]
 
 
 @pytest.mark.parametrize("name", FROB_CASES)
@@ -107,7 +108,8 @@ def test_frobenius_matrix_matches_reference(name):
     assert fr["combines"] == g["ledger"]["combines"]
 
 
-@pytest.mark.parametrize("name", ["fermat_cubic_curve_f7.json", "quintic_f7_s1.json", "random_quartic_curve_f7_s2.json"])
+@pytest.mark.parametrize("name", ["fermat_cubic_curve_f7.json", "quintic_f7_s1.json", "random_quartic_curve_f7_s2.json",
+                                  "k3_f11_s1.json", "threefold_f13_s1.json"])
 def test_zeta_matches_reference(name):
     g = golden(name)
     z = drzg.zeta(g["p"], g["n"], g["d"], g["coeffs"])
