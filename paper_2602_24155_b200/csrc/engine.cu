@@ -46,6 +46,15 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     }
     i64 cmax = (127 + R * (T.dp.q - 1) / 2) / (T.dp.q - 1) + 1;
     DRZG_REQUIRE(cmax < 32767, "engine: Dixon carries exceed int16");
+    // fp32-reciprocal epilogues are exact when every operand is < 2^23:
+    // digit GEMM |acc| <= nLp (q/2)^2, carry numerators <= 127 + cmax + R q/2,
+    // T epilogue <= nv (max weight) (q/2) + carry
+    const i64 half = T.dp.q / 2;
+    i64 wmax = 0;
+    for (int r = 0; r < T.nL; ++r) wmax = std::max<i64>(wmax, T.sol_mu[r]);
+    i64 bound = std::max<i64>((i64)nLp_ * half * half, 127 + cmax + R * half);
+    bound = std::max<i64>(bound, (i64)T.nv * (4096 + wmax) * half + 4096);
+    fast_ = (T.dp.q & 1) && bound < ((i64)1 << 23);
     if (want_tc && maxv < 256) {
       std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);
       for (int r = 0; r < T.nL; ++r)
@@ -275,6 +284,7 @@ dev::StepArgs ReductionEngine::make_args(int b0, int nb, int y) {
   a.Ld = T.dp.Ld;
   a.q = T.dp.q;
   a.fq = FastQ::make(T.dp.q);
+  a.fast = fast_ ? 1 : 0;
   a.pool = pool_;
   a.slot_stride = slot_stride_;
   a.slot = d_slot_.p + b0;
@@ -306,6 +316,7 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
       e.N = nb;
       e.q = T.dp.q;
       e.fq = FastQ::make(T.dp.q);
+      e.fast = fast_ ? 1 : 0;
       e.Ld = T.dp.Ld;
       e.k = k;
       e.nLp = nLp_;
@@ -396,6 +407,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   int colbits = 1;
   while ((1 << colbits) < ncol) ++colbits;
   DRZG_REQUIRE(nv * bits + colbits <= 64, "engine: state key does not fit 64 bits");
+  // the fp32 epilogue bound assumed exponents below 4096
+  if ((i64)T.d * maxpole >= 4096) fast_ = false;
   auto key = [&](int c, const Expo& u) { return ((u64)c << (nv * bits)) | u.pack(bits); };
 
   cudaEvent_t run0, run1;

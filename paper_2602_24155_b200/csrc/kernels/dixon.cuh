@@ -180,9 +180,13 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
     const int rn = cont ? a.ginv[(size_t)vd * a.side + g] : -1;
     int carry = 0;
     for (int t = 0; t < a.Ld; ++t) {
-      int rr;
-      int qt = a.fq.divfloor(acc[t] + carry, rr);
-      if (rr > (a.q >> 1)) rr -= a.q, ++qt;
+      int rr, qt;
+      if (a.fast) {
+        rr = a.fq.balq(acc[t] + carry, qt);
+      } else {
+        qt = a.fq.divfloor(acc[t] + carry, rr);
+        if (rr > (a.q >> 1)) rr -= a.q, ++qt;
+      }
       carry = qt;
       if (!cont)
         a.W[(size_t)t * wplane + (size_t)g * a.P + s] = (int8_t)rr;

@@ -28,6 +28,7 @@ struct StepArgs {
   const int* sol_mu;      // ... and mu_i
   int nv, nL, nLp, side, sidep, Ld, q;
   FastQ fq;
+  int fast;               // fp32 reciprocal path valid (all operands < 2^23)
   // state pool
   int8_t* pool;           // slots x (Ld * sidep)
   long long slot_stride;  // Ld * sidep

@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int q4 = 0; q4 < 4; ++q4) {
             uint32_t word = 0;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) word |= (uint32_t)(uint8_t)(int8_t)epi.fq.bal(v[q4 * 4 + b]) << (8 * b);
+            for (int b = 0; b < 4; ++b)
+              word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_fast(v[q4 * 4 + b]) : epi.fq.bal(v[q4 * 4 + b]))
+                      << (8 * b);
             w4[q4] = word;
           }
           *reinterpret_cast<uint4*>(epi.Y + ((size_t)epi.k * epi.nLp + m) * epi.P + nb) =
@@ -249,10 +251,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           uint32_t in4[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            int rem;
-            int cnew = epi.fq.divfloor((int)b0[j] + (int)cc[j] - v[j], rem);  // exact
+            int cnew, inb;
+            if (epi.fast) {
+              cnew = epi.fq.div_exact_fast((int)b0[j] + (int)cc[j] - v[j]);
+              inb = epi.fq.bal_fast((int)b1[j] + cnew);
+            } else {
+              int rem;
+              cnew = epi.fq.divfloor((int)b0[j] + (int)cc[j] - v[j], rem);  // exact
+              inb = epi.fq.bal((int)b1[j] + cnew);
+            }
             cc[j] = (int16_t)cnew;
-            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)epi.fq.bal((int)b1[j] + cnew) << (8 * (j & 3));
+            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * (j & 3));
           }
           cyp[0] = c4[0];
           cyp[1] = c4[1];

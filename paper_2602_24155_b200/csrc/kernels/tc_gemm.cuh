@@ -30,6 +30,7 @@ struct TcEpiArgs {
   int M = 0, N = 0;        // valid output extent
   int q = 0, Ld = 0, k = 0;
   FastQ fq;
+  int fast = 0;            // every epilogue operand is below 2^23 in magnitude (host-checked)
   int nLp = 0, nL = 0;
   // raw
   int32_t* out = nullptr;  // N x M (row n holds the M outputs of column n)
