@@ -46,7 +46,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     }
     i64 cmax = (127 + R * (T.dp.q - 1) / 2) / (T.dp.q - 1) + 1;
     DRZG_REQUIRE(cmax < 32767, "engine: Dixon carries exceed int16");
-    // fp32-reciprocal epilogues are exact when every operand is < 2^23:
+    // multiply-high epilogues are exact when every operand is < 2^22:
     // digit GEMM |acc| <= nLp (q/2)^2, carry numerators <= 127 + cmax + R q/2,
     // T epilogue <= nv (max weight) (q/2) + carry
     const i64 half = T.dp.q / 2;
@@ -54,7 +54,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     for (int r = 0; r < T.nL; ++r) wmax = std::max<i64>(wmax, T.sol_mu[r]);
     i64 bound = std::max<i64>((i64)nLp_ * half * half, 127 + cmax + R * half);
     bound = std::max<i64>(bound, (i64)T.nv * (4096 + wmax) * half + 4096);
-    fast_ = (T.dp.q & 1) && bound < ((i64)1 << 23);
+    fast_ = bound < ((i64)1 << 22);
     if (want_tc && maxv < 256) {
       std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);
       for (int r = 0; r < T.nL; ++r)

@@ -9,21 +9,23 @@ namespace drzg {
 // |x| < 2^30: u = x + q*2^30 >= 0, floor(u / q) = mulhi64(u, ceil(2^64/q))
 // (exact because u < 2^39 and q < 2^8)
 //
-// Fast path (|x| < 2^23, q odd): t = rint(x * (1/q)) in fp32 is the nearest
-// integer to x/q exactly — the relative error of the product is < 2^-24, so
-// the absolute error is < 2^-1/q, below the 1/(2q) gap between x/q and any
-// half-integer — and x - q*t is the balanced residue.
+// Fast path (|x| < 2^22): x' = x + q*K with K = ceil(2^22/q) is in [0, 2^23),
+// and for x' < 2^32/q (true for q < 512) floor(x'/q) = umulhi(x', ceil(2^32/q)):
+// the magic's excess is < 1, so the product overshoots x'/q by < x'/2^32 <
+// 1/q, which never crosses an integer.  All full-rate integer instructions.
 struct FastQ {
   int q = 0;
   unsigned long long magic = 0;
   long long off = 0;  // q * 2^30
-  float inv = 0.f;    // 1/q rounded
+  unsigned m32 = 0;   // ceil(2^32 / q)
+  int k22 = 0;        // ceil(2^22 / q)
   static FastQ make(int q) {
     FastQ f;
     f.q = q;
     f.magic = ~0ull / (unsigned long long)q + 1;
     f.off = (long long)q << 30;
-    f.inv = 1.0f / (float)q;
+    f.m32 = (unsigned)(((1ull << 32) + (unsigned long long)q - 1) / (unsigned long long)q);
+    f.k22 = (int)(((1 << 22) + q - 1) / q);
     return f;
   }
 #ifdef __CUDACC__
@@ -39,19 +41,25 @@ struct FastQ {
     divfloor(x, r);
     return r > (q >> 1) ? r - q : r;
   }
-  // nearest quotient t and balanced residue x - q t, for |x| < 2^23
+  // balanced residue x - q t and its quotient t, for |x| < 2^22
   __device__ __forceinline__ int balq(int x, int& t) const {
-    float fx = (float)x;
-    float ft = rintf(fx * inv);
-    t = (int)ft;
-    return x - q * t;
+    unsigned xp = (unsigned)(x + q * k22);
+    int tt = (int)__umulhi(xp, m32);
+    int r = (int)xp - tt * q;
+    tt -= k22;
+    if (r > (q >> 1)) r -= q, ++tt;
+    t = tt;
+    return r;
   }
   __device__ __forceinline__ int bal_fast(int x) const {
     int t;
     return balq(x, t);
   }
-  // x / q for x divisible by q, |x| < 2^23
-  __device__ __forceinline__ int div_exact_fast(int x) const { return (int)rintf((float)x * inv); }
+  // x / q for x divisible by q, |x| < 2^22
+  __device__ __forceinline__ int div_exact_fast(int x) const {
+    unsigned xp = (unsigned)(x + q * k22);
+    return (int)__umulhi(xp, m32) - k22;
+  }
 #endif
 };
 
