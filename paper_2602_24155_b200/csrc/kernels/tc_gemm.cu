@@ -216,7 +216,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (!mok || nb >= epi.N) continue;
         const int cnt = min(16, epi.N - nb);
         if (epi.mode == (int)TcEpilogue::raw) {
-          for (int j = 0; j < cnt; ++j) epi.out[(size_t)(nb + j) * epi.M + m] = v[j];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < cnt) epi.out[(size_t)(nb + j) * epi.M + m] = v[j];
         } else if (epi.b_mn && epi.mode == (int)TcEpilogue::digit) {
           // Y[k][m][n0..n0+15]: one 16-byte store
           uint32_t w4[4];
@@ -240,31 +242,36 @@ __global__ void __launch_bounds__(THREADS, 1)
                            : __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P + nb));
           uint4* cyp = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
           // c_0 = 0: digit 0 ignores whatever the previous step left in Cy
-          uint4 c4[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
+          uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
           if (epi.k) {
-            c4[0] = cyp[0];
-            c4[1] = cyp[1];
+            c0 = cyp[0];
+            c1 = cyp[1];
           }
-          const int8_t* b0 = reinterpret_cast<const int8_t*>(&bk);
-          const int8_t* b1 = reinterpret_cast<const int8_t*>(&bk1);
-          int16_t* cc = reinterpret_cast<int16_t*>(c4);
+          // unpack with shifts only (pointer views would spill to local memory)
+          const uint32_t bw[4] = {bk.x, bk.y, bk.z, bk.w};
+          const uint32_t b1w[4] = {bk1.x, bk1.y, bk1.z, bk1.w};
+          const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          uint32_t cn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
           uint32_t in4[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
+            const int b0j = (int)(int8_t)(bw[j >> 2] >> (8 * (j & 3)));
+            const int b1j = (int)(int8_t)(b1w[j >> 2] >> (8 * (j & 3)));
+            const int ccj = (int)(int16_t)(cw[j >> 1] >> (16 * (j & 1)));
             int cnew, inb;
             if (epi.fast) {
-              cnew = epi.fq.div_exact_fast((int)b0[j] + (int)cc[j] - v[j]);
-              inb = epi.fq.bal_fast((int)b1[j] + cnew);
+              cnew = epi.fq.div_exact_fast(b0j + ccj - v[j]);
+              inb = epi.fq.bal_fast(b1j + cnew);
             } else {
               int rem;
-              cnew = epi.fq.divfloor((int)b0[j] + (int)cc[j] - v[j], rem);  // exact
-              inb = epi.fq.bal((int)b1[j] + cnew);
+              cnew = epi.fq.divfloor(b0j + ccj - v[j], rem);  // exact
+              inb = epi.fq.bal(b1j + cnew);
             }
-            cc[j] = (int16_t)cnew;
+            cn[j >> 1] |= ((uint32_t)cnew & 0xFFFFu) << (16 * (j & 1));
             in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * (j & 3));
           }
-          cyp[0] = c4[0];
-          cyp[1] = c4[1];
+          cyp[0] = make_uint4(cn[0], cn[1], cn[2], cn[3]);
+          cyp[1] = make_uint4(cn[4], cn[5], cn[6], cn[7]);
           if (!last)
             *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
         }
