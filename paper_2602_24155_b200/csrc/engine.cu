@@ -570,10 +570,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
             p2.push_back((int)g2.size());
           }
           if (s2.empty()) continue;
-          d_a.upload(s2, st_);
-          d_b.upload(p2, st_);
-          d_c.upload(g2, st_);
-          d_dig.upload(d2, st_);
+          d_a.stage(s2, stager_, st_);
+          d_b.stage(p2, stager_, st_);
+          d_c.stage(g2, stager_, st_);
+          d_dig.stage(d2, stager_, st_);
           if (pass == 0)
             timed(&clock.other_ms, [&] {
               dev::seed_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p,
@@ -622,8 +622,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
           gptr.push_back((int)mem.size());
           led.combines += (i64)g.size() - 1;
         }
-        d_a.upload(gptr, st_);
-        d_b.upload(mem, st_);
+        d_a.stage(gptr, stager_, st_);
+        d_b.stage(mem, stager_, st_);
         dim3 gm((unsigned)((T.side + 127) / 128) * extra.size());
         timed(&clock.other_ms, [&] {
           dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_a.p, d_b.p);
@@ -657,10 +657,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       ks.push_back(kk[i]);
       for (int j = 0; j < nv; ++j) hu0.push_back(front[i].u[j]);
     }
-    d_slot_.upload(hslot, st_);
-    d_vdir_.upload(hvdir, st_);
-    d_u0_.upload(hu0, st_);
-    d_k_.upload(ks, st_);
+    d_slot_.stage(hslot, stager_, st_);
+    d_vdir_.stage(hvdir, stager_, st_);
+    d_u0_.stage(hu0, stager_, st_);
+    d_k_.stage(ks, stager_, st_);
     led.matvecs += run_sweep(ks);
     led.startups += (i64)front.size();
     // land every state at pole P - k
@@ -698,8 +698,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         mem.insert(mem.end(), kv.second.begin(), kv.second.end());
         gptr.push_back((int)mem.size());
       }
-      d_b.upload(gptr, st_);
-      d_c.upload(mem, st_);
+      d_b.stage(gptr, stager_, st_);
+      d_c.stage(mem, stager_, st_);
       dim3 gm((unsigned)((T.side + 127) / 128) * merges.size());
       timed(&clock.other_ms, [&] {
         dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_b.p, d_c.p);
@@ -708,9 +708,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         for (int s : kv.second) free_slot(s);
     }
     if (!fs.empty()) {
-      d_a.upload(fs, st_);
-      d_b.upload(fc, st_);
-      d_c.upload(fu, st_);
+      d_a.stage(fs, stager_, st_);
+      d_b.stage(fc, stager_, st_);
+      d_c.stage(fu, stager_, st_);
       dim3 gf((unsigned)((T.side + 127) / 128) * fs.size());
       timed(&clock.other_ms, [&] {
         dev::floor_kernel<<<gf, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, nv, d_a.p, d_b.p, d_c.p,
@@ -768,10 +768,10 @@ void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<
     hvdir.push_back(vdir[i]);
     for (int j = 0; j < nv; ++j) hu0.push_back(u[i][j]);
   }
-  d_slot_.upload(hslot, st_);
-  d_vdir_.upload(hvdir, st_);
-  d_u0_.upload(hu0, st_);
-  d_k_.upload(ks, st_);
+  d_slot_.stage(hslot, stager_, st_);
+  d_vdir_.stage(hvdir, stager_, st_);
+  d_u0_.stage(hu0, stager_, st_);
+  d_k_.stage(ks, stager_, st_);
   led.matvecs += run_sweep(ks);
   led.startups += B;
   for (int i = 0; i < B; ++i) {

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstring>
 #include <functional>
 #include <unordered_map>
 #include <unordered_set>
@@ -49,6 +50,47 @@ struct KernelClock {
   double gemm_macs = 0;  // algorithmic int8 MACs issued (nL x nL per state-digit)
 };
 
+// pinned staging ring: host-side inputs of a sweep are copied through
+// page-locked buffers, so cudaMemcpyAsync really is asynchronous and the host
+// policy runs ahead of the device (bounded by the ring: a buffer is reused
+// only after the copy that read it has completed)
+class Stager {
+ public:
+  ~Stager() {
+    for (auto& b : bufs_) {
+      if (b.h) cudaFreeHost(b.h);
+      if (b.ev) cudaEventDestroy(b.ev);
+    }
+  }
+  void copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    Buf& b = bufs_[next_];
+    next_ = (next_ + 1) % kRing;
+    if (!b.ev) DRZG_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+    if (b.used) DRZG_CUDA(cudaEventSynchronize(b.ev));
+    if (b.cap < bytes) {
+      if (b.h) DRZG_CUDA(cudaFreeHost(b.h));
+      b.cap = std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
+      DRZG_CUDA(cudaMallocHost(&b.h, b.cap));
+    }
+    std::memcpy(b.h, src, bytes);
+    DRZG_CUDA(cudaMemcpyAsync(dst, b.h, bytes, cudaMemcpyHostToDevice, st));
+    DRZG_CUDA(cudaEventRecord(b.ev, st));
+    b.used = true;
+  }
+
+ private:
+  static constexpr int kRing = 64;
+  struct Buf {
+    void* h = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+  };
+  Buf bufs_[kRing];
+  int next_ = 0;
+};
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -57,7 +99,7 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFree(p);  // also valid for stream-ordered allocations
   }
   void alloc(size_t count) {
     if (count <= n) return;
@@ -76,6 +118,20 @@ struct DevBuf {
     if (!v.empty()) DRZG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     g_traffic.h2d += (long long)(v.size() * sizeof(T));
   }
+  // stream-ordered growth and a pinned-staged copy: never blocks the host on
+  // earlier device work
+  void stage(const std::vector<T>& v, Stager& sg, cudaStream_t st) {
+    if (v.size() > n) {
+      if (p) DRZG_CUDA(cudaFreeAsync(p, st));
+      size_t cnt = std::max<size_t>(v.size() + v.size() / 2, 1024);
+      DRZG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), st));
+      n = cnt;
+      async_ = true;
+    }
+    sg.copy(p, v.data(), v.size() * sizeof(T), st);
+    g_traffic.h2d += (long long)(v.size() * sizeof(T));
+  }
+  bool async_ = false;
 };
 
 class ReductionEngine {
@@ -152,6 +208,7 @@ class ReductionEngine {
   DevBuf<int16_t> Cy_;
   DevBuf<int8_t> W_;
   cudaEvent_t ev0_, ev1_;
+  Stager stager_;
   std::vector<Expo> dirs_host_;
 };
 
