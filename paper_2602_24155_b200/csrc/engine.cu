@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <string>
@@ -460,6 +462,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       if (li != landed_idx.end()) front_idx.swap(li->second);
       landed_idx.erase(P);
     }
+    auto hp0 = std::chrono::steady_clock::now();
     // materialise the seeds whose pole is P.  Seeds sharing (column, u) are
     // combined here on the host (the reference's combine_states of those
     // seeds, counted in the ledger) so each distinct state takes one slot;
@@ -587,6 +590,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         }
       }
     }
+    auto hp1 = std::chrono::steady_clock::now();
     // combine_states: merge equal (col, u) except in a column's first sweep
     {
       std::unordered_map<u64, int> first;
@@ -633,6 +637,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       }
       front.swap(keep);
     }
+    auto hp2 = std::chrono::steady_clock::now();
     // moves (reduction.hpp:486-496), longest chunks first
     std::vector<int> vd(front.size());
     std::vector<i64> kk(front.size());
@@ -661,7 +666,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     d_vdir_.stage(hvdir, stager_, st_);
     d_u0_.stage(hu0, stager_, st_);
     d_k_.stage(ks, stager_, st_);
+    auto hp3 = std::chrono::steady_clock::now();
     led.matvecs += run_sweep(ks);
+    auto hp4 = std::chrono::steady_clock::now();
     led.startups += (i64)front.size();
     // land every state at pole P - k
     std::vector<int> fs, fc, fu;
@@ -707,6 +714,15 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       for (auto& kv : merges)
         for (int s : kv.second) free_slot(s);
     }
+    auto hp5 = std::chrono::steady_clock::now();
+    {
+      auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+      host_t_[0] += sec(hp0, hp1);
+      host_t_[1] += sec(hp1, hp2);
+      host_t_[2] += sec(hp2, hp3);
+      host_t_[3] += sec(hp3, hp4);
+      host_t_[4] += sec(hp4, hp5);
+    }
     if (!fs.empty()) {
       d_a.stage(fs, stager_, st_);
       d_b.stage(fc, stager_, st_);
@@ -720,6 +736,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
   }
   for (int c = 0; c < ncol; ++c) led.combines += floor_arrivals[c] - (i64)floor_keys[c].size();
+  if (std::getenv("DRZG_VERBOSE"))
+    std::fprintf(stderr, "[drzg] host s: seeds %.3f combine %.3f moves %.3f launch %.3f land %.3f\n", host_t_[0],
+                 host_t_[1], host_t_[2], host_t_[3], host_t_[4]);
   std::vector<long long> hG(dG.n);
   DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
   g_traffic.d2h += (long long)(dG.n * sizeof(long long));

@@ -209,6 +209,7 @@ class ReductionEngine {
   DevBuf<int8_t> W_;
   cudaEvent_t ev0_, ev1_;
   Stager stager_;
+  double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
   std::vector<Expo> dirs_host_;
 };
 
