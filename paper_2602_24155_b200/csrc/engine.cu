@@ -11,6 +11,10 @@
 #include <string>
 
 #include "engine.cuh"
+#include "host/flatmap.hpp"
+
+#include <exception>
+#include <thread>
 #include "kernels/dixon.cuh"
 #include "kernels/tc_gemm.cuh"
 
@@ -437,14 +441,18 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   // per pole: key -> position in landed[pole]; a state landing on a key that
   // is already there is combined at once (the reference combines after every
   // sweep, reduction.hpp:502, so the ledger is unchanged)
-  std::map<int, std::unordered_map<u64, int>> landed_idx;
-  std::vector<std::unordered_set<u64>> floor_keys(ncol);
+  std::map<int, FlatMap> landed_idx;
+  std::vector<FlatMap> floor_keys(ncol);
   std::vector<i64> floor_arrivals(ncol, 0);
   std::vector<std::map<int, SeedBucket>::reverse_iterator> sit(ncol);
   for (int c = 0; c < ncol; ++c) sit[c] = cols[c].by_pole.rbegin();
 
-  DevBuf<int> d_a, d_b, d_c;
-  DevBuf<int8_t> d_dig;
+  // separate device buffers per use within a sweep: with the host running
+  // ahead, a restaged buffer must not be one an earlier kernel of the same
+  // sweep still reads (the stream orders copies and kernels, so reuse across
+  // uses is safe; distinct buffers just avoid needless reallocations)
+  DevBuf<int> d_a, d_b, d_c, d_s2, d_p2, d_g2, d_mp, d_mm;
+  DevBuf<int8_t> d_dig, d_dig2;
   for (;;) {
     int P = -1;
     if (!landed.empty()) P = landed.begin()->first;
@@ -456,109 +464,91 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       front = std::move(landed.begin()->second);
       landed.erase(landed.begin());
     }
-    std::unordered_map<u64, int> front_idx;  // key -> position in front (landed at P)
+    FlatMap front_idx(16);  // key -> position in front (states landed at P)
     {
       auto li = landed_idx.find(P);
       if (li != landed_idx.end()) front_idx.swap(li->second);
       landed_idx.erase(P);
     }
     auto hp0 = std::chrono::steady_clock::now();
-    // materialise the seeds whose pole is P.  Seeds sharing (column, u) are
-    // combined here on the host (the reference's combine_states of those
-    // seeds, counted in the ledger) so each distinct state takes one slot;
-    // a column's first sweep keeps its seeds apart, as the reference does
+    // materialise the seeds whose pole is P.  Seeds sharing (column, u) form
+    // one state (the reference's combine_states of those seeds, counted in
+    // the ledger); a state already landed at P absorbs them in place; a
+    // column's first sweep keeps its seeds apart, as the reference does.
+    // Landed states are unique per key (combined as they land), so after
+    // this no two live states at P share a key.
     {
-      std::vector<int> ss, eptr{0}, eg;
-      std::vector<int> add_slots;  // per new group: -1 = fresh slot, else absorbed in place
-      std::vector<int> accd;  // Ld per entry (int sums, normalised below)
+      std::vector<int> ss, eptr{0}, eg, add_slots;
+      std::vector<int8_t> ed;
+      std::vector<int> acc(Ld);
+      const int q = T.dp.q;
       for (int c = 0; c < ncol; ++c) {
         if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
         SeedBucket& bk = sit[c]->second;
         const bool first_sweep = top0[c] == P;
-        std::unordered_map<u64, int> grp;  // key -> index into ss
-        std::vector<std::unordered_map<int, int>> ent;  // per new state: g -> entry
-        const size_t base_state = ss.size();
-        for (size_t i = 0; i < bk.size(); ++i) {
+        const size_t ns = bk.size();
+        std::vector<u64> kv(ns);
+        for (size_t i = 0; i < ns; ++i) {
           Expo u(nv);
           for (int j = 0; j < nv; ++j) u[j] = bk.u[i * nv + j];
-          int st;
-          const u64 ku = key(c, u);
-          auto it = first_sweep ? grp.end() : grp.find(ku);
-          if (it == grp.end()) {
-            // a state already landed at this pole absorbs the seed in place
-            auto fit = first_sweep ? front_idx.end() : front_idx.find(ku);
-            int slot;
-            if (fit != front_idx.end()) {
-              slot = front[fit->second].slot;
-              led.combines += 1;
-              add_slots.push_back(slot);
-            } else {
-              HS h;
-              h.col = c;
-              h.u = u;
-              h.pole = P;
-              h.slot = slot = alloc_slot();
-              front.push_back(h);
-              add_slots.push_back(-1);
-            }
-            st = (int)(ss.size() - base_state);
-            ss.push_back(slot);
-            ent.emplace_back();
-            if (!first_sweep) grp.emplace(ku, st);
-          } else {
-            st = it->second;
+          kv[i] = key(c, u);
+        }
+        std::vector<int> ord(ns);
+        for (size_t i = 0; i < ns; ++i) ord[i] = (int)i;
+        if (!first_sweep)
+          std::sort(ord.begin(), ord.end(), [&](int a, int b) {
+            return kv[a] != kv[b] ? kv[a] < kv[b] : bk.g[a] < bk.g[b];
+          });
+        size_t i = 0;
+        while (i < ns) {
+          size_t j = i + 1;
+          if (!first_sweep)
+            while (j < ns && kv[ord[j]] == kv[ord[i]]) ++j;
+          const int s0i = ord[i];
+          const int fpos = first_sweep ? -1 : front_idx.find(kv[s0i]);
+          int slot;
+          if (fpos >= 0) {
+            slot = front[fpos].slot;
             led.combines += 1;
-          }
-          auto& em = ent[st];
-          auto eit = em.find(bk.g[i]);
-          int e;
-          if (eit == em.end()) {
-            e = (int)(eg.size());
-            em.emplace(bk.g[i], e);
-            eg.push_back(bk.g[i]);
-            accd.resize(accd.size() + Ld, 0);
+            add_slots.push_back(slot);
           } else {
-            e = eit->second;
+            HS h;
+            h.col = c;
+            h.u = Expo(nv);
+            for (int t = 0; t < nv; ++t) h.u[t] = bk.u[(size_t)s0i * nv + t];
+            h.pole = P;
+            h.slot = slot = alloc_slot();
+            front.push_back(h);
+            add_slots.push_back(-1);
           }
-          for (int t = 0; t < Ld; ++t) accd[(size_t)e * Ld + t] += bk.dig[i * Ld + t];
+          led.combines += (i64)(j - i - 1);
+          ss.push_back(slot);
+          for (size_t a = i; a < j;) {
+            size_t b2 = a + 1;
+            while (b2 < j && bk.g[ord[b2]] == bk.g[ord[a]]) ++b2;
+            std::fill(acc.begin(), acc.end(), 0);
+            for (size_t x = a; x < b2; ++x)
+              for (int t = 0; t < Ld; ++t) acc[t] += bk.dig[(size_t)ord[x] * Ld + t];
+            int carry = 0;
+            for (int t = 0; t < Ld; ++t) {
+              int v = acc[t] + carry;
+              int r = ((v % q) + q) % q;
+              if (r > q / 2) r -= q;
+              carry = (v - r) / q;
+              ed.push_back((int8_t)r);
+            }
+            eg.push_back(bk.g[ord[a]]);
+            a = b2;
+          }
+          eptr.push_back((int)eg.size());
+          i = j;
         }
-        // entries grouped by state in ss order
-        std::vector<int> order_e;
-        for (auto& em : ent) {
-          std::vector<int> es;
-          for (auto& kv : em) es.push_back(kv.second);
-          std::sort(es.begin(), es.end());
-          order_e.insert(order_e.end(), es.begin(), es.end());
-          eptr.push_back(eptr.back() + (int)es.size());
-        }
-        // permute this column's entries into state order
-        const size_t e0 = eg.size() - order_e.size();
-        std::vector<int> eg2(order_e.size()), ac2(order_e.size() * Ld);
-        for (size_t k = 0; k < order_e.size(); ++k) {
-          eg2[k] = eg[order_e[k]];
-          for (int t = 0; t < Ld; ++t) ac2[k * Ld + t] = accd[(size_t)order_e[k] * Ld + t];
-        }
-        std::copy(eg2.begin(), eg2.end(), eg.begin() + e0);
-        std::copy(ac2.begin(), ac2.end(), accd.begin() + e0 * Ld);
         SeedBucket().u.swap(bk.u);  // release host memory
         SeedBucket().g.swap(bk.g);
         SeedBucket().dig.swap(bk.dig);
         ++sit[c];
       }
       if (!ss.empty()) {
-        // normalise summed digits (balanced base q, top carry dropped)
-        std::vector<int8_t> ed(accd.size());
-        const int q = T.dp.q;
-        for (size_t e = 0; e < eg.size(); ++e) {
-          int carry = 0;
-          for (int t = 0; t < Ld; ++t) {
-            int v = accd[e * Ld + t] + carry;
-            int r = ((v % q) + q) % q;
-            if (r > q / 2) r -= q;
-            carry = (v - r) / q;
-            ed[e * Ld + t] = (int8_t)r;
-          }
-        }
         // fresh slots are zeroed and written; absorbed groups add in place
         for (int pass = 0; pass < 2; ++pass) {
           std::vector<int> s2, p2{0}, g2;
@@ -573,10 +563,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
             p2.push_back((int)g2.size());
           }
           if (s2.empty()) continue;
-          d_a.stage(s2, stager_, st_);
-          d_b.stage(p2, stager_, st_);
-          d_c.stage(g2, stager_, st_);
-          d_dig.stage(d2, stager_, st_);
+          (pass == 0 ? d_a : d_s2).stage(s2, stager_, st_);
+          (pass == 0 ? d_b : d_p2).stage(p2, stager_, st_);
+          (pass == 0 ? d_c : d_g2).stage(g2, stager_, st_);
+          (pass == 0 ? d_dig : d_dig2).stage(d2, stager_, st_);
           if (pass == 0)
             timed(&clock.other_ms, [&] {
               dev::seed_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p,
@@ -585,82 +575,62 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
           else
             timed(&clock.other_ms, [&] {
               dev::add_entries_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, T.dp.q,
-                                                                      d_a.p, d_b.p, d_c.p, d_dig.p, (int)s2.size());
+                                                                      d_s2.p, d_p2.p, d_g2.p, d_dig2.p,
+                                                                      (int)s2.size());
             });
         }
       }
     }
     auto hp1 = std::chrono::steady_clock::now();
-    // combine_states: merge equal (col, u) except in a column's first sweep
+    auto hp2 = hp1;
+    // moves (reduction.hpp:486-496) for every state, on host threads
+    const size_t nf = front.size();
+    std::vector<int> vd(nf);
+    std::vector<i64> kk(nf);
     {
-      std::unordered_map<u64, int> first;
-      first.reserve(front.size() * 2);
-      std::vector<HS> keep;
-      keep.reserve(front.size());
-      std::vector<std::vector<int>> extra;  // per kept index: merged slots
-      std::vector<int> gidx_of;
-      for (auto& h : front) {
-        if (top0[h.col] == P) {
-          keep.push_back(h);
-          continue;
-        }
-        u64 k = key(h.col, h.u);
-        auto it = first.find(k);
-        if (it == first.end()) {
-          first.emplace(k, (int)keep.size());
-          keep.push_back(h);
-        } else {
-          int dst = it->second;
-          if ((int)gidx_of.size() <= dst) gidx_of.resize(keep.size(), -1);
-          if (gidx_of[dst] < 0) {
-            gidx_of[dst] = (int)extra.size();
-            extra.push_back({keep[dst].slot});
+      const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_, nf / 4096 + 1));
+      std::vector<std::thread> pool;
+      std::vector<std::exception_ptr> errs(nth);
+      for (int t = 0; t < nth; ++t)
+        pool.emplace_back([&, t] {
+          try {
+            for (size_t i = t * nf / nth; i < (t + 1) * nf / nth; ++i) {
+              Expo v;
+              i64 k;
+              pchunk_move(T.d, n_, (i64)p_, front[i].u, front[i].pole, T.S, &v, &k);
+              DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
+              DRZG_REQUIRE(legal(T.d, front[i].u, v, k, T.S), "reduce_chunk: illegal move");
+              vd[i] = (int)rank_of(v);
+              kk[i] = k;
+            }
+          } catch (...) {
+            errs[t] = std::current_exception();
           }
-          extra[gidx_of[dst]].push_back(h.slot);
-        }
-      }
-      if (!extra.empty()) {
-        std::vector<int> gptr{0}, mem;
-        for (auto& g : extra) {
-          mem.insert(mem.end(), g.begin(), g.end());
-          gptr.push_back((int)mem.size());
-          led.combines += (i64)g.size() - 1;
-        }
-        d_a.stage(gptr, stager_, st_);
-        d_b.stage(mem, stager_, st_);
-        dim3 gm((unsigned)((T.side + 127) / 128) * extra.size());
-        timed(&clock.other_ms, [&] {
-          dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_a.p, d_b.p);
         });
-        for (auto& g : extra)
-          for (size_t i = 1; i < g.size(); ++i) free_slot(g[i]);
-      }
-      front.swap(keep);
+      for (auto& th : pool) th.join();
+      for (auto& e2 : errs)
+        if (e2) std::rethrow_exception(e2);
     }
-    auto hp2 = std::chrono::steady_clock::now();
-    // moves (reduction.hpp:486-496), longest chunks first
-    std::vector<int> vd(front.size());
-    std::vector<i64> kk(front.size());
-    for (size_t i = 0; i < front.size(); ++i) {
-      Expo v;
-      i64 k;
-      pchunk_move(T.d, n_, (i64)p_, front[i].u, front[i].pole, T.S, &v, &k);
-      DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
-      DRZG_REQUIRE(legal(T.d, front[i].u, v, k, T.S), "reduce_chunk: illegal move");
-      vd[i] = (int)rank_of(v);
-      kk[i] = k;
+    // longest chunks first, then by direction: counting sort on (k, v)
+    std::vector<int> order(nf);
+    {
+      const int ndir = T.ndir;
+      i64 kmx = 1;
+      for (i64 k : kk) kmx = std::max(kmx, k);
+      std::vector<int> cnt((size_t)(kmx + 1) * ndir + 1, 0);
+      auto bucket = [&](size_t i) { return (size_t)(kmx - kk[i]) * ndir + vd[i]; };
+      for (size_t i = 0; i < nf; ++i) ++cnt[bucket(i) + 1];
+      for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
+      for (size_t i = 0; i < nf; ++i) order[cnt[bucket(i)]++] = (int)i;
     }
-    std::vector<int> order(front.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int a, int b) { return kk[a] != kk[b] ? kk[a] > kk[b] : vd[a] < vd[b]; });
-    std::vector<int> hslot, hvdir, hu0;
-    std::vector<i64> ks;
-    for (int i : order) {
-      hslot.push_back(front[i].slot);
-      hvdir.push_back(vd[i]);
-      ks.push_back(kk[i]);
-      for (int j = 0; j < nv; ++j) hu0.push_back(front[i].u[j]);
+    std::vector<int> hslot(nf), hvdir(nf), hu0(nf * nv);
+    std::vector<i64> ks(nf);
+    for (size_t o = 0; o < nf; ++o) {
+      const int i = order[o];
+      hslot[o] = front[i].slot;
+      hvdir[o] = vd[i];
+      ks[o] = kk[i];
+      for (int j = 0; j < nv; ++j) hu0[o * nv + j] = front[i].u[j];
     }
     d_slot_.stage(hslot, stager_, st_);
     d_vdir_.stage(hvdir, stager_, st_);
@@ -670,49 +640,52 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     led.matvecs += run_sweep(ks);
     auto hp4 = std::chrono::steady_clock::now();
     led.startups += (i64)front.size();
-    // land every state at pole P - k
+    // land every state at pole P - k; a state landing on a key already there
+    // is combined at once (reduction.hpp:502 combines after every sweep)
     std::vector<int> fs, fc, fu;
-    std::unordered_map<int, std::vector<int>> merges;  // dst slot -> merged slots
+    std::vector<std::pair<int, int>> merges;  // (dst slot, src slot)
     for (int i : order) {
       HS h = front[i];
       const Expo& v = dirs_host_[vd[i]];
       for (int j = 0; j < nv; ++j) h.u[j] -= (int)(kk[i] * v[j]);
       h.pole -= (int)kk[i];
+      const u64 kh = key(h.col, h.u);
       if (h.pole == n_) {
         fs.push_back(h.slot);
         fc.push_back(h.col);
         for (int j = 0; j < nv; ++j) fu.push_back(h.u[j]);
         floor_arrivals[h.col]++;
-        floor_keys[h.col].insert(key(h.col, h.u));
+        floor_keys[h.col].insert(kh, 0);
       } else {
         auto& idx = landed_idx[h.pole];
         auto& lst = landed[h.pole];
-        u64 kh = key(h.col, h.u);
-        auto it = idx.find(kh);
-        if (it == idx.end()) {
-          idx.emplace(kh, (int)lst.size());
+        const int pos = idx.insert(kh, (int)lst.size());
+        if (pos == (int)lst.size()) {
           lst.push_back(h);
         } else {
-          merges[lst[it->second].slot].push_back(h.slot);
+          merges.emplace_back(lst[pos].slot, h.slot);
           led.combines += 1;
         }
       }
     }
     if (!merges.empty()) {
+      std::sort(merges.begin(), merges.end());
       std::vector<int> gptr{0}, mem;
-      for (auto& kv : merges) {
-        mem.push_back(kv.first);
-        mem.insert(mem.end(), kv.second.begin(), kv.second.end());
+      for (size_t a = 0; a < merges.size();) {
+        size_t b2 = a;
+        mem.push_back(merges[a].first);
+        while (b2 < merges.size() && merges[b2].first == merges[a].first) mem.push_back(merges[b2++].second);
         gptr.push_back((int)mem.size());
+        a = b2;
       }
-      d_b.stage(gptr, stager_, st_);
-      d_c.stage(mem, stager_, st_);
-      dim3 gm((unsigned)((T.side + 127) / 128) * merges.size());
+      d_mp.stage(gptr, stager_, st_);
+      d_mm.stage(mem, stager_, st_);
+      const size_t ng = gptr.size() - 1;
+      dim3 gm((unsigned)((T.side + 127) / 128) * ng);
       timed(&clock.other_ms, [&] {
-        dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_b.p, d_c.p);
+        dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_mp.p, d_mm.p);
       });
-      for (auto& kv : merges)
-        for (int s : kv.second) free_slot(s);
+      for (auto& m : merges) free_slot(m.second);
     }
     auto hp5 = std::chrono::steady_clock::now();
     {

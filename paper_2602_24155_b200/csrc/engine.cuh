@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstring>
 #include <functional>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -210,6 +211,7 @@ class ReductionEngine {
   cudaEvent_t ev0_, ev1_;
   Stager stager_;
   double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
+  unsigned host_threads_ = std::max(1u, std::thread::hardware_concurrency());
   std::vector<Expo> dirs_host_;
 };
 
