@@ -209,6 +209,62 @@ __global__ void __launch_bounds__(THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int m = m0 + quarter * 32 + lane;
       const bool mok = m < epi.M;
+      if (epi.b_mn && epi.mode == (int)TcEpilogue::carry) {
+        // carry on state-contiguous rows, software-pipelined: the 16-byte
+        // loads of chunk c+16 are in flight while chunk c is computed
+        const size_t P = (size_t)epi.P;
+        const bool last = epi.k + 1 >= epi.Ld;
+        const int cbeg = half * (BN / 2), cend = (half + 1) * (BN / 2);
+        const int8_t* bgk = epi.Bg + ((size_t)epi.k * epi.nLp + m) * P;
+        const int8_t* bgk1 = epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P;
+        uint4 nbk = make_uint4(0, 0, 0, 0), nbk1 = nbk, nc0 = nbk, nc1 = nbk;
+        auto fetch = [&](int c) {
+          const int nb = n0 + c;
+          if (!mok || nb >= epi.N) return;
+          nbk = __ldg(reinterpret_cast<const uint4*>(bgk + nb));
+          if (!last) nbk1 = __ldg(reinterpret_cast<const uint4*>(bgk1 + nb));
+          if (epi.k) {
+            const uint4* cyp = reinterpret_cast<const uint4*>(epi.Cy + (size_t)m * P + nb);
+            nc0 = cyp[0];
+            nc1 = cyp[1];
+          }
+        };
+        fetch(cbeg);
+        for (int c = cbeg; c < cend; c += 16) {
+          const uint4 bk = nbk, bk1 = nbk1, c0 = nc0, c1 = nc1;
+          if (c + 16 < cend) fetch(c + 16);
+          int v[16];
+          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+          const int nb = n0 + c;
+          if (!mok || nb >= epi.N) continue;
+          const uint32_t bw[4] = {bk.x, bk.y, bk.z, bk.w};
+          const uint32_t b1w[4] = {bk1.x, bk1.y, bk1.z, bk1.w};
+          const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          uint32_t cn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          uint32_t in4[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int b0j = (int)(int8_t)(bw[j >> 2] >> (8 * (j & 3)));
+            const int b1j = (int)(int8_t)(b1w[j >> 2] >> (8 * (j & 3)));
+            const int ccj = epi.k ? (int)(int16_t)(cw[j >> 1] >> (16 * (j & 1))) : 0;
+            int cnew, inb;
+            if (epi.fast) {
+              cnew = epi.fq.div_exact_fast(b0j + ccj - v[j]);
+              inb = epi.fq.bal_fast(b1j + cnew);
+            } else {
+              int rem;
+              cnew = epi.fq.divfloor(b0j + ccj - v[j], rem);  // exact
+              inb = epi.fq.bal(b1j + cnew);
+            }
+            cn[j >> 1] |= ((uint32_t)cnew & 0xFFFFu) << (16 * (j & 1));
+            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * (j & 3));
+          }
+          uint4* cyw = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
+          cyw[0] = make_uint4(cn[0], cn[1], cn[2], cn[3]);
+          cyw[1] = make_uint4(cn[4], cn[5], cn[6], cn[7]);
+          if (!last) *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+        }
+      } else
       for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
         int v[16];
         tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
