@@ -506,3 +506,38 @@ extern "C" int drzg_test_tc_gemm_mn(int32_t M, int32_t N, int32_t K, const int8_
     DRZG_CUDA(cudaMemcpy(D, dD.p, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
   });
 }
+
+// test hook: host vs device pivot scan (rows x cols over F_p) and inverse mod
+// q (n x n, made invertible by construction); *mismatches = differing entries
+extern "C" int drzg_test_setup(uint64_t p, uint64_t q, int32_t n, int32_t cols, uint64_t seed, int64_t* mismatches) {
+  return guard_int([&] {
+    std::mt19937_64 rng(seed);
+    std::vector<u32> m((size_t)n * cols);
+    for (auto& x : m) x = (u32)(rng() % p);
+    auto host = pivot_scan_fp(p, n, cols, m);
+    auto devp = pivot_scan_device(p, n, cols, m);
+    i64 bad = 0;
+    for (int r = 0; r < n; ++r) bad += host.pivot_col_of_row[r] != devp[r];
+    // unit lower x unit upper (mod q) is invertible
+    std::vector<u32> a((size_t)n * n, 0);
+    {
+      std::vector<u64> Lm((size_t)n * n, 0), Um((size_t)n * n, 0);
+      for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+          if (j < i) Lm[(size_t)i * n + j] = rng() % q;
+          if (j > i) Um[(size_t)i * n + j] = rng() % q;
+        }
+      for (int i = 0; i < n; ++i) Lm[(size_t)i * n + i] = Um[(size_t)i * n + i] = 1 + rng() % (p - 1);
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k <= i; ++k) {
+          u64 l = Lm[(size_t)i * n + k];
+          if (!l) continue;
+          for (int j = k; j < n; ++j) a[(size_t)i * n + j] = (u32)((a[(size_t)i * n + j] + l * Um[(size_t)k * n + j]) % q);
+        }
+    }
+    auto hi = inverse_mod_q(p, q, n, a);
+    auto di = inverse_mod_q_device(p, q, n, a);
+    for (size_t i = 0; i < hi.size(); ++i) bad += hi[i] != di[i];
+    *mismatches = bad;
+  });
+}

@@ -135,7 +135,13 @@ class FinalReducer {
       for (int s = 0; s < (int)B_->h[m]; ++s) data[(size_t)rank_of(B_->mons[base + s]) * L.ncols + col + s] = 1;
       std::vector<u32> modp(data.size());
       for (size_t e = 0; e < data.size(); ++e) modp[e] = data[e] % (u32)X_->p;
-      PivotScan ps = pivot_scan_fp(X_->p, L.rows, L.ncols, std::move(modp));
+      PivotScan ps;
+      if (L.rows >= kDeviceSetupMin) {
+        ps.pivot_col_of_row = pivot_scan_device(X_->p, L.rows, L.ncols, modp);
+        for (int pc : ps.pivot_col_of_row) ps.rank += pc >= 0;
+      } else {
+        ps = pivot_scan_fp(X_->p, L.rows, L.ncols, std::move(modp));
+      }
       DRZG_REQUIRE(ps.rank == L.rows, "FinalReducer: class outside Jacobian + basis span");
       L.pc = ps.pivot_col_of_row;
       L.sys = make_dixon(dp_, L.rows, L.ncols, data, L.pc);

@@ -25,6 +25,7 @@
 #include <set>
 #include <vector>
 
+#include "../kernels/setup.cuh"
 #include "cohom.hpp"
 #include "policy.hpp"
 
@@ -80,7 +81,8 @@ inline DixonSystem make_dixon(const DigitPlan& dp, int rows, int cols, const std
     }
     sys.rowptr[r + 1] = (i32)sys.col.size();
   }
-  auto inv = inverse_mod_q(dp.p, (u64)dp.q, rows, std::move(sq));
+  auto inv = rows >= kDeviceSetupMin ? inverse_mod_q_device(dp.p, (u64)dp.q, rows, sq)
+                                     : inverse_mod_q(dp.p, (u64)dp.q, rows, std::move(sq));
   sys.Cq.resize(inv.size());
   for (size_t i = 0; i < inv.size(); ++i) {
     int v = (int)inv[i];
@@ -152,7 +154,13 @@ inline RuvTables build_tables(const Hypersurface& X, int M, const std::set<int>&
   }
   std::vector<u32> Jp_mod_p(J.size());
   for (size_t k = 0; k < J.size(); ++k) Jp_mod_p[k] = (u32)(J[k] % X.p);
-  PivotScan ps = pivot_scan_fp(X.p, T.nL, cols, std::move(Jp_mod_p));
+  PivotScan ps;
+  if (T.nL >= kDeviceSetupMin) {
+    ps.pivot_col_of_row = pivot_scan_device(X.p, T.nL, cols, Jp_mod_p);
+    for (int pc : ps.pivot_col_of_row) ps.rank += pc >= 0;
+  } else {
+    ps = pivot_scan_fp(X.p, T.nL, cols, std::move(Jp_mod_p));
+  }
   DRZG_REQUIRE(ps.rank == T.nL, "RuvContext: solve failed; input not S-smooth enough");
   T.sys = make_dixon(T.dp, T.nL, cols, J, ps.pivot_col_of_row);
 
