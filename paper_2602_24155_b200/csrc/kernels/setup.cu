@@ -46,15 +46,24 @@ __global__ void normalise_row_kernel(int* row, int cols, int m, const int* cptr,
   }
 }
 
-// rows [r_lo, r_hi) (except `skip`) += (m - f_r) * pivot_row, f_r = a[r][c] mod m
+// f[r] = a[r][c] mod m for rows [r_lo, r_hi): snapshot of the pivot column
+// taken before any block of the update can zero it
+__global__ void factors_kernel(const int* a, int ld, int r_lo, int r_hi, const int* cptr, int m, int* f) {
+  const int c = *cptr;
+  const int r = r_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r_hi) return;
+  f[r] = c < 0 ? 0 : ((a[(size_t)r * ld + c] % m) + m) % m;
+}
+
+// rows [r_lo, r_hi) (except `skip`) += (m - f_r) * pivot_row
 __global__ void eliminate_kernel(int* a, int ld, int cols, int r_lo, int r_hi, int skip, const int* pivot_row,
-                                 const int* cptr, int m) {
+                                 const int* cptr, int m, const int* fac) {
   const int c = *cptr;
   if (c < 0) return;
   const int r = r_lo + blockIdx.y;
   if (r >= r_hi || r == skip) return;
   int* row = a + (size_t)r * ld;
-  const int f = ((row[c] % m) + m) % m;
+  const int f = fac[r];
   if (f == 0) return;
   const int g = m - f;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) row[j] += g * pivot_row[j];
@@ -106,8 +115,9 @@ std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<
   DRZG_REQUIRE((int64_t)rows * ((int64_t)(p - 1) * (p - 1) + p) < (1ll << 31), "pivot_scan_device: lazy bound");
   cudaStream_t st;
   ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
-  int *da = nullptr, *dpiv = nullptr, *dinv = nullptr;
+  int *da = nullptr, *dpiv = nullptr, *dinv = nullptr, *dfac = nullptr;
   size_t nn = (size_t)rows * cols;
+  ck(cudaMallocAsync(&dfac, rows * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&da, nn * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&dpiv, rows * sizeof(int), st), "alloc");
   auto itab = inverse_table((int)p, (int)p);
@@ -123,10 +133,11 @@ std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<
     dev::normalise_row_kernel<<<cblocks, threads, 0, st>>>(row, cols, (int)p, dpiv + r, dinv);
     if (r + 1 < rows) {
       // rows below, in slabs of 65535 (grid.y limit)
+      dev::factors_kernel<<<(rows - r - 1 + 255) / 256, 256, 0, st>>>(da, cols, r + 1, rows, dpiv + r, (int)p, dfac);
       for (int lo = r + 1; lo < rows; lo += 65535) {
         int hi = std::min(rows, lo + 65535);
         dim3 g(cblocks, hi - lo);
-        dev::eliminate_kernel<<<g, threads, 0, st>>>(da, cols, cols, lo, hi, -1, row, dpiv + r, (int)p);
+        dev::eliminate_kernel<<<g, threads, 0, st>>>(da, cols, cols, lo, hi, -1, row, dpiv + r, (int)p, dfac);
       }
     }
   }
@@ -137,6 +148,7 @@ std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<
   cudaFreeAsync(da, st);
   cudaFreeAsync(dpiv, st);
   cudaFreeAsync(dinv, st);
+  cudaFreeAsync(dfac, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   return piv;
@@ -152,7 +164,8 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
     for (int j = 0; j < n; ++j) h[(size_t)i * w + j] = (int)(a[(size_t)i * n + j] % q);
     h[(size_t)i * w + n + i] = 1;
   }
-  int *da = nullptr, *dr = nullptr, *dc = nullptr, *dinv = nullptr;
+  int *da = nullptr, *dr = nullptr, *dc = nullptr, *dinv = nullptr, *dfac = nullptr;
+  ck(cudaMallocAsync(&dfac, n * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&da, h.size() * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&dr, sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&dc, sizeof(int), st), "alloc");
@@ -168,10 +181,11 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
     dev::set_const_kernel<<<1, 1, 0, st>>>(dc, c);
     int* prow = da + (size_t)c * w;
     dev::normalise_row_kernel<<<cblocks, threads, 0, st>>>(prow, w, (int)q, dc, dinv);
+    dev::factors_kernel<<<(n + 255) / 256, 256, 0, st>>>(da, w, 0, n, dc, (int)q, dfac);
     for (int lo = 0; lo < n; lo += 65535) {
       int hi = std::min(n, lo + 65535);
       dim3 g(cblocks, hi - lo);
-      dev::eliminate_kernel<<<g, threads, 0, st>>>(da, w, w, lo, hi, c, prow, dc, (int)q);
+      dev::eliminate_kernel<<<g, threads, 0, st>>>(da, w, w, lo, hi, c, prow, dc, (int)q, dfac);
     }
   }
   dev::reduce_all_kernel<<<1024, 256, 0, st>>>(da, h.size(), (int)q);
@@ -184,6 +198,7 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
   cudaFreeAsync(dr, st);
   cudaFreeAsync(dc, st);
   cudaFreeAsync(dinv, st);
+  cudaFreeAsync(dfac, st);
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   std::vector<u32> inv((size_t)n * n);
