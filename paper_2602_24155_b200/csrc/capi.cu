@@ -541,3 +541,21 @@ extern "C" int drzg_test_setup(uint64_t p, uint64_t q, int32_t n, int32_t cols, 
     *mismatches = bad;
   });
 }
+
+// test hook: build the reduction tables with the host and the device setup
+// and count differing pivot choices / inverse entries
+extern "C" int drzg_test_tables(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int64_t* diff) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    setenv("DRZG_SETUP", "host", 1);
+    RuvTables A = build_tables(X, M, default_S(n, d));
+    setenv("DRZG_SETUP", "device", 1);
+    RuvTables B = build_tables(X, M, default_S(n, d));
+    unsetenv("DRZG_SETUP");
+    i64 bad = 0;
+    for (size_t i = 0; i < A.sol_row.size(); ++i) bad += A.sol_row[i] != B.sol_row[i] || A.sol_i[i] != B.sol_i[i];
+    for (size_t i = 0; i < A.sys.Cq.size(); ++i) bad += A.sys.Cq[i] != B.sys.Cq[i];
+    bad += A.sys.col != B.sys.col || A.sys.val != B.sys.val;
+    *diff = bad;
+  });
+}

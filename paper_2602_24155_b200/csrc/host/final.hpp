@@ -136,7 +136,7 @@ class FinalReducer {
       std::vector<u32> modp(data.size());
       for (size_t e = 0; e < data.size(); ++e) modp[e] = data[e] % (u32)X_->p;
       PivotScan ps;
-      if (L.rows >= kDeviceSetupMin) {
+      if (use_device_setup(L.rows)) {
         ps.pivot_col_of_row = pivot_scan_device(X_->p, L.rows, L.ncols, modp);
         for (int pc : ps.pivot_col_of_row) ps.rank += pc >= 0;
       } else {

@@ -81,8 +81,8 @@ inline DixonSystem make_dixon(const DigitPlan& dp, int rows, int cols, const std
     }
     sys.rowptr[r + 1] = (i32)sys.col.size();
   }
-  auto inv = rows >= kDeviceSetupMin ? inverse_mod_q_device(dp.p, (u64)dp.q, rows, sq)
-                                     : inverse_mod_q(dp.p, (u64)dp.q, rows, std::move(sq));
+  auto inv = use_device_setup(rows) ? inverse_mod_q_device(dp.p, (u64)dp.q, rows, sq)
+                                    : inverse_mod_q(dp.p, (u64)dp.q, rows, std::move(sq));
   sys.Cq.resize(inv.size());
   for (size_t i = 0; i < inv.size(); ++i) {
     int v = (int)inv[i];
@@ -155,7 +155,7 @@ inline RuvTables build_tables(const Hypersurface& X, int M, const std::set<int>&
   std::vector<u32> Jp_mod_p(J.size());
   for (size_t k = 0; k < J.size(); ++k) Jp_mod_p[k] = (u32)(J[k] % X.p);
   PivotScan ps;
-  if (T.nL >= kDeviceSetupMin) {
+  if (use_device_setup(T.nL)) {
     ps.pivot_col_of_row = pivot_scan_device(X.p, T.nL, cols, Jp_mod_p);
     for (int pc : ps.pivot_col_of_row) ps.rank += pc >= 0;
   } else {

@@ -1,6 +1,8 @@
 // Setup-time eliminations on the device (see setup.cu).
 #pragma once
 
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "../host/common.hpp"
@@ -16,5 +18,12 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
 
 // order at which the device versions are used (host below: launch latency wins)
 constexpr int kDeviceSetupMin = 768;
+// DRZG_SETUP=host|device overrides the size rule (tests compare both)
+inline bool use_device_setup(int n) {
+  const char* e = std::getenv("DRZG_SETUP");
+  if (e && std::string(e) == "host") return false;
+  if (e && std::string(e) == "device") return true;
+  return n >= kDeviceSetupMin;
+}
 
 }  // namespace drzg
