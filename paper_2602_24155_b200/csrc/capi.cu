@@ -559,3 +559,29 @@ extern "C" int drzg_test_tables(uint64_t p, int32_t n, int32_t d, const uint64_t
     *diff = bad;
   });
 }
+
+extern "C" int drzg_test_final_levels(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int64_t* diff) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    Basis B = compute_basis(X);
+    DigitPlan dp = DigitPlan::make(p, M);
+    HostMod hm = HostMod::make(p, M);
+    setenv("DRZG_SETUP", "host", 1);
+    FinalReducer fa(X, B, dp, hm);
+    fa.prepare();
+    setenv("DRZG_SETUP", "device", 1);
+    FinalReducer fb(X, B, dp, hm);
+    fb.prepare();
+    unsetenv("DRZG_SETUP");
+    i64 bad = 0;
+    for (int m = 1; m <= n; ++m) {
+      bad += fa.level_pivots(m) != fb.level_pivots(m) ? 1000000 : 0;
+      const auto& a = fa.level_inverse(m);
+      const auto& b = fb.level_inverse(m);
+      if (a.size() != b.size()) bad += 1000;
+      else
+        for (size_t i = 0; i < a.size(); ++i) bad += a[i] != b[i];
+    }
+    *diff = bad;
+  });
+}

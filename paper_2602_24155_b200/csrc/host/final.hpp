@@ -57,6 +57,10 @@ class FinalReducer {
     for (int m = 1; m <= X_->n; ++m) level(m);
   }
 
+  // test access: pivot columns and inverse of level m
+  const std::vector<int>& level_pivots(int m) const { return levels_.at(m).pc; }
+  const std::vector<i8>& level_inverse(int m) const { return levels_.at(m).sys.Cq; }
+
   // g over monos(nv, dm-n-1) as residues mod p^M; returns the b-vector
   std::vector<Z> reduce(std::vector<Z> g, int m) const {
     DRZG_REQUIRE(m >= 1 && m <= X_->n, "FinalReducer: pole order out of range");
