@@ -33,13 +33,18 @@ __global__ void first_nonzero_kernel(const int* row, int cols, int p, int* out) 
   if (threadIdx.x == 0) *out = best < cols ? best : -1;
 }
 
-// normalise row r by the inverse of row[c] (mod m, table lookup); also
-// reduces it fully; skipped when c < 0
-__global__ void normalise_row_kernel(int* row, int cols, int m, const int* cptr, const int* inv_tab) {
+// inverse of the pivot entry, taken once before any block rescales the row
+__global__ void pivot_inverse_kernel(const int* row, int m, const int* cptr, const int* inv_tab, int* iv_out) {
+  const int c = *cptr;
+  if (c >= 0) *iv_out = inv_tab[((row[c] % m) + m) % m];
+}
+
+// normalise row r by the pivot inverse *ivp (and reduce it fully); skipped
+// when c < 0
+__global__ void normalise_row_kernel(int* row, int cols, int m, const int* cptr, const int* ivp) {
   const int c = *cptr;
   if (c < 0) return;
-  const int pv = ((row[c] % m) + m) % m;
-  const int iv = inv_tab[pv];
+  const int iv = *ivp;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x) {
     int v = ((row[j] % m) + m) % m;
     row[j] = (v * iv) % m;
@@ -117,7 +122,7 @@ std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<
   ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
   int *da = nullptr, *dpiv = nullptr, *dinv = nullptr, *dfac = nullptr;
   size_t nn = (size_t)rows * cols;
-  ck(cudaMallocAsync(&dfac, rows * sizeof(int), st), "alloc");
+  ck(cudaMallocAsync(&dfac, (rows + 1) * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&da, nn * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&dpiv, rows * sizeof(int), st), "alloc");
   auto itab = inverse_table((int)p, (int)p);
@@ -130,7 +135,8 @@ std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<
   for (int r = 0; r < rows; ++r) {
     int* row = da + (size_t)r * cols;
     dev::first_nonzero_kernel<<<1, 1024, 0, st>>>(row, cols, (int)p, dpiv + r);
-    dev::normalise_row_kernel<<<cblocks, threads, 0, st>>>(row, cols, (int)p, dpiv + r, dinv);
+    dev::pivot_inverse_kernel<<<1, 1, 0, st>>>(row, (int)p, dpiv + r, dinv, dfac + rows);
+    dev::normalise_row_kernel<<<cblocks, threads, 0, st>>>(row, cols, (int)p, dpiv + r, dfac + rows);
     if (r + 1 < rows) {
       // rows below, in slabs of 65535 (grid.y limit)
       dev::factors_kernel<<<(rows - r - 1 + 255) / 256, 256, 0, st>>>(da, cols, r + 1, rows, dpiv + r, (int)p, dfac);
@@ -165,7 +171,7 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
     h[(size_t)i * w + n + i] = 1;
   }
   int *da = nullptr, *dr = nullptr, *dc = nullptr, *dinv = nullptr, *dfac = nullptr;
-  ck(cudaMallocAsync(&dfac, n * sizeof(int), st), "alloc");
+  ck(cudaMallocAsync(&dfac, (n + 1) * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&da, h.size() * sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&dr, sizeof(int), st), "alloc");
   ck(cudaMallocAsync(&dc, sizeof(int), st), "alloc");
@@ -180,7 +186,8 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
     dev::swap_rows_kernel<<<cblocks, threads, 0, st>>>(da, w, w, c, dr);
     dev::set_const_kernel<<<1, 1, 0, st>>>(dc, c);
     int* prow = da + (size_t)c * w;
-    dev::normalise_row_kernel<<<cblocks, threads, 0, st>>>(prow, w, (int)q, dc, dinv);
+    dev::pivot_inverse_kernel<<<1, 1, 0, st>>>(prow, (int)q, dc, dinv, dfac + n);
+    dev::normalise_row_kernel<<<cblocks, threads, 0, st>>>(prow, w, (int)q, dc, dfac + n);
     dev::factors_kernel<<<(n + 255) / 256, 256, 0, st>>>(da, w, 0, n, dc, (int)q, dfac);
     for (int lo = 0; lo < n; lo += 65535) {
       int hi = std::min(n, lo + 65535);
