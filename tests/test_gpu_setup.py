@@ -20,3 +20,16 @@ def test_device_setup_matches_host():
                                ctypes.byref(bad))
         assert rc == 0, drzg._err()
         assert bad.value == 0
+
+
+@pytest.mark.parametrize("p,n,d,M", [(7, 5, 3, 7), (7, 5, 3, 24), (11, 3, 4, 17)])
+def test_device_tables_and_final_levels_match_host(p, n, d, M):
+    # the random fourfold's 3003 x 6237 solve matrix and 2002-row final level
+    # take the device path; both must equal the host restatement exactly
+    import ctypes
+    L = drzg.lib()
+    co = drzg.random_hypersurface(p, n, d, 1)
+    for fn in (L.drzg_test_tables, L.drzg_test_final_levels):
+        diff = ctypes.c_int64(-1)
+        assert fn(ctypes.c_uint64(p), n, d, drzg._u64arr(co), M, ctypes.byref(diff)) == 0, drzg._err()
+        assert diff.value == 0
