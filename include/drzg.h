@@ -95,6 +95,10 @@ int drzg_random_hypersurface(uint64_t p, int32_t n, int32_t d, uint64_t seed, in
 int drzg_count_points(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r, int64_t budget,
                       int64_t* out);
 
+/* the same count enumerated on the GPU (one thread per point) */
+int drzg_count_points_device(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r, int64_t budget,
+                             int64_t* out);
+
 /* charpoly + recover_Q on a given F (zeta.hpp:456-470); F as b*b decimal strings */
 char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t nm_override, int32_t b,
                     const char* const* F);

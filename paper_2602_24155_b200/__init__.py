@@ -182,6 +182,14 @@ def count_points(p, n, d, coeffs, r, budget=200_000_000):
     return out.value
 
 
+def count_points_device(p, n, d, coeffs, r, budget=200_000_000):
+    """the GPU point count (kernels/count.cu)"""
+    out = ctypes.c_int64()
+    _check(lib().drzg_count_points_device(ctypes.c_uint64(p), n, d, _u64arr(coeffs), r, ctypes.c_int64(budget),
+                                          ctypes.byref(out)))
+    return out.value
+
+
 def charpoly(p, n, d, F, b, r_uniform=0, nm=0):
     """berkowitz_charpoly + recover_Q on a given F (zeta.hpp:456-470)"""
     arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F])

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/drzg.h"
+#include "kernels/count.cuh"
 #include "kernels/linrec.cuh"
 #include "kernels/tc_gemm.cuh"
 #include "pipeline.cuh"
@@ -371,6 +372,15 @@ int drzg_count_points(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, 
   return guard_int([&] {
     Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
     *out = count_points(X, r, budget);
+  });
+}
+
+// the device enumeration (kernels/count.cu)
+int drzg_count_points_device(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r, int64_t budget,
+                             int64_t* out) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    *out = count_points_device(X, r, budget);
   });
 }
 

@@ -7,6 +7,7 @@
 #include <thread>
 
 #include "pipeline.cuh"
+#include "kernels/count.cuh"
 
 namespace drzg {
 
@@ -185,6 +186,16 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   return out;
 }
 
+namespace {
+// #X(F_{p^r}): device enumeration for large fields, host below
+i64 count_points_any(const Hypersurface& X, int r, i64 budget) {
+  Z pts(0);
+  for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
+  if (pts >= Z((long)kDeviceCountMin)) return count_points_device(X, r, budget);
+  return count_points(X, r, budget);
+}
+}  // namespace
+
 ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
   double t0 = now_s();
   if (!check_smooth(X, full_set(X.nv())))
@@ -224,7 +235,7 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
         for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
         if (pts > Z((long)opt.count_budget)) break;
         ++rounds;
-        Z truth((long)count_points(X, r, opt.count_budget));
+        Z truth((long)count_points_any(X, r, opt.count_budget));
         std::vector<std::vector<Z>> kept;
         for (auto& c : cands)
           if (counts_from_zeta(c, X.p, X.n, r) == truth) kept.push_back(c);
@@ -258,7 +269,7 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
         CountCheck ck;
         ck.r = r;
         ck.from_zeta = counts_from_zeta(a, X.p, X.n, r);
-        ck.from_count = Z((long)count_points(X, r, opt.count_budget));
+        ck.from_count = Z((long)count_points_any(X, r, opt.count_budget));
         ck.ok = ck.from_zeta == ck.from_count;
         counts_ok = counts_ok && ck.ok;
         checks.push_back(ck);

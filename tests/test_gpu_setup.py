@@ -33,3 +33,10 @@ def test_device_tables_and_final_levels_match_host(p, n, d, M):
         diff = ctypes.c_int64(-1)
         assert fn(ctypes.c_uint64(p), n, d, drzg._u64arr(co), M, ctypes.byref(diff)) == 0, drzg._err()
         assert diff.value == 0
+
+
+@pytest.mark.parametrize("p,n,d,r", [(7, 2, 5, 2), (11, 3, 4, 1), (11, 3, 4, 2), (13, 4, 3, 1), (7, 5, 3, 1),
+                                     (7, 3, 5, 2)])
+def test_device_point_count_matches_host(p, n, d, r):
+    co = drzg.random_hypersurface(p, n, d, 1)
+    assert drzg.count_points_device(p, n, d, co, r) == drzg.count_points(p, n, d, co, r)
