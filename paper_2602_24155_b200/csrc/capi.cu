@@ -120,7 +120,8 @@ std::string frob_json_body(const FrobResult& fr) {
      << ",\"kernels\":{\"gemm_ms\":" << fr.clk.gemm_ms << ",\"carry_ms\":" << fr.clk.carry_ms
      << ",\"gather_ms\":" << fr.clk.gather_ms << ",\"epilogue_ms\":" << fr.clk.epi_ms
      << ",\"other_ms\":" << fr.clk.other_ms << ",\"gemm_launches\":" << fr.clk.gemm_launches
-     << ",\"gemm_macs\":" << fr.clk.gemm_macs << ",\"device_ms\":" << fr.clk.device_ms << ",\"peak_live_states\":" << fr.clk.peak_live << "}"
+     << ",\"gemm_macs\":" << fr.clk.gemm_macs << ",\"carry_launches\":" << fr.clk.carry_launches
+     << ",\"carry_macs\":" << fr.clk.carry_macs << ",\"device_ms\":" << fr.clk.device_ms << ",\"peak_live_states\":" << fr.clk.peak_live << "}"
      << ",\"traffic\":{\"h2d_bytes\":" << g_traffic.h2d.load() << ",\"d2h_bytes\":" << g_traffic.d2h.load()
      << ",\"launches\":" << g_traffic.launches.load() << "}";
   return os.str();

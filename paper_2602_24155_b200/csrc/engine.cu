@@ -345,8 +345,8 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
         timed(&clock.carry_ms, [&] {
           tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
         });
-        ++clock.gemm_launches;
-        clock.gemm_macs += (double)T.nL * T.nL * nb;
+        ++clock.carry_launches;
+        clock.carry_macs += (double)T.nL * T.nL * nb;
       }
     } else {
       timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });

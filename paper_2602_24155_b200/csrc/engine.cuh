@@ -48,7 +48,9 @@ struct KernelClock {
   i64 gemm_launches = 0;
   double device_ms = 0;  // CUDA-event time of the whole device-resident run
   i64 peak_live = 0;     // most state slots live at once
-  double gemm_macs = 0;  // algorithmic int8 MACs issued (nL x nL per state-digit)
+  double gemm_macs = 0;  // digit GEMMs: int8 MACs issued (nL x nL per state-digit)
+  i64 carry_launches = 0;
+  double carry_macs = 0; // carry GEMMs (Jp . y_k)
 };
 
 // pinned staging ring: host-side inputs of a sweep are copied through
