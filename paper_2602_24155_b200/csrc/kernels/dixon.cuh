@@ -152,34 +152,50 @@ __global__ void __launch_bounds__(256) gather_w_kernel(StepArgs a) {
   }
 }
 
-// w' = T_x y into W (Ld x sidep x P), carry-normalised digits; lanes = states
+__device__ __forceinline__ int pick6(int i, int x0, int x1, int x2, int x3, int x4, int x5) {
+  return i == 0 ? x0 : i == 1 ? x1 : i == 2 ? x2 : i == 3 ? x3 : i == 4 ? x4 : x5;
+}
+
+// w' = T_x y into W (Ld x sidep x P), carry-normalised digits; lanes = states.
+// LD = digit planes at compile time so the per-digit accumulators live in
+// registers (a runtime-indexed array would sit in local memory)
+template <int LD>
 __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = blockIdx.x * 32 + lane;
   if (s >= a.B) return;
-  int x[6] = {0, 0, 0, 0, 0, 0};
   const int vd = a.vdir[s];
   const bool cont = a.y < a.ks[s];
+  int x0 = 0, x1 = 0, x2 = 0, x3 = 0, x4 = 0, x5 = 0;
   {
     const int* v = a.dirs + (size_t)vd * a.nv;
-    for (int i = 0; i < a.nv; ++i) x[i] = a.u0[(size_t)s * a.nv + i] - a.y * v[i];
+    const int* u = a.u0 + (size_t)s * a.nv;
+    x0 = u[0] - a.y * v[0];
+    if (a.nv > 1) x1 = u[1] - a.y * v[1];
+    if (a.nv > 2) x2 = u[2] - a.y * v[2];
+    if (a.nv > 3) x3 = u[3] - a.y * v[3];
+    if (a.nv > 4) x4 = u[4] - a.y * v[4];
+    if (a.nv > 5) x5 = u[5] - a.y * v[5];
   }
   const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
   for (int g = blockIdx.y * 64 + warp; g < min(a.side, (int)(blockIdx.y + 1) * 64); g += 8) {
-    int acc[kLdMax];
-    for (int t = 0; t < a.Ld; ++t) acc[t] = 0;
+    int acc[LD];
+#pragma unroll
+    for (int t = 0; t < LD; ++t) acc[t] = 0;
     for (int e = a.t_ptr[g]; e < a.t_ptr[g + 1]; ++e) {
-      int r = a.t_src[e];
-      int wgt = x[a.sol_i[r]] + a.sol_mu[r];
+      const int r = a.t_src[e];
+      const int wgt = pick6(a.sol_i[r], x0, x1, x2, x3, x4, x5) + a.sol_mu[r];
       const int8_t* yr = a.Y + (size_t)r * a.P + s;
-      for (int t = 0; t < a.Ld; ++t) acc[t] += wgt * (int)yr[(size_t)t * plane];
+#pragma unroll
+      for (int t = 0; t < LD; ++t) acc[t] += wgt * (int)__ldg(yr + (size_t)t * plane);
     }
     // the next step of this chunk reads row ginv[v][g] of its operand: write
     // it there directly (lanes of a (k, v)-sorted batch share v); a state
     // whose chunk ends here goes to W for the flush into the slot pool
     const int rn = cont ? a.ginv[(size_t)vd * a.side + g] : -1;
     int carry = 0;
-    for (int t = 0; t < a.Ld; ++t) {
+#pragma unroll
+    for (int t = 0; t < LD; ++t) {
       int rr, qt;
       if (a.fast) {
         rr = a.fq.balq(acc[t] + carry, qt);
@@ -193,6 +209,23 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
       else if (rn >= 0)
         a.Bg[(size_t)t * plane + (size_t)rn * a.P + s] = (int8_t)rr;
     }
+  }
+}
+
+// host dispatch over the digit-plane count
+inline void launch_epilogue(const StepArgs& a, dim3 grid, cudaStream_t st) {
+  switch (a.Ld) {
+#define DRZG_EPI(L) \
+  case L:           \
+    epilogue_kernel<L><<<grid, 256, 0, st>>>(a); \
+    break;
+    DRZG_EPI(1) DRZG_EPI(2) DRZG_EPI(3) DRZG_EPI(4) DRZG_EPI(5) DRZG_EPI(6) DRZG_EPI(7) DRZG_EPI(8)
+    DRZG_EPI(9) DRZG_EPI(10) DRZG_EPI(11) DRZG_EPI(12) DRZG_EPI(13) DRZG_EPI(14) DRZG_EPI(15) DRZG_EPI(16)
+    DRZG_EPI(17) DRZG_EPI(18) DRZG_EPI(19) DRZG_EPI(20) DRZG_EPI(21) DRZG_EPI(22) DRZG_EPI(23) DRZG_EPI(24)
+    DRZG_EPI(25) DRZG_EPI(26) DRZG_EPI(27) DRZG_EPI(28) DRZG_EPI(29) DRZG_EPI(30) DRZG_EPI(31) DRZG_EPI(32)
+#undef DRZG_EPI
+    default:
+      break;
   }
 }
 
