@@ -156,58 +156,89 @@ __device__ __forceinline__ int pick6(int i, int x0, int x1, int x2, int x3, int 
   return i == 0 ? x0 : i == 1 ? x1 : i == 2 ? x2 : i == 3 ? x3 : i == 4 ? x4 : x5;
 }
 
-// w' = T_x y into W (Ld x sidep x P), carry-normalised digits; lanes = states.
-// LD = digit planes at compile time so the per-digit accumulators live in
-// registers (a runtime-indexed array would sit in local memory)
+// w' = T_x y into W (Ld x sidep x P), carry-normalised digits.  Each lane
+// owns 4 consecutive states so every global access is a 32-bit word (four
+// states of one digit plane); LD = digit planes at compile time so the
+// accumulators live in registers.
 template <int LD>
 __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x * 32 + lane;
-  if (s >= a.B) return;
-  const int vd = a.vdir[s];
-  const bool cont = a.y < a.ks[s];
-  int x0 = 0, x1 = 0, x2 = 0, x3 = 0, x4 = 0, x5 = 0;
-  {
-    const int* v = a.dirs + (size_t)vd * a.nv;
-    const int* u = a.u0 + (size_t)s * a.nv;
-    x0 = u[0] - a.y * v[0];
-    if (a.nv > 1) x1 = u[1] - a.y * v[1];
-    if (a.nv > 2) x2 = u[2] - a.y * v[2];
-    if (a.nv > 3) x3 = u[3] - a.y * v[3];
-    if (a.nv > 4) x4 = u[4] - a.y * v[4];
-    if (a.nv > 5) x5 = u[5] - a.y * v[5];
+  const int s4 = (blockIdx.x * 32 + lane) * 4;  // first of this lane's 4 states
+  if (s4 >= a.B) return;
+  int xs[4][6];
+  int vds[4];
+  bool conts[4], valid[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int s = s4 + j;
+    valid[j] = s < a.B;
+    const int sv = valid[j] ? s : s4;
+    vds[j] = a.vdir[sv];
+    conts[j] = valid[j] && a.y < a.ks[sv];
+    const int* v = a.dirs + (size_t)vds[j] * a.nv;
+    const int* u = a.u0 + (size_t)sv * a.nv;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) xs[j][i] = i < a.nv ? u[i] - a.y * v[i] : 0;
   }
+  const bool same_v = vds[0] == vds[1] && vds[0] == vds[2] && vds[0] == vds[3];
+  const bool all_cont = conts[0] && conts[1] && conts[2] && conts[3];
+  const bool none_cont = !conts[0] && !conts[1] && !conts[2] && !conts[3] && valid[3];
   const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
   for (int g = blockIdx.y * 64 + warp; g < min(a.side, (int)(blockIdx.y + 1) * 64); g += 8) {
-    int acc[LD];
+    int acc[LD][4];
 #pragma unroll
-    for (int t = 0; t < LD; ++t) acc[t] = 0;
+    for (int t = 0; t < LD; ++t)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[t][j] = 0;
     for (int e = a.t_ptr[g]; e < a.t_ptr[g + 1]; ++e) {
       const int r = a.t_src[e];
-      const int wgt = pick6(a.sol_i[r], x0, x1, x2, x3, x4, x5) + a.sol_mu[r];
-      const int8_t* yr = a.Y + (size_t)r * a.P + s;
+      const int ii = a.sol_i[r], mu = a.sol_mu[r];
+      int wg[4];
 #pragma unroll
-      for (int t = 0; t < LD; ++t) acc[t] += wgt * (int)__ldg(yr + (size_t)t * plane);
+      for (int j = 0; j < 4; ++j) wg[j] = pick6(ii, xs[j][0], xs[j][1], xs[j][2], xs[j][3], xs[j][4], xs[j][5]) + mu;
+      const uint32_t* yr = reinterpret_cast<const uint32_t*>(a.Y + (size_t)r * a.P + s4);
+#pragma unroll
+      for (int t = 0; t < LD; ++t) {
+        const uint32_t w4 = yr[(t * plane) >> 2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[t][j] += wg[j] * (int)(int8_t)(w4 >> (8 * j));
+      }
     }
-    // the next step of this chunk reads row ginv[v][g] of its operand: write
-    // it there directly (lanes of a (k, v)-sorted batch share v); a state
-    // whose chunk ends here goes to W for the flush into the slot pool
-    const int rn = cont ? a.ginv[(size_t)vd * a.side + g] : -1;
-    int carry = 0;
+    // next step's operand row of side row g (per state's v), or W at chunk end
+    int rn[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? a.ginv[(size_t)vds[j] * a.side + g] : -1;
+    int carry[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int t = 0; t < LD; ++t) {
-      int rr, qt;
-      if (a.fast) {
-        rr = a.fq.balq(acc[t] + carry, qt);
-      } else {
-        qt = a.fq.divfloor(acc[t] + carry, rr);
-        if (rr > (a.q >> 1)) rr -= a.q, ++qt;
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        int rr, qt;
+        if (a.fast) {
+          rr = a.fq.balq(acc[t][j] + carry[j], qt);
+        } else {
+          qt = a.fq.divfloor(acc[t][j] + carry[j], rr);
+          if (rr > (a.q >> 1)) rr -= a.q, ++qt;
+        }
+        carry[j] = qt;
+        word |= (uint32_t)(uint8_t)(int8_t)rr << (8 * j);
       }
-      carry = qt;
-      if (!cont)
-        a.W[(size_t)t * wplane + (size_t)g * a.P + s] = (int8_t)rr;
-      else if (rn >= 0)
-        a.Bg[(size_t)t * plane + (size_t)rn * a.P + s] = (int8_t)rr;
+      if (none_cont) {
+        *reinterpret_cast<uint32_t*>(a.W + (size_t)t * wplane + (size_t)g * a.P + s4) = word;
+      } else if (all_cont && same_v) {
+        if (rn[0] >= 0) *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * plane + (size_t)rn[0] * a.P + s4) = word;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (!valid[j]) continue;
+          const int8_t b = (int8_t)(word >> (8 * j));
+          if (!conts[j])
+            a.W[(size_t)t * wplane + (size_t)g * a.P + s4 + j] = b;
+          else if (rn[j] >= 0)
+            a.Bg[(size_t)t * plane + (size_t)rn[j] * a.P + s4 + j] = b;
+        }
+      }
     }
   }
 }
