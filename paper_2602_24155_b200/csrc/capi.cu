@@ -468,7 +468,7 @@ extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int3
     e.P = states;
     auto run = [&] {
       if (mode == 2)
-        tc_gemm_i8(A.p, nLp, nLp, Y.p + (size_t)3 * states, states, Ld * states, nLp, e, 0);
+        tc_gemm_i8(A.p, nLp, nLp, Y.p + (size_t)3 * nLp * states, states, states, nLp, e, 0);
       else
         tc_gemm_i8(A.p, nLp, nLp, IN.p, states, states, nLp, e, 0);
     };

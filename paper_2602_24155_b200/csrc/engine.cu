@@ -331,10 +331,8 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
       e.b_mn = 1;
       e.P = bcap_;
       // in_0 = bal(b_0 + 0) = b_0: digit 0 reads the gathered plane directly
-      // (Bg rows are Ld planes of P states: plane 0 is a view with pitch Ld P)
       const int8_t* in = k ? IN_.p : Bg_.p;
-      const int pitch = k ? bcap_ : T.dp.Ld * bcap_;
-      timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, in, nb, pitch, nLp_, e, st_); });
+      timed(&clock.gemm_ms, [&] { tc_gemm_i8(C_.p, nLp_, nLp_, in, nb, bcap_, nLp_, e, st_); });
       ++clock.gemm_launches;
       clock.gemm_macs += (double)T.nL * T.nL * nb;
       if (k + 1 < T.dp.Ld) {
@@ -345,7 +343,7 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
         e.Cy = Cy_.p;
         e.IN = IN_.p;
         timed(&clock.carry_ms, [&] {
-          tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * bcap_, nb, T.dp.Ld * bcap_, nLp_, e, st_);
+          tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
         });
         ++clock.carry_launches;
         clock.carry_macs += (double)T.nL * T.nL * nb;

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) gather_kernel(StepArgs a) {
       if (rr >= a.nL) continue;
       uint32_t word = *reinterpret_cast<const uint32_t*>(&tile[row][w * 4]);
       size_t off = (size_t)rr * a.P + s0 + w * 4;
-      *reinterpret_cast<uint32_t*>(a.Bg + ((size_t)rr * a.Ld + t) * a.P + s0 + w * 4) = word;
+      *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * a.nLp * a.P + off) = word;
       if (t == 0) {
         uint32_t inw = 0;
 #pragma unroll
@@ -86,8 +86,8 @@ __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
       int rr = l >> 6, cc = l & 63;
       Cs[rr][cc] = a.C[(size_t)(r0 + rr) * a.nLp + j0 + cc];
       // digit 0 reads b_0 itself (balanced digits, c_0 = 0)
-      const int8_t* src = k ? a.IN + (size_t)(j0 + rr) * a.P : a.Bg + (size_t)(j0 + rr) * a.Ld * a.P;
-      Is[rr][cc] = s0 + cc < a.P ? src[s0 + cc] : (int8_t)0;
+      const int8_t* src = k ? a.IN : a.Bg;
+      Is[rr][cc] = s0 + cc < a.P ? src[(size_t)(j0 + rr) * a.P + s0 + cc] : (int8_t)0;
     }
     __syncthreads();
     for (int j = 0; j < 64; ++j) {
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
       int s = s0 + tx * 4 + jj;
-      if (s < a.B) a.Y[((size_t)r * a.Ld + k) * a.P + s] = (int8_t)a.fq.bal(acc[i][jj]);
+      if (s < a.B) a.Y[((size_t)k * a.nLp + r) * a.P + s] = (int8_t)a.fq.bal(acc[i][jj]);
     }
   }
 }
@@ -119,15 +119,37 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
   if (s >= a.B || r >= a.nL) return;
+  const int8_t* y = a.Y + (size_t)k * a.nLp * a.P;
   int sum = 0;
-  for (int e = a.jp_ptr[r]; e < a.jp_ptr[r + 1]; ++e)
-    sum += a.jp_val[e] * (int)a.Y[((size_t)a.jp_col[e] * a.Ld + k) * a.P + s];
+  for (int e = a.jp_ptr[r]; e < a.jp_ptr[r + 1]; ++e) sum += a.jp_val[e] * (int)y[(size_t)a.jp_col[e] * a.P + s];
   size_t off = (size_t)r * a.P + s;
   int rem;
-  const size_t boff = ((size_t)r * a.Ld + k) * a.P + s;
-  int c = a.fq.divfloor((int)a.Bg[boff] + (k ? (int)a.Cy[off] : 0) - sum, rem);
+  int c = a.fq.divfloor((int)a.Bg[(size_t)k * a.nLp * a.P + off] + (k ? (int)a.Cy[off] : 0) - sum, rem);
   a.Cy[off] = (int16_t)c;
-  if (k + 1 < a.Ld) a.IN[off] = (int8_t)a.fq.bal((int)a.Bg[boff + a.P] + c);
+  if (k + 1 < a.Ld) a.IN[off] = (int8_t)a.fq.bal((int)a.Bg[(size_t)(k + 1) * a.nLp * a.P + off] + c);
+}
+
+// b = P_v W for the second and later steps of a chunk: lanes are states of
+// one (k, v)-sorted batch, so neighbouring lanes usually share v and read the
+// same W row: both sides state-contiguous
+__global__ void __launch_bounds__(256) gather_w_kernel(StepArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * 32 + lane;
+  if (s >= a.B) return;
+  const int vd = a.vdir[s];
+  const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
+  for (int r = blockIdx.y * 64 + warp; r < min(a.nL, (int)(blockIdx.y + 1) * 64); r += 8) {
+    const int g = a.gidx[(size_t)vd * a.nL + r];
+    const size_t off = (size_t)r * a.P + s;
+    int8_t b0 = 0;
+    for (int t = 0; t < a.Ld; ++t) {
+      int8_t bt = g >= 0 ? a.W[(size_t)t * wplane + (size_t)g * a.P + s] : (int8_t)0;
+      a.Bg[(size_t)t * plane + off] = bt;
+      if (t == 0) b0 = bt;
+    }
+    a.IN[off] = (int8_t)a.fq.bal(b0);
+    a.Cy[off] = 0;
+  }
 }
 
 __device__ __forceinline__ int pick6(int i, int x0, int x1, int x2, int x3, int x4, int x5) {
@@ -161,7 +183,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
   const bool same_v = vds[0] == vds[1] && vds[0] == vds[2] && vds[0] == vds[3];
   const bool all_cont = conts[0] && conts[1] && conts[2] && conts[3];
   const bool none_cont = !conts[0] && !conts[1] && !conts[2] && !conts[3] && valid[3];
-  const size_t P = (size_t)a.P;
+  const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
   for (int g = blockIdx.y * 64 + warp; g < min(a.side, (int)(blockIdx.y + 1) * 64); g += 8) {
     int acc[LD][4];
 #pragma unroll
@@ -174,11 +196,10 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
       int wg[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) wg[j] = pick6(ii, xs[j][0], xs[j][1], xs[j][2], xs[j][3], xs[j][4], xs[j][5]) + mu;
-      // row-major digit planes: the LD words of row r are P bytes apart
-      const int8_t* yr = a.Y + (size_t)r * LD * P + s4;
+      const uint32_t* yr = reinterpret_cast<const uint32_t*>(a.Y + (size_t)r * a.P + s4);
 #pragma unroll
       for (int t = 0; t < LD; ++t) {
-        const uint32_t w4 = *reinterpret_cast<const uint32_t*>(yr + (size_t)t * P);
+        const uint32_t w4 = yr[(t * plane) >> 2];
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[t][j] += wg[j] * (int)(int8_t)(w4 >> (8 * j));
       }
@@ -204,18 +225,18 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
         word |= (uint32_t)(uint8_t)(int8_t)rr << (8 * j);
       }
       if (none_cont) {
-        *reinterpret_cast<uint32_t*>(a.W + ((size_t)g * LD + t) * P + s4) = word;
+        *reinterpret_cast<uint32_t*>(a.W + (size_t)t * wplane + (size_t)g * a.P + s4) = word;
       } else if (all_cont && same_v) {
-        if (rn[0] >= 0) *reinterpret_cast<uint32_t*>(a.Bg + ((size_t)rn[0] * LD + t) * P + s4) = word;
+        if (rn[0] >= 0) *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * plane + (size_t)rn[0] * a.P + s4) = word;
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (!valid[j]) continue;
           const int8_t b = (int8_t)(word >> (8 * j));
           if (!conts[j])
-            a.W[((size_t)g * LD + t) * P + s4 + j] = b;
+            a.W[(size_t)t * wplane + (size_t)g * a.P + s4 + j] = b;
           else if (rn[j] >= 0)
-            a.Bg[((size_t)rn[j] * LD + t) * P + s4 + j] = b;
+            a.Bg[(size_t)t * plane + (size_t)rn[j] * a.P + s4 + j] = b;
         }
       }
     }
@@ -244,10 +265,11 @@ inline void launch_epilogue(const StepArgs& a, dim3 grid, cudaStream_t st) {
 __global__ void __launch_bounds__(256) flush_kernel(StepArgs a, int s_lo, int s_hi) {
   extern __shared__ int8_t ft[];  // Ld x kFlushRows x kFlushStates
   const int g0 = blockIdx.y * kFlushRows, s0 = s_lo + blockIdx.x * kFlushStates;
+  const size_t wplane = (size_t)a.sidep * a.P;
   for (int e = threadIdx.x; e < a.Ld * kFlushRows * kFlushStates; e += 256) {
     int sl = e % kFlushStates, gl = (e / kFlushStates) % kFlushRows, t = e / (kFlushStates * kFlushRows);
     int g = g0 + gl, s = s0 + sl;
-    ft[e] = (g < a.side && s < s_hi) ? a.W[((size_t)g * a.Ld + t) * a.P + s] : (int8_t)0;
+    ft[e] = (g < a.side && s < s_hi) ? a.W[(size_t)t * wplane + (size_t)g * a.P + s] : (int8_t)0;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;  // lane = state

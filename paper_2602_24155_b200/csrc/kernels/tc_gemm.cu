@@ -215,9 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const size_t P = (size_t)epi.P;
         const bool last = epi.k + 1 >= epi.Ld;
         const int cbeg = half * (BN / 2), cend = (half + 1) * (BN / 2);
-        // row-major digit planes: plane k+1 of row m follows plane k
-        const int8_t* bgk = epi.Bg + ((size_t)m * epi.Ld + epi.k) * P;
-        const int8_t* bgk1 = bgk + P;
+        const int8_t* bgk = epi.Bg + ((size_t)epi.k * epi.nLp + m) * P;
+        const int8_t* bgk1 = epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P;
         uint4 nbk = make_uint4(0, 0, 0, 0), nbk1 = nbk, nc0 = nbk, nc1 = nbk;
         auto fetch = [&](int c) {
           const int nb = n0 + c;
@@ -288,15 +287,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                       << (8 * b);
             w4[q4] = word;
           }
-          *reinterpret_cast<uint4*>(epi.Y + ((size_t)m * epi.Ld + epi.k) * epi.P + nb) =
+          *reinterpret_cast<uint4*>(epi.Y + ((size_t)epi.k * epi.nLp + m) * epi.P + nb) =
               make_uint4(w4[0], w4[1], w4[2], w4[3]);
         } else if (epi.b_mn) {
           // carry on state-contiguous rows: 16-byte vector loads and stores
           const size_t P = (size_t)epi.P;
           const bool last = epi.k + 1 >= epi.Ld;
-          uint4 bk = __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)m * epi.Ld + epi.k) * P + nb));
+          uint4 bk = __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)epi.k * epi.nLp + m) * P + nb));
           uint4 bk1 = last ? make_uint4(0, 0, 0, 0)
-                           : __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)m * epi.Ld + epi.k + 1) * P + nb));
+                           : __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P + nb));
           uint4* cyp = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
           // c_0 = 0: digit 0 ignores whatever the previous step left in Cy
           uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
@@ -380,7 +379,7 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
   DRZG_REQUIRE(lda % 16 == 0 && ldb % 16 == 0, "tc_gemm: row pitch must be a multiple of 16 bytes");
   DRZG_REQUIRE(((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0, "tc_gemm: operands must be 16-byte aligned");
   CUtensorMap ma = make_map(A, rowsA, lda, K, tc::BM);
-  CUtensorMap mb = epi.b_mn ? make_map(B, K, ldb, epi.P, tc::BK)  // K rows (pitch ldb) x P states, box 128 x 128
+  CUtensorMap mb = epi.b_mn ? make_map(B, K, ldb, ldb, tc::BK)  // K rows x ldb states, box 128 x 128
                             : make_map(B, rowsB, ldb, K, tc::BN);
   // kind::i8 instruction descriptor: D s32, A signed (Cq) or unsigned (Jp),
   // B signed, both K-major, N = BN, M = 128
