@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdrzg.so")
+LIB_PATH = os.environ.get("DRZG_LIB") or os.path.join(_HERE, "libdrzg.so")
 POLICIES = {"p-chunk": 0, "pchunk": 0, "depth-first": 1, "depth": 1, "var-by-var": 2, "varbyvar": 2}
 
 _lib = None
