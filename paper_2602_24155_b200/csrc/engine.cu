@@ -380,7 +380,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
         timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 256, 0, st_>>>(a); });
       }  // later steps: the previous epilogue already wrote this step's operand
       dixon(a);
-      dim3 gE((By + 127) / 128, (T.side + 63) / 64);
+      dim3 gE((By + 127) / 128, (T.side + dev::kEpiRows - 1) / dev::kEpiRows);
       timed(&clock.epi_ms, [&] { dev::launch_epilogue(a, gE, st_); });
       mv += By;
       const int Bn = count_ge(y + 1);

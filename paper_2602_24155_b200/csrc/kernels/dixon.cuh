@@ -156,74 +156,84 @@ __device__ __forceinline__ int pick6(int i, int x0, int x1, int x2, int x3, int 
   return i == 0 ? x0 : i == 1 ? x1 : i == 2 ? x2 : i == 3 ? x3 : i == 4 ? x4 : x5;
 }
 
-// w' = T_x y into W (Ld x sidep x P), carry-normalised digits.  Each lane
-// owns 4 consecutive states so every global access is a 32-bit word (four
-// states of one digit plane); LD = digit planes at compile time so the
-// accumulators live in registers.
+// w' = T_x y into W (Ld x sidep x P) or the next step's gathered operand Bg,
+// carry-normalised digits.  A block owns 128 states (each lane 4 consecutive
+// states, so every global access is a 32-bit word of one digit plane) and
+// kEpiRows side rows, 8 per warp.  The per-state data (x = u - y v, the
+// direction, whether the state continues) and the block's T_x terms
+// (solution index r, variable i, mu) are staged in shared memory once, so the
+// only global loads left on a row's critical path are the Y digit words —
+// issued all at once (LD independent loads per term).  Rows fed by one or two
+// terms (nearly all of them: T_x is close to a permutation) run with the
+// digits in registers and a plane-sequential carry; other rows take a plane
+// loop.  Low register use keeps 4 blocks (32 warps) resident per SM.
+constexpr int kEpiRows = 64, kEpiTermCap = 512;
+
 template <int LD>
-__global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s4 = (blockIdx.x * 32 + lane) * 4;  // first of this lane's 4 states
+__device__ __forceinline__ void epi_load(const int8_t* __restrict__ Y, size_t plane, size_t off, uint32_t (&w)[LD]) {
+  const uint32_t* yr = reinterpret_cast<const uint32_t*>(Y + off);
+#pragma unroll
+  for (int t = 0; t < LD; ++t) w[t] = __ldg(yr + ((t * plane) >> 2));
+}
+
+template <int LD>
+__global__ void __launch_bounds__(256, 3) epilogue_kernel(StepArgs a) {
+  __shared__ int xs_s[6][128];
+  __shared__ int vd_s[128];
+  __shared__ int ct_s[128];  // bit 0 valid, bit 1 continues
+  __shared__ int tp_s[kEpiRows + 1];
+  __shared__ int2 tm_s[kEpiTermCap];  // {r, i | mu << 8}
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int sb = blockIdx.x * 128;
+  const int g0 = blockIdx.y * kEpiRows, g1 = min(a.side, g0 + kEpiRows);
+  if (tid < 128) {
+    const int s = sb + tid;
+    const bool valid = s < a.B;
+    const int sv = valid ? s : sb;
+    const int vd = a.vdir[sv];
+    vd_s[tid] = vd;
+    ct_s[tid] = (valid ? 1 : 0) | ((valid && a.y < a.ks[sv]) ? 2 : 0);
+    for (int i = 0; i < a.nv; ++i) xs_s[i][tid] = a.u0[(size_t)sv * a.nv + i] - a.y * a.dirs[(size_t)vd * a.nv + i];
+  }
+  for (int j = tid; j <= g1 - g0; j += 256) tp_s[j] = a.t_ptr[g0 + j];
+  __syncthreads();
+  const int e0 = tp_s[0], ne = tp_s[g1 - g0] - e0;
+  const bool staged = ne <= kEpiTermCap;
+  if (staged)
+    for (int j = tid; j < ne; j += 256) {
+      const int r = a.t_src[e0 + j];
+      tm_s[j] = make_int2(r, a.sol_i[r] | (a.sol_mu[r] << 8));
+    }
+  __syncthreads();
+  const int s4 = sb + lane * 4;
   if (s4 >= a.B) return;
-  int xs[4][6];
   int vds[4];
   bool conts[4], valid[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const int s = s4 + j;
-    valid[j] = s < a.B;
-    const int sv = valid[j] ? s : s4;
-    vds[j] = a.vdir[sv];
-    conts[j] = valid[j] && a.y < a.ks[sv];
-    const int* v = a.dirs + (size_t)vds[j] * a.nv;
-    const int* u = a.u0 + (size_t)sv * a.nv;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) xs[j][i] = i < a.nv ? u[i] - a.y * v[i] : 0;
+    vds[j] = vd_s[lane * 4 + j];
+    valid[j] = ct_s[lane * 4 + j] & 1;
+    conts[j] = ct_s[lane * 4 + j] & 2;
   }
   const bool same_v = vds[0] == vds[1] && vds[0] == vds[2] && vds[0] == vds[3];
   const bool all_cont = conts[0] && conts[1] && conts[2] && conts[3];
   const bool none_cont = !conts[0] && !conts[1] && !conts[2] && !conts[3] && valid[3];
   const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
-  for (int g = blockIdx.y * 64 + warp; g < min(a.side, (int)(blockIdx.y + 1) * 64); g += 8) {
-    int acc[LD][4];
+  auto term = [&](int e) {
+    return staged ? tm_s[e - e0] : make_int2(a.t_src[e], a.sol_i[a.t_src[e]] | (a.sol_mu[a.t_src[e]] << 8));
+  };
+  auto weights = [&](int2 tm, int (&wg)[4]) {
+    const int ii = tm.y & 0xFF, mu = tm.y >> 8;
 #pragma unroll
-    for (int t = 0; t < LD; ++t)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[t][j] = 0;
-    for (int e = a.t_ptr[g]; e < a.t_ptr[g + 1]; ++e) {
-      const int r = a.t_src[e];
-      const int ii = a.sol_i[r], mu = a.sol_mu[r];
-      int wg[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) wg[j] = pick6(ii, xs[j][0], xs[j][1], xs[j][2], xs[j][3], xs[j][4], xs[j][5]) + mu;
-      const uint32_t* yr = reinterpret_cast<const uint32_t*>(a.Y + (size_t)r * a.P + s4);
-#pragma unroll
-      for (int t = 0; t < LD; ++t) {
-        const uint32_t w4 = yr[(t * plane) >> 2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[t][j] += wg[j] * (int)(int8_t)(w4 >> (8 * j));
-      }
-    }
+    for (int j = 0; j < 4; ++j) wg[j] = xs_s[ii][lane * 4 + j] + mu;
+  };
+  for (int g = g0 + warp; g < g1; g += 8) {
+    const int eb = tp_s[g - g0], nt = tp_s[g - g0 + 1] - eb;
     // next step's operand row of side row g (per state's v), or W at chunk end
     int rn[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? a.ginv[(size_t)vds[j] * a.side + g] : -1;
-    int carry[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < LD; ++t) {
-      uint32_t word = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        int rr, qt;
-        if (a.fast) {
-          rr = a.fq.balq(acc[t][j] + carry[j], qt);
-        } else {
-          qt = a.fq.divfloor(acc[t][j] + carry[j], rr);
-          if (rr > (a.q >> 1)) rr -= a.q, ++qt;
-        }
-        carry[j] = qt;
-        word |= (uint32_t)(uint8_t)(int8_t)rr << (8 * j);
-      }
+    for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? __ldg(a.ginv + (size_t)vds[j] * a.side + g) : -1;
+    auto put = [&](int t, uint32_t word) {
       if (none_cont) {
         *reinterpret_cast<uint32_t*>(a.W + (size_t)t * wplane + (size_t)g * a.P + s4) = word;
       } else if (all_cont && same_v) {
@@ -238,6 +248,59 @@ __global__ void __launch_bounds__(256) epilogue_kernel(StepArgs a) {
           else if (rn[j] >= 0)
             a.Bg[(size_t)t * plane + (size_t)rn[j] * a.P + s4 + j] = b;
         }
+      }
+    };
+    auto digit = [&](int acc, int& carry) {
+      int rr, qt;
+      if (a.fast) {
+        rr = a.fq.balq(acc + carry, qt);
+      } else {
+        qt = a.fq.divfloor(acc + carry, rr);
+        if (rr > (a.q >> 1)) rr -= a.q, ++qt;
+      }
+      carry = qt;
+      return (uint32_t)(uint8_t)(int8_t)rr;
+    };
+    int carry[4] = {0, 0, 0, 0};
+    if (nt == 1 || nt == 2) {
+      int wg0[4], wg1[4] = {0, 0, 0, 0};
+      uint32_t w0[LD], w1[LD];
+      const int2 t0 = term(eb);
+      weights(t0, wg0);
+      epi_load<LD>(a.Y, plane, (size_t)t0.x * a.P + s4, w0);
+      if (nt == 2) {
+        const int2 t1 = term(eb + 1);
+        weights(t1, wg1);
+        epi_load<LD>(a.Y, plane, (size_t)t1.x * a.P + s4, w1);
+      } else {
+#pragma unroll
+        for (int t = 0; t < LD; ++t) w1[t] = 0;
+      }
+#pragma unroll
+      for (int t = 0; t < LD; ++t) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          word |= digit(wg0[j] * (int)(int8_t)(w0[t] >> (8 * j)) + wg1[j] * (int)(int8_t)(w1[t] >> (8 * j)),
+                        carry[j])
+                  << (8 * j);
+        put(t, word);
+      }
+    } else {
+      for (int t = 0; t < LD; ++t) {
+        int acc[4] = {0, 0, 0, 0};
+        for (int e = eb; e < eb + nt; ++e) {
+          const int2 tm = term(e);
+          int wg[4];
+          weights(tm, wg);
+          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a.Y + (size_t)t * plane + (size_t)tm.x * a.P + s4));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[j] += wg[j] * (int)(int8_t)(w >> (8 * j));
+        }
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) word |= digit(acc[j], carry[j]) << (8 * j);
+        put(t, word);
       }
     }
   }

@@ -205,10 +205,24 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
       const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
       const int acc = i & 1;
-      mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
       const int m = m0 + quarter * 32 + lane;
       const bool mok = m < epi.M;
+      if (epi.b_mn && epi.mode == (int)TcEpilogue::carry && mok && n0 + half * (BN / 2) < epi.N) {
+        // the carry inputs do not depend on the accumulator: pull this
+        // thread's row segments into L2 while the mainloop runs
+        const size_t P = (size_t)epi.P;
+        const size_t nb = (size_t)(n0 + half * (BN / 2));
+        const int8_t* bgk = epi.Bg + ((size_t)epi.k * epi.nLp + m) * P + nb;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(bgk));
+        if (epi.k + 1 < epi.Ld) asm volatile("prefetch.global.L2 [%0];" ::"l"(bgk + (size_t)epi.nLp * P));
+        if (epi.k) {
+          const int16_t* cy = epi.Cy + (size_t)m * P + nb;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cy));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(cy + 64));
+        }
+      }
+      mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
       if (epi.b_mn && epi.mode == (int)TcEpilogue::carry) {
         // carry on state-contiguous rows, software-pipelined: the 16-byte
         // loads of chunk c+16 are in flight while chunk c is computed
