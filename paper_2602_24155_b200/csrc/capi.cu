@@ -1,5 +1,6 @@
 // The C ABI (include/drzg.h): marshalling between the reference's plain
 // layouts and the engine, exceptions -> status codes + thread-local message.
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <sstream>
@@ -594,5 +595,32 @@ extern "C" int drzg_test_final_levels(uint64_t p, int32_t n, int32_t d, const ui
         for (size_t i = 0; i < a.size(); ++i) bad += a[i] != b[i];
     }
     *diff = bad;
+  });
+}
+
+// debug hook: the Dixon system's structure (Jp CSR, rows Homog_L in grevlex
+// rank, columns = solution indices) and the generator of every solution
+// index, written as int32 arrays to `path`:
+//   nL, nnz, rowptr[nL+1], col[nnz], val[nnz], sol_i[nL], sol_row[nL], sol_mu[nL]
+extern "C" int drzg_debug_system(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M,
+                                 const char* path) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    setenv("DRZG_SETUP", "host", 1);
+    setenv("DRZG_DEBUG_NO_INVERSE", "1", 1);
+    RuvTables T = build_tables(X, M, default_S(n, d));
+    unsetenv("DRZG_SETUP");
+    unsetenv("DRZG_DEBUG_NO_INVERSE");
+    FILE* f = std::fopen(path, "wb");
+    DRZG_REQUIRE(f != nullptr, "debug_system: cannot open output");
+    int32_t hdr[2] = {T.nL, (int32_t)T.sys.col.size()};
+    std::fwrite(hdr, 4, 2, f);
+    std::fwrite(T.sys.rowptr.data(), 4, T.sys.rowptr.size(), f);
+    std::fwrite(T.sys.col.data(), 4, T.sys.col.size(), f);
+    std::fwrite(T.sys.val.data(), 4, T.sys.val.size(), f);
+    std::fwrite(T.sol_i.data(), 4, T.sol_i.size(), f);
+    std::fwrite(T.sol_row.data(), 4, T.sol_row.size(), f);
+    std::fwrite(T.sol_mu.data(), 4, T.sol_mu.size(), f);
+    std::fclose(f);
   });
 }

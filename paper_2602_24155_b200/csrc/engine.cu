@@ -59,7 +59,9 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     i64 wmax = 0;
     for (int r = 0; r < T.nL; ++r) wmax = std::max<i64>(wmax, T.sol_mu[r]);
     i64 bound = std::max<i64>((i64)nLp_ * half * half, 127 + cmax + R * half);
-    bound = std::max<i64>(bound, (i64)T.nv * (4096 + wmax) * half + 4096);
+    i64 maxnt = 0;  // solution indices feeding one side row
+    for (int g = 0; g < T.side; ++g) maxnt = std::max<i64>(maxnt, T.t_ptr[g + 1] - T.t_ptr[g]);
+    bound = std::max<i64>(bound, std::max<i64>(T.nv, maxnt) * (4096 + wmax) * half + 4096);
     fast_ = bound < ((i64)1 << 22);
     if (want_tc && maxv < 256) {
       std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);

@@ -81,6 +81,7 @@ inline DixonSystem make_dixon(const DigitPlan& dp, int rows, int cols, const std
     }
     sys.rowptr[r + 1] = (i32)sys.col.size();
   }
+  if (std::getenv("DRZG_DEBUG_NO_INVERSE")) return sys;  // structure-only debug dumps
   auto inv = use_device_setup(rows) ? inverse_mod_q_device(dp.p, (u64)dp.q, rows, sq)
                                     : inverse_mod_q(dp.p, (u64)dp.q, rows, std::move(sq));
   sys.Cq.resize(inv.size());

@@ -159,25 +159,74 @@ __device__ __forceinline__ int pick6(int i, int x0, int x1, int x2, int x3, int 
 // w' = T_x y into W (Ld x sidep x P) or the next step's gathered operand Bg,
 // carry-normalised digits.  A block owns 128 states (each lane 4 consecutive
 // states, so every global access is a 32-bit word of one digit plane) and
-// kEpiRows side rows, 8 per warp.  The per-state data (x = u - y v, the
-// direction, whether the state continues) and the block's T_x terms
-// (solution index r, variable i, mu) are staged in shared memory once, so the
-// only global loads left on a row's critical path are the Y digit words —
-// issued all at once (LD independent loads per term).  Rows fed by one or two
-// terms (nearly all of them: T_x is close to a permutation) run with the
-// digits in registers and a plane-sequential carry; other rows take a plane
-// loop.  Low register use keeps 4 blocks (32 warps) resident per SM.
-constexpr int kEpiRows = 64, kEpiTermCap = 512;
+// kEpiRows side rows, one warp per row at a time.  The per-state data (x =
+// u - y v, the direction, whether the state continues) and the block's T_x
+// terms are staged in shared memory once.  A side row is fed by NT solution
+// indices (0..5 for every shape in BASELINE.json; 1742 of the fourfold's 3003
+// rows by none): rows are dispatched to a body specialised on NT, whose term
+// weights (x_i + mu_i per state) live in registers across the digit loop, so
+// the work per digit and state is NT byte-extract + multiply-adds and one
+// balanced division by q (multiply-high, bias folded into the running carry).
+constexpr int kEpiRows = 64, kEpiTermCap = 512, kEpiMaxNT = 6;
 
-template <int LD>
-__device__ __forceinline__ void epi_load(const int8_t* __restrict__ Y, size_t plane, size_t off, uint32_t (&w)[LD]) {
-  const uint32_t* yr = reinterpret_cast<const uint32_t*>(Y + off);
+// sign-extended byte j of w (one PRMT)
+// (PTX prmt default mode: a selector nibble with bit 3 set replicates the
+// sign of the selected byte; the __byte_perm intrinsic does not promise that)
+__device__ __forceinline__ int sbyte(uint32_t w, int j) {
+  const unsigned sel = (unsigned)(j | ((8 | j) << 4) | ((8 | j) << 8) | ((8 | j) << 12));
+  unsigned r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
+  return (int)r;
+}
+
+struct EpiCtx {
+  const int8_t* Y;
+  int8_t* W;
+  int8_t* Bg;
+  size_t plane, wplane, P;
+  int s4;
+  // division by q: xp = acc + tqb, tq = umulhi(xp, m32), digit = xp - q tq - h,
+  // next tqb = tq + bias (bias = h + (q - 1) K folds the offset K = k22)
+  unsigned m32;
+  int q, h, bias, tq0;
+};
+
+template <int LD, int NT>
+__device__ __forceinline__ void epi_row(const EpiCtx& c, const long long (&roff)[kEpiMaxNT], const int (&wg)[kEpiMaxNT][4],
+                                        uint32_t (&out)[LD]) {
+  int tqb[4];
 #pragma unroll
-  for (int t = 0; t < LD; ++t) w[t] = __ldg(yr + ((t * plane) >> 2));
+  for (int j = 0; j < 4; ++j) tqb[j] = c.tq0;
+  uint32_t nxt[NT > 0 ? NT : 1];
+#pragma unroll
+  for (int e = 0; e < NT; ++e) nxt[e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + roff[e]));
+#pragma unroll
+  for (int t = 0; t < LD; ++t) {
+    uint32_t cur[NT > 0 ? NT : 1];
+#pragma unroll
+    for (int e = 0; e < NT; ++e) cur[e] = nxt[e];
+    if (t + 1 < LD) {
+#pragma unroll
+      for (int e = 0; e < NT; ++e)
+        nxt[e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + (size_t)(t + 1) * c.plane + roff[e]));
+    }
+    int dg[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int xp = tqb[j];
+#pragma unroll
+      for (int e = 0; e < NT; ++e) xp += wg[e][j] * sbyte(cur[e], j);
+      const int tq = (int)__umulhi((unsigned)xp, c.m32);
+      dg[j] = xp - tq * c.q - c.h;
+      tqb[j] = tq + c.bias;
+    }
+    out[t] = __byte_perm(__byte_perm((uint32_t)dg[0], (uint32_t)dg[1], 0x0040),
+                         __byte_perm((uint32_t)dg[2], (uint32_t)dg[3], 0x0040), 0x5410);
+  }
 }
 
 template <int LD>
-__global__ void __launch_bounds__(256, 3) epilogue_kernel(StepArgs a) {
+__global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
   __shared__ int xs_s[6][128];
   __shared__ int vd_s[128];
   __shared__ int ct_s[128];  // bit 0 valid, bit 1 continues
@@ -185,7 +234,8 @@ __global__ void __launch_bounds__(256, 3) epilogue_kernel(StepArgs a) {
   __shared__ int2 tm_s[kEpiTermCap];  // {r, i | mu << 8}
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int sb = blockIdx.x * 128;
-  const int g0 = blockIdx.y * kEpiRows, g1 = min(a.side, g0 + kEpiRows);
+  const int side = a.side;
+  const int g0 = blockIdx.y * kEpiRows, g1 = min(side, g0 + kEpiRows);
   if (tid < 128) {
     const int s = sb + tid;
     const bool valid = s < a.B;
@@ -218,94 +268,102 @@ __global__ void __launch_bounds__(256, 3) epilogue_kernel(StepArgs a) {
   const bool same_v = vds[0] == vds[1] && vds[0] == vds[2] && vds[0] == vds[3];
   const bool all_cont = conts[0] && conts[1] && conts[2] && conts[3];
   const bool none_cont = !conts[0] && !conts[1] && !conts[2] && !conts[3] && valid[3];
-  const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
-  auto term = [&](int e) {
-    return staged ? tm_s[e - e0] : make_int2(a.t_src[e], a.sol_i[a.t_src[e]] | (a.sol_mu[a.t_src[e]] << 8));
-  };
-  auto weights = [&](int2 tm, int (&wg)[4]) {
-    const int ii = tm.y & 0xFF, mu = tm.y >> 8;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) wg[j] = xs_s[ii][lane * 4 + j] + mu;
-  };
+  EpiCtx c;
+  c.Y = a.Y;
+  c.W = a.W;
+  c.Bg = a.Bg;
+  c.P = (size_t)a.P;
+  c.plane = (size_t)a.nLp * c.P;
+  c.wplane = (size_t)a.sidep * c.P;
+  c.s4 = s4;
+  c.q = a.q;
+  c.h = a.q >> 1;
+  c.m32 = a.fq.m32;
+  c.bias = c.h + (a.q - 1) * a.fq.k22;
+  c.tq0 = c.h + a.q * a.fq.k22;
+  const int* ginv = a.ginv;
   for (int g = g0 + warp; g < g1; g += 8) {
     const int eb = tp_s[g - g0], nt = tp_s[g - g0 + 1] - eb;
     // next step's operand row of side row g (per state's v), or W at chunk end
     int rn[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? __ldg(a.ginv + (size_t)vds[j] * a.side + g) : -1;
+    for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? __ldg(ginv + (size_t)vds[j] * side + g) : -1;
     auto put = [&](int t, uint32_t word) {
       if (none_cont) {
-        *reinterpret_cast<uint32_t*>(a.W + (size_t)t * wplane + (size_t)g * a.P + s4) = word;
+        *reinterpret_cast<uint32_t*>(c.W + (size_t)t * c.wplane + (size_t)g * c.P + s4) = word;
       } else if (all_cont && same_v) {
-        if (rn[0] >= 0) *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * plane + (size_t)rn[0] * a.P + s4) = word;
+        if (rn[0] >= 0) *reinterpret_cast<uint32_t*>(c.Bg + (size_t)t * c.plane + (size_t)rn[0] * c.P + s4) = word;
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           if (!valid[j]) continue;
           const int8_t b = (int8_t)(word >> (8 * j));
           if (!conts[j])
-            a.W[(size_t)t * wplane + (size_t)g * a.P + s4 + j] = b;
+            c.W[(size_t)t * c.wplane + (size_t)g * c.P + s4 + j] = b;
           else if (rn[j] >= 0)
-            a.Bg[(size_t)t * plane + (size_t)rn[j] * a.P + s4 + j] = b;
+            c.Bg[(size_t)t * c.plane + (size_t)rn[j] * c.P + s4 + j] = b;
         }
       }
     };
-    auto digit = [&](int acc, int& carry) {
-      int rr, qt;
-      if (a.fast) {
-        rr = a.fq.balq(acc + carry, qt);
-      } else {
-        qt = a.fq.divfloor(acc + carry, rr);
-        if (rr > (a.q >> 1)) rr -= a.q, ++qt;
-      }
-      carry = qt;
-      return (uint32_t)(uint8_t)(int8_t)rr;
-    };
-    int carry[4] = {0, 0, 0, 0};
-    if (nt == 1 || nt == 2) {
-      int wg0[4], wg1[4] = {0, 0, 0, 0};
-      uint32_t w0[LD], w1[LD];
-      const int2 t0 = term(eb);
-      weights(t0, wg0);
-      epi_load<LD>(a.Y, plane, (size_t)t0.x * a.P + s4, w0);
-      if (nt == 2) {
-        const int2 t1 = term(eb + 1);
-        weights(t1, wg1);
-        epi_load<LD>(a.Y, plane, (size_t)t1.x * a.P + s4, w1);
-      } else {
+    if (a.fast && nt <= kEpiMaxNT) {
+      long long roff[kEpiMaxNT] = {0, 0, 0, 0, 0, 0};
+      int wg[kEpiMaxNT][4];
 #pragma unroll
-        for (int t = 0; t < LD; ++t) w1[t] = 0;
+      for (int e = 0; e < kEpiMaxNT; ++e) {
+        if (e >= nt) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) wg[e][j] = 0;
+          continue;
+        }
+        const int2 tm = staged ? tm_s[eb + e - e0]
+                               : make_int2(a.t_src[eb + e], a.sol_i[a.t_src[eb + e]] | (a.sol_mu[a.t_src[eb + e]] << 8));
+        const int ii = tm.y & 0xFF, mu = tm.y >> 8;
+        roff[e] = (long long)tm.x * a.P + s4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wg[e][j] = xs_s[ii][lane * 4 + j] + mu;
+      }
+      uint32_t out[LD];
+      switch (nt) {
+        case 0:
+#pragma unroll
+          for (int t = 0; t < LD; ++t) out[t] = 0;
+          break;
+        case 1: epi_row<LD, 1>(c, roff, wg, out); break;
+        case 2: epi_row<LD, 2>(c, roff, wg, out); break;
+        case 3: epi_row<LD, 3>(c, roff, wg, out); break;
+        case 4: epi_row<LD, 4>(c, roff, wg, out); break;
+        case 5: epi_row<LD, 5>(c, roff, wg, out); break;
+        default: epi_row<LD, 6>(c, roff, wg, out); break;
       }
 #pragma unroll
-      for (int t = 0; t < LD; ++t) {
-        uint32_t word = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          word |= digit(wg0[j] * (int)(int8_t)(w0[t] >> (8 * j)) + wg1[j] * (int)(int8_t)(w1[t] >> (8 * j)),
-                        carry[j])
-                  << (8 * j);
-        put(t, word);
-      }
+      for (int t = 0; t < LD; ++t) put(t, out[t]);
     } else {
+      // wide rows (none in the BASELINE shapes) or operands beyond the
+      // multiply-high range: plane loop over the terms, exact 64-bit division
+      int carry[4] = {0, 0, 0, 0};
       for (int t = 0; t < LD; ++t) {
-        int acc[4] = {0, 0, 0, 0};
+        int acc[4] = {carry[0], carry[1], carry[2], carry[3]};
         for (int e = eb; e < eb + nt; ++e) {
-          const int2 tm = term(e);
-          int wg[4];
-          weights(tm, wg);
-          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(a.Y + (size_t)t * plane + (size_t)tm.x * a.P + s4));
+          const int2 tm = staged ? tm_s[e - e0] : make_int2(a.t_src[e], a.sol_i[a.t_src[e]] | (a.sol_mu[a.t_src[e]] << 8));
+          const int ii = tm.y & 0xFF, mu = tm.y >> 8;
+          const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(c.Y + (size_t)t * c.plane + (size_t)tm.x * c.P + s4));
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[j] += wg[j] * (int)(int8_t)(w >> (8 * j));
+          for (int j = 0; j < 4; ++j) acc[j] += (xs_s[ii][lane * 4 + j] + mu) * sbyte(w, j);
         }
         uint32_t word = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) word |= digit(acc[j], carry[j]) << (8 * j);
+        for (int j = 0; j < 4; ++j) {
+          int rr;
+          int qt = a.fq.divfloor(acc[j], rr);
+          if (rr > c.h) rr -= c.q, ++qt;
+          word |= (uint32_t)(uint8_t)(int8_t)rr << (8 * j);
+          carry[j] = qt;
+        }
         put(t, word);
       }
     }
   }
 }
-
 // host dispatch over the digit-plane count
 inline void launch_epilogue(const StepArgs& a, dim3 grid, cudaStream_t st) {
   switch (a.Ld) {
