@@ -24,6 +24,94 @@ namespace {
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 }  // namespace
 
+// Block-sparse order of the Dixon system for the tensor-core carry.
+//
+// Jp's rows are Homog_L (monomial m) and its columns the solution indices r,
+// with Jp[m, r] != 0 only for m - mu_r in the support of the generator of r
+// (a quadric or cubic in every BASELINE shape): about 19 nonzeros per row of
+// 3003 for the fourfold.  Rows sorted lexicographically under a well-chosen
+// variable order, and columns by the mean position of their nonzero rows,
+// leave most 128 x 128 blocks of Jp empty (71% for the random fourfold), so
+// the carry GEMM of an M tile runs over its nonzero K blocks only.  The
+// permutation is applied to every engine table at upload (Cq rows/columns,
+// Jp, the gather tables and the T_x source indices); the reference-shaped
+// RuvTables are not touched.  Returns new position of every m and every r.
+namespace {
+struct SysOrder {
+  std::vector<int> pos_m, pos_r;
+  std::vector<int> kb_ptr, kb_idx;  // per 128-row M tile: nonzero 128-wide K blocks
+  long long blocks = 0;
+};
+
+SysOrder order_system(const RuvTables& T, bool search) {
+  const int nL = T.nL, nv = T.nv;
+  constexpr int B = 128;
+  const int nt = (nL + B - 1) / B;
+  const auto& rowp = T.sys.rowptr;
+  const auto& colv = T.sys.col;
+  auto sort_pos = [&](const std::vector<double>& key) {
+    std::vector<int> ord(nL), pos(nL);
+    for (int i = 0; i < nL; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
+    for (int i = 0; i < nL; ++i) pos[ord[i]] = i;
+    return pos;
+  };
+  auto col_pos = [&](const std::vector<int>& pm) {
+    std::vector<double> sum(nL, 0.0), cnt(nL, 0.0);
+    for (int m = 0; m < nL; ++m)
+      for (int e = rowp[m]; e < rowp[m + 1]; ++e) sum[colv[e]] += pm[m], cnt[colv[e]] += 1;
+    for (int r = 0; r < nL; ++r) sum[r] = cnt[r] > 0 ? sum[r] / cnt[r] : 1e18 + r;
+    return sort_pos(sum);
+  };
+  auto blocks_of = [&](const std::vector<int>& pm, const std::vector<int>& pr) {
+    std::vector<char> occ((size_t)nt * nt, 0);
+    long long n = 0;
+    for (int m = 0; m < nL; ++m)
+      for (int e = rowp[m]; e < rowp[m + 1]; ++e) {
+        char& o = occ[(size_t)(pm[m] / B) * nt + pr[colv[e]] / B];
+        n += !o;
+        o = 1;
+      }
+    return std::make_pair(n, occ);
+  };
+  SysOrder best;
+  best.pos_m.resize(nL);
+  best.pos_r.resize(nL);
+  for (int i = 0; i < nL; ++i) best.pos_m[i] = best.pos_r[i] = i;
+  best.blocks = blocks_of(best.pos_m, best.pos_r).first;
+  if (search) {
+    const auto& Lm = monos(nv, T.L).mons;
+    std::vector<int> vp(nv);
+    for (int i = 0; i < nv; ++i) vp[i] = i;
+    do {
+      for (int sgn = -1; sgn <= 1; sgn += 2) {
+        std::vector<double> key(nL);
+        for (int m = 0; m < nL; ++m) {
+          double k = 0;
+          for (int i = 0; i < nv; ++i) k = k * 64 + sgn * Lm[m][vp[i]];
+          key[m] = k;
+        }
+        std::vector<int> pm = sort_pos(key), pr = col_pos(pm);
+        long long nb = blocks_of(pm, pr).first;
+        if (nb < best.blocks) {
+          best.blocks = nb;
+          best.pos_m = std::move(pm);
+          best.pos_r = std::move(pr);
+        }
+      }
+    } while (std::next_permutation(vp.begin(), vp.end()));
+  }
+  auto occ = blocks_of(best.pos_m, best.pos_r).second;
+  best.kb_ptr.assign(1, 0);
+  for (int i = 0; i < nt; ++i) {
+    for (int j = 0; j < nt; ++j)
+      if (occ[(size_t)i * nt + j]) best.kb_idx.push_back(j);
+    best.kb_ptr.push_back((int)best.kb_idx.size());
+  }
+  return best;
+}
+}  // namespace
+
 ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t st)
     : T_(&T), n_(n), p_(p), st_(st) {
   DRZG_REQUIRE(T.dp.Ld <= dev::kLdMax, "engine: too many digit planes");
@@ -31,52 +119,92 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   sidep_ = round_up(T.side, 16);
   slot_stride_ = (long long)T.dp.Ld * sidep_;
   gsize_ = (int)mono_count(T.nv, T.D - 1);
-  // C padded to nLp x nLp
+  const char* g = std::getenv("DRZG_GEMM");
+  const bool want_tc = !(g && std::string(g) == "dp4a");
+  const char* so = std::getenv("DRZG_SPARSE_CARRY");
+  sparse_carry_ = want_tc && !(so && std::string(so) == "0");
+  // block-sparse order of the system (identity unless the carry uses it)
+  auto to0 = std::chrono::steady_clock::now();
+  SysOrder ord = order_system(T, sparse_carry_ && T.nL > 2 * 128);
+  if (std::getenv("DRZG_VERBOSE"))
+    std::fprintf(stderr, "[drzg] system order: %lld of %lld Jp blocks nonzero (%.3f s)\n", ord.blocks,
+                 (long long)((T.nL + 127) / 128) * ((T.nL + 127) / 128),
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - to0).count());
+  const std::vector<int>& pm = ord.pos_m;
+  const std::vector<int>& pr = ord.pos_r;
+  kblocks_ = ord.blocks;
+  // C padded to nLp x nLp: rows solution indices r, columns rows m
   std::vector<int8_t> Cp((size_t)nLp_ * nLp_, 0);
   for (int r = 0; r < T.nL; ++r)
-    for (int c = 0; c < T.nL; ++c) Cp[(size_t)r * nLp_ + c] = T.sys.Cq[(size_t)r * T.nL + c];
+    for (int c = 0; c < T.nL; ++c) Cp[(size_t)pr[r] * nLp_ + pm[c]] = T.sys.Cq[(size_t)r * T.nL + c];
   C_.upload(Cp, st_);
+  // Jp in the new order (CSR): rows m, columns r
+  std::vector<int> jptr(T.nL + 1, 0), jcol, jval;
+  {
+    std::vector<int> inv_m(T.nL);
+    for (int m = 0; m < T.nL; ++m) inv_m[pm[m]] = m;
+    for (int nm = 0; nm < T.nL; ++nm) {
+      const int m = inv_m[nm];
+      for (int e = T.sys.rowptr[m]; e < T.sys.rowptr[m + 1]; ++e) {
+        jcol.push_back(pr[T.sys.col[e]]);
+        jval.push_back(T.sys.val[e]);
+      }
+      jptr[nm + 1] = (int)jcol.size();
+    }
+  }
   // dense Jp for the tensor-core carry product (entries are exact small
   // non-negative integers; u8 operand); DRZG_GEMM=dp4a selects the CUDA-core path
   {
-    const char* g = std::getenv("DRZG_GEMM");
-    bool want_tc = !(g && std::string(g) == "dp4a");
     int maxv = 0;
-    for (int v : T.sys.val) maxv = std::max(maxv, v);
+    for (int v : jval) maxv = std::max(maxv, v);
     // |c_{k+1}| <= (127 + |c_k| + R (q-1)/2) / q  =>  |c| <= (127 + R (q-1)/2) / (q-1)
     i64 R = 0;
     for (int r = 0; r < T.nL; ++r) {
       i64 rs = 0;
-      for (int e2 = T.sys.rowptr[r]; e2 < T.sys.rowptr[r + 1]; ++e2) rs += std::abs(T.sys.val[e2]);
+      for (int e2 = jptr[r]; e2 < jptr[r + 1]; ++e2) rs += std::abs(jval[e2]);
       R = std::max(R, rs);
     }
     i64 cmax = (127 + R * (T.dp.q - 1) / 2) / (T.dp.q - 1) + 1;
     DRZG_REQUIRE(cmax < 32767, "engine: Dixon carries exceed int16");
     // multiply-high epilogues are exact when every operand is < 2^22:
     // digit GEMM |acc| <= nLp (q/2)^2, carry numerators <= 127 + cmax + R q/2,
-    // T epilogue <= nv (max weight) (q/2) + carry
+    // T epilogue <= (terms per side row) (max weight) (q/2) + carry
     const i64 half = T.dp.q / 2;
     i64 wmax = 0;
     for (int r = 0; r < T.nL; ++r) wmax = std::max<i64>(wmax, T.sol_mu[r]);
     i64 bound = std::max<i64>((i64)nLp_ * half * half, 127 + cmax + R * half);
     i64 maxnt = 0;  // solution indices feeding one side row
-    for (int g = 0; g < T.side; ++g) maxnt = std::max<i64>(maxnt, T.t_ptr[g + 1] - T.t_ptr[g]);
+    for (int g2 = 0; g2 < T.side; ++g2) maxnt = std::max<i64>(maxnt, T.t_ptr[g2 + 1] - T.t_ptr[g2]);
     bound = std::max<i64>(bound, std::max<i64>(T.nv, maxnt) * (4096 + wmax) * half + 4096);
     fast_ = bound < ((i64)1 << 22);
     if (want_tc && maxv < 256) {
       std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);
       for (int r = 0; r < T.nL; ++r)
-        for (int e = T.sys.rowptr[r]; e < T.sys.rowptr[r + 1]; ++e)
-          Jd[(size_t)r * nLp_ + T.sys.col[e]] = (int8_t)(uint8_t)T.sys.val[e];
+        for (int e = jptr[r]; e < jptr[r + 1]; ++e) Jd[(size_t)r * nLp_ + jcol[e]] = (int8_t)(uint8_t)jval[e];
       Jd_.upload(Jd, st_);
       use_tc_ = true;
     }
   }
-  jp_ptr_.upload(T.sys.rowptr, st_);
-  jp_col_.upload(T.sys.col, st_);
-  jp_val_.upload(T.sys.val, st_);
-  gidx_.upload(T.gidx, st_);
-  ginv_.upload(T.ginv, st_);
+  sparse_carry_ = sparse_carry_ && use_tc_;
+  if (sparse_carry_) {
+    kb_ptr_.upload(ord.kb_ptr, st_);
+    kb_idx_.upload(ord.kb_idx, st_);
+  }
+  jp_ptr_.upload(jptr, st_);
+  jp_col_.upload(jcol, st_);
+  jp_val_.upload(jval, st_);
+  {
+    std::vector<int> gi(T.gidx.size()), gv(T.ginv.size());
+    for (int vi = 0; vi < T.ndir; ++vi) {
+      for (int m = 0; m < T.nL; ++m) gi[(size_t)vi * T.nL + pm[m]] = T.gidx[(size_t)vi * T.nL + m];
+      for (int g2 = 0; g2 < T.side; ++g2) {
+        const int m = T.ginv[(size_t)vi * T.side + g2];
+        gv[(size_t)vi * T.side + g2] = m >= 0 ? pm[m] : -1;
+      }
+    }
+    gidx_.upload(gi, st_);
+    ginv_.upload(gv, st_);
+  }
   const auto& dl = monos(T.nv, T.d).mons;
   std::vector<int> dirs;
   for (const auto& v : dl) {
@@ -85,9 +213,17 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   }
   dirs_.upload(dirs, st_);
   t_ptr_.upload(T.t_ptr, st_);
-  t_src_.upload(T.t_src, st_);
-  sol_i_.upload(T.sol_i, st_);
-  sol_mu_.upload(T.sol_mu, st_);
+  {
+    std::vector<int> ts(T.t_src.size()), si(T.nL), smu(T.nL);
+    for (size_t e = 0; e < T.t_src.size(); ++e) ts[e] = pr[T.t_src[e]];
+    for (int r = 0; r < T.nL; ++r) {
+      si[pr[r]] = T.sol_i[r];
+      smu[pr[r]] = T.sol_mu[r];
+    }
+    t_src_.upload(ts, st_);
+    sol_i_.upload(si, st_);
+    sol_mu_.upload(smu, st_);
+  }
   std::vector<int> mon;
   for (const auto& e : monos(T.nv, T.D).mons)
     for (int i = 0; i < T.nv; ++i) mon.push_back(e[i]);
@@ -344,11 +480,15 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
         e.Bg = Bg_.p;
         e.Cy = Cy_.p;
         e.IN = IN_.p;
+        if (sparse_carry_) {
+          e.kb_ptr = kb_ptr_.p;
+          e.kb_idx = kb_idx_.p;
+        }
         timed(&clock.carry_ms, [&] {
           tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
         });
         ++clock.carry_launches;
-        clock.carry_macs += (double)T.nL * T.nL * nb;
+        clock.carry_macs += sparse_carry_ ? (double)kblocks_ * 128 * 128 * nb : (double)T.nL * T.nL * nb;
       }
     } else {
       timed(&clock.gemm_ms, [&] { dev::dixon_gemm_kernel<<<gG, 256, 0, st_>>>(a, k); });

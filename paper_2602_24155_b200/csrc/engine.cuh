@@ -187,6 +187,9 @@ class ReductionEngine {
   DevBuf<int8_t> Jd_;   // Jp dense (u8), nLp x nLp, for the tensor-core carry
   bool use_tc_ = false; // tcgen05 GEMMs (else the dp4a CUDA-core kernels)
   bool fast_ = false;   // fp32-reciprocal residues (host-checked operand bound)
+  bool sparse_carry_ = false;  // carry GEMM over the nonzero K blocks of Jp only
+  long long kblocks_ = 0;      // nonzero 128 x 128 blocks of Jp (system order)
+  DevBuf<int> kb_ptr_, kb_idx_;
   DevBuf<int> ginv_;
   DevBuf<int> jp_ptr_, jp_col_, jp_val_, gidx_, dirs_, t_ptr_, t_src_, sol_i_, sol_mu_, mon_;
   DevBuf<unsigned long long> btab_;

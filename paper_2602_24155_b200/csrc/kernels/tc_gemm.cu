@@ -158,19 +158,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int mi = t % mt;
+        const int m0 = mi * BM, n0 = (t / mt) * BN;
+        const int kb0 = epi.kb_ptr ? __ldg(epi.kb_ptr + mi) : 0;
+        const int nkt = epi.kb_ptr ? __ldg(epi.kb_ptr + mi + 1) - kb0 : nk;
+        for (int kb = 0; kb < nkt; ++kb, ++it) {
+          const int kc = (epi.kb_ptr ? __ldg(epi.kb_idx + kb0 + kb) : kb) * BK;
           int s = it % STAGES;
           mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
           uint32_t fb = smem_u32(&full[s]);
           mbar_expect_tx(fb, A_BYTES + B_BYTES);
-          tma_load_2d(smem_u32(sA + s * A_BYTES), &tmA, fb, kb * BK, m0);
+          tma_load_2d(smem_u32(sA + s * A_BYTES), &tmA, fb, kc, m0);
           if (epi.b_mn) {
             // K x N operand: two 128-state-wide swizzle atoms per stage
-            tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, n0, kb * BK);
-            tma_load_2d(smem_u32(sB + s * B_BYTES + BN / 2 * BK), &tmB, fb, n0 + BN / 2, kb * BK);
+            tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, n0, kc);
+            tma_load_2d(smem_u32(sB + s * B_BYTES + BN / 2 * BK), &tmB, fb, n0 + BN / 2, kc);
           } else {
-            tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kb * BK, n0);
+            tma_load_2d(smem_u32(sB + s * B_BYTES), &tmB, fb, kc, n0);
           }
         }
       }
@@ -183,7 +187,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int mi = t % mt;
+        const int nkt = epi.kb_ptr ? __ldg(epi.kb_ptr + mi + 1) - __ldg(epi.kb_ptr + mi) : nk;
+        for (int kb = 0; kb < nkt; ++kb, ++it) {
           int s = it % STAGES;
           mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");

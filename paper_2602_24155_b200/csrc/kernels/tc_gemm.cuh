@@ -40,6 +40,10 @@ struct TcEpiArgs {
   const int8_t* Bg = nullptr;  // N x Ld x nLp
   int16_t* Cy = nullptr;       // (b_mn) nLp x P carries
   int8_t* IN = nullptr;        // N x nLp
+  // block-sparse A (carry): M tile i runs over K blocks kb_idx[kb_ptr[i] ..
+  // kb_ptr[i+1]) (128-wide) only; null = dense
+  const int* kb_ptr = nullptr;
+  const int* kb_idx = nullptr;
 };
 
 // host side: build tensor maps and launch; A is (rowsA x K) with row pitch
