@@ -13,7 +13,11 @@
 #include "engine.cuh"
 #include "host/flatmap.hpp"
 
+#include <condition_variable>
+#include <deque>
 #include <exception>
+#include <memory>
+#include <mutex>
 #include <thread>
 #include "kernels/dixon.cuh"
 #include "kernels/tc_gemm.cuh"
@@ -123,6 +127,8 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   const bool want_tc = !(g && std::string(g) == "dp4a");
   const char* so = std::getenv("DRZG_SPARSE_CARRY");
   sparse_carry_ = want_tc && !(so && std::string(so) == "0");
+  const char* ck = std::getenv("DRZG_CARRY");
+  carry_kernel_ = ck && std::string(ck) == "kernel";
   // block-sparse order of the system (identity unless the carry uses it)
   auto to0 = std::chrono::steady_clock::now();
   SysOrder ord = order_system(T, sparse_carry_ && T.nL > 2 * 128);
@@ -485,7 +491,10 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
           e.kb_idx = kb_idx_.p;
         }
         timed(&clock.carry_ms, [&] {
-          tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
+          if (carry_kernel_)
+            tc_carry_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, bcap_, nLp_, e, st_);
+          else
+            tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
         });
         ++clock.carry_launches;
         clock.carry_macs += sparse_carry_ ? (double)kblocks_ * 128 * 128 * nb : (double)T.nL * T.nL * nb;
@@ -538,6 +547,153 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
   return mv;
 }
 
+namespace {
+// one seed bucket (column c, pole P), grouped: group gi is a state (one key),
+// entries [eptr[gi], eptr[gi+1]) its distinct side rows with Ld carried digits
+struct PrepBucket {
+  int col = 0, pole = 0;
+  bool first = false;
+  std::vector<u64> key;
+  std::vector<int> u;  // nv per group
+  std::vector<int> eptr{0}, eg;
+  std::vector<int8_t> ed;
+  i64 combines = 0;  // seeds folded into an earlier seed of the same group
+  bool ready = false;
+};
+
+class SeedPreparer {
+ public:
+  template <class KeyFn>
+  SeedPreparer(std::vector<ColumnSeeds>& cols, const std::vector<int>& top0, KeyFn keyfn, int nv, int Ld, int q,
+               unsigned threads)
+      : nv_(nv), Ld_(Ld), q_(q) {
+    for (int c = 0; c < (int)cols.size(); ++c)
+      for (auto& kv : cols[c].by_pole) {
+        auto pb = std::make_unique<PrepBucket>();
+        pb->col = c;
+        pb->pole = kv.first;
+        pb->first = top0[c] == kv.first;
+        order_.push_back({kv.first, c, &kv.second, pb.get()});
+        index_[((u64)(u32)kv.first << 32) | (u32)c] = pb.get();
+        owned_.push_back(std::move(pb));
+      }
+    std::stable_sort(order_.begin(), order_.end(), [](const Job& a, const Job& b) {
+      return a.pole != b.pole ? a.pole > b.pole : a.col < b.col;
+    });
+    key_ = [keyfn](int c, const Expo& u) { return keyfn(c, u); };
+    for (unsigned t = 0; t < threads; ++t) workers_.emplace_back([this] { work(); });
+  }
+  ~SeedPreparer() {
+    stop_ = true;
+    for (auto& w : workers_) w.join();
+  }
+  PrepBucket& wait(int c, int P) {
+    PrepBucket* pb = index_.at(((u64)(u32)P << 32) | (u32)c);
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return pb->ready || err_; });
+    if (err_) std::rethrow_exception(err_);
+    return *pb;
+  }
+  void release(int c, int P) {
+    PrepBucket* pb = index_.at(((u64)(u32)P << 32) | (u32)c);
+    PrepBucket empty;
+    std::swap(pb->key, empty.key);
+    std::swap(pb->u, empty.u);
+    std::swap(pb->eptr, empty.eptr);
+    std::swap(pb->eg, empty.eg);
+    std::swap(pb->ed, empty.ed);
+  }
+
+ private:
+  struct Job {
+    int pole, col;
+    SeedBucket* bk;
+    PrepBucket* pb;
+  };
+  void work() {
+    for (;;) {
+      if (stop_) return;
+      const size_t j = next_.fetch_add(1);
+      if (j >= order_.size()) return;
+      try {
+        prepare(order_[j]);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!err_) err_ = std::current_exception();
+        cv_.notify_all();
+        return;
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        order_[j].pb->ready = true;
+      }
+      cv_.notify_all();
+    }
+  }
+  void prepare(const Job& jb) {
+    SeedBucket& bk = *jb.bk;
+    PrepBucket& pb = *jb.pb;
+    const int nv = nv_, Ld = Ld_, q = q_;
+    const size_t ns = bk.size();
+    std::vector<u64> kv(ns);
+    for (size_t i = 0; i < ns; ++i) {
+      Expo u(nv);
+      for (int j = 0; j < nv; ++j) u[j] = bk.u[i * nv + j];
+      kv[i] = key_(jb.col, u);
+    }
+    std::vector<int> ord(ns);
+    for (size_t i = 0; i < ns; ++i) ord[i] = (int)i;
+    if (!pb.first)
+      std::sort(ord.begin(), ord.end(), [&](int a, int b) { return kv[a] != kv[b] ? kv[a] < kv[b] : bk.g[a] < bk.g[b]; });
+    std::vector<int> acc(Ld);
+    size_t i = 0;
+    while (i < ns) {
+      size_t j = i + 1;
+      if (!pb.first)
+        while (j < ns && kv[ord[j]] == kv[ord[i]]) ++j;
+      const int s0i = ord[i];
+      pb.key.push_back(kv[s0i]);
+      for (int t = 0; t < nv; ++t) pb.u.push_back(bk.u[(size_t)s0i * nv + t]);
+      pb.combines += (i64)(j - i - 1);
+      for (size_t a = i; a < j;) {
+        size_t b2 = a + 1;
+        while (b2 < j && bk.g[ord[b2]] == bk.g[ord[a]]) ++b2;
+        std::fill(acc.begin(), acc.end(), 0);
+        for (size_t x = a; x < b2; ++x)
+          for (int t = 0; t < Ld; ++t) acc[t] += bk.dig[(size_t)ord[x] * Ld + t];
+        int carry = 0;
+        for (int t = 0; t < Ld; ++t) {
+          int v = acc[t] + carry;
+          int r = ((v % q) + q) % q;
+          if (r > q / 2) r -= q;
+          carry = (v - r) / q;
+          pb.ed.push_back((int8_t)r);
+        }
+        pb.eg.push_back(bk.g[ord[a]]);
+        a = b2;
+      }
+      pb.eptr.push_back((int)pb.eg.size());
+      i = j;
+    }
+    SeedBucket().u.swap(bk.u);  // release host memory
+    SeedBucket().g.swap(bk.g);
+    SeedBucket().dig.swap(bk.dig);
+  }
+
+  int nv_, Ld_, q_;
+  std::function<u64(int, const Expo&)> key_;
+  std::vector<Job> order_;
+  std::unordered_map<u64, PrepBucket*> index_;
+  std::vector<std::unique_ptr<PrepBucket>> owned_;
+  std::vector<std::thread> workers_;
+  std::atomic<size_t> next_{0};
+  std::atomic<bool> stop_{false};
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::exception_ptr err_;
+};
+}  // namespace
+
 void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led) {
   const RuvTables& T = *T_;
   const int nv = T.nv, Ld = T.dp.Ld, ncol = (int)cols.size();
@@ -579,6 +735,15 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     grow_pool((int)std::max<size_t>(1024, std::min<size_t>(total_seeds / 3 + 1, budget)));
   }
 
+  // DRZG_TIMELINE: device time of every sweep and the device idle time
+  // between sweeps (the host policy falling behind), summarised at the end
+  const bool timeline = std::getenv("DRZG_TIMELINE") != nullptr;
+  struct SweepMark {
+    cudaEvent_t e0, e1;
+    int pole;
+    i64 states, matvecs;
+  };
+  std::vector<SweepMark> tl;
   std::map<int, std::vector<HS>, std::greater<int>> landed;
   // per pole: key -> position in landed[pole]; a state landing on a key that
   // is already there is combined at once (the reference combines after every
@@ -593,8 +758,41 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   // ahead, a restaged buffer must not be one an earlier kernel of the same
   // sweep still reads (the stream orders copies and kernels, so reuse across
   // uses is safe; distinct buffers just avoid needless reallocations)
-  DevBuf<int> d_a, d_b, d_c, d_s2, d_p2, d_g2, d_mp, d_mm;
-  DevBuf<int8_t> d_dig, d_dig2;
+  // background preparation of every seed bucket, in consumption order
+  // (descending pole): key sort, grouping by (column, u) and by side row g,
+  // and the carried digit sums of each group's entries
+  SeedPreparer prep(cols, top0, [&](int c, const Expo& u) { return key(c, u); }, nv, Ld, T.dp.q,
+                    std::max(1u, std::min(host_threads_, 8u)));
+  // The policy (moves, landing, combines, seeds, slot bookkeeping) never
+  // needs a device result, so it runs on its own thread as far ahead as it
+  // likes and hands every sweep to this thread as a command; this thread only
+  // stages inputs and launches kernels (and is the one the CUDA launch queue
+  // throttles).  The device never waits on host bookkeeping after the first
+  // sweep unless the policy is slower than the device in total.
+  struct SweepCmd {
+    int pole = 0;
+    bool done = false;
+    std::vector<int> s_new, p_new, g_new, s_add, p_add, g_add;
+    std::vector<int8_t> d_new, d_add;
+    std::vector<int> hslot, hvdir, hu0;
+    std::vector<i64> ks;
+    i64 matvecs = 0;
+    std::vector<int> gptr, mem;  // merges
+    std::vector<int> fs, fc, fu; // floor arrivals
+  };
+  std::mutex qmu;
+  std::condition_variable qcv;
+  std::deque<std::unique_ptr<SweepCmd>> queue;
+  std::exception_ptr perr;
+  auto push = [&](std::unique_ptr<SweepCmd> c) {
+    {
+      std::lock_guard<std::mutex> lk(qmu);
+      queue.push_back(std::move(c));
+    }
+    qcv.notify_one();
+  };
+  std::thread policy([&] {
+    try {
   for (;;) {
     int P = -1;
     if (!landed.empty()) P = landed.begin()->first;
@@ -618,109 +816,47 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     // the ledger); a state already landed at P absorbs them in place; a
     // column's first sweep keeps its seeds apart, as the reference does.
     // Landed states are unique per key (combined as they land), so after
-    // this no two live states at P share a key.
+    // this no two live states at P share a key.  The grouping and digit sums
+    // of every seed bucket were prepared by the background workers; only
+    // the (u, pole) lookups against landed states and slot allocation run here.
+    auto cmd = std::make_unique<SweepCmd>();
+    cmd->pole = P;
     {
-      std::vector<int> ss, eptr{0}, eg, add_slots;
-      std::vector<int8_t> ed;
-      std::vector<int> acc(Ld);
-      const int q = T.dp.q;
+      std::vector<int>& s_new = cmd->s_new; std::vector<int>& p_new = cmd->p_new; std::vector<int>& g_new = cmd->g_new;
+      std::vector<int>& s_add = cmd->s_add; std::vector<int>& p_add = cmd->p_add; std::vector<int>& g_add = cmd->g_add;
+      std::vector<int8_t>& d_new = cmd->d_new; std::vector<int8_t>& d_add = cmd->d_add;
+      p_new.assign(1, 0);
+      p_add.assign(1, 0);
       for (int c = 0; c < ncol; ++c) {
         if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
-        SeedBucket& bk = sit[c]->second;
-        const bool first_sweep = top0[c] == P;
-        const size_t ns = bk.size();
-        std::vector<u64> kv(ns);
-        for (size_t i = 0; i < ns; ++i) {
-          Expo u(nv);
-          for (int j = 0; j < nv; ++j) u[j] = bk.u[i * nv + j];
-          kv[i] = key(c, u);
-        }
-        std::vector<int> ord(ns);
-        for (size_t i = 0; i < ns; ++i) ord[i] = (int)i;
-        if (!first_sweep)
-          std::sort(ord.begin(), ord.end(), [&](int a, int b) {
-            return kv[a] != kv[b] ? kv[a] < kv[b] : bk.g[a] < bk.g[b];
-          });
-        size_t i = 0;
-        while (i < ns) {
-          size_t j = i + 1;
-          if (!first_sweep)
-            while (j < ns && kv[ord[j]] == kv[ord[i]]) ++j;
-          const int s0i = ord[i];
-          const int fpos = first_sweep ? -1 : front_idx.find(kv[s0i]);
-          int slot;
+        PrepBucket& pb = prep.wait(c, P);
+        led.combines += pb.combines;
+        const size_t ng = pb.key.size();
+        for (size_t gi = 0; gi < ng; ++gi) {
+          const int fpos = pb.first ? -1 : front_idx.find(pb.key[gi]);
+          const int e0 = pb.eptr[gi], e1 = pb.eptr[gi + 1];
           if (fpos >= 0) {
-            slot = front[fpos].slot;
             led.combines += 1;
-            add_slots.push_back(slot);
+            s_add.push_back(front[fpos].slot);
+            g_add.insert(g_add.end(), pb.eg.begin() + e0, pb.eg.begin() + e1);
+            d_add.insert(d_add.end(), pb.ed.begin() + (size_t)e0 * Ld, pb.ed.begin() + (size_t)e1 * Ld);
+            p_add.push_back((int)g_add.size());
           } else {
             HS h;
             h.col = c;
             h.u = Expo(nv);
-            for (int t = 0; t < nv; ++t) h.u[t] = bk.u[(size_t)s0i * nv + t];
+            for (int t = 0; t < nv; ++t) h.u[t] = pb.u[gi * nv + t];
             h.pole = P;
-            h.slot = slot = alloc_slot();
+            h.slot = alloc_slot();
             front.push_back(h);
-            add_slots.push_back(-1);
+            s_new.push_back(h.slot);
+            g_new.insert(g_new.end(), pb.eg.begin() + e0, pb.eg.begin() + e1);
+            d_new.insert(d_new.end(), pb.ed.begin() + (size_t)e0 * Ld, pb.ed.begin() + (size_t)e1 * Ld);
+            p_new.push_back((int)g_new.size());
           }
-          led.combines += (i64)(j - i - 1);
-          ss.push_back(slot);
-          for (size_t a = i; a < j;) {
-            size_t b2 = a + 1;
-            while (b2 < j && bk.g[ord[b2]] == bk.g[ord[a]]) ++b2;
-            std::fill(acc.begin(), acc.end(), 0);
-            for (size_t x = a; x < b2; ++x)
-              for (int t = 0; t < Ld; ++t) acc[t] += bk.dig[(size_t)ord[x] * Ld + t];
-            int carry = 0;
-            for (int t = 0; t < Ld; ++t) {
-              int v = acc[t] + carry;
-              int r = ((v % q) + q) % q;
-              if (r > q / 2) r -= q;
-              carry = (v - r) / q;
-              ed.push_back((int8_t)r);
-            }
-            eg.push_back(bk.g[ord[a]]);
-            a = b2;
-          }
-          eptr.push_back((int)eg.size());
-          i = j;
         }
-        SeedBucket().u.swap(bk.u);  // release host memory
-        SeedBucket().g.swap(bk.g);
-        SeedBucket().dig.swap(bk.dig);
+        prep.release(c, P);
         ++sit[c];
-      }
-      if (!ss.empty()) {
-        // fresh slots are zeroed and written; absorbed groups add in place
-        for (int pass = 0; pass < 2; ++pass) {
-          std::vector<int> s2, p2{0}, g2;
-          std::vector<int8_t> d2;
-          for (size_t i = 0; i < ss.size(); ++i) {
-            if ((add_slots[i] >= 0) != (pass == 1)) continue;
-            s2.push_back(ss[i]);
-            for (int e2 = eptr[i]; e2 < eptr[i + 1]; ++e2) {
-              g2.push_back(eg[e2]);
-              d2.insert(d2.end(), ed.begin() + (size_t)e2 * Ld, ed.begin() + (size_t)(e2 + 1) * Ld);
-            }
-            p2.push_back((int)g2.size());
-          }
-          if (s2.empty()) continue;
-          (pass == 0 ? d_a : d_s2).stage(s2, stager_, st_);
-          (pass == 0 ? d_b : d_p2).stage(p2, stager_, st_);
-          (pass == 0 ? d_c : d_g2).stage(g2, stager_, st_);
-          (pass == 0 ? d_dig : d_dig2).stage(d2, stager_, st_);
-          if (pass == 0)
-            timed(&clock.other_ms, [&] {
-              dev::seed_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p,
-                                                                d_dig.p, (int)s2.size());
-            });
-          else
-            timed(&clock.other_ms, [&] {
-              dev::add_entries_kernel<<<(int)s2.size(), 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, T.dp.q,
-                                                                      d_s2.p, d_p2.p, d_g2.p, d_dig2.p,
-                                                                      (int)s2.size());
-            });
-        }
       }
     }
     auto hp1 = std::chrono::steady_clock::now();
@@ -765,8 +901,14 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
       for (size_t i = 0; i < nf; ++i) order[cnt[bucket(i)]++] = (int)i;
     }
-    std::vector<int> hslot(nf), hvdir(nf), hu0(nf * nv);
-    std::vector<i64> ks(nf);
+    std::vector<int>& hslot = cmd->hslot;
+    std::vector<int>& hvdir = cmd->hvdir;
+    std::vector<int>& hu0 = cmd->hu0;
+    std::vector<i64>& ks = cmd->ks;
+    hslot.resize(nf);
+    hvdir.resize(nf);
+    hu0.resize(nf * nv);
+    ks.resize(nf);
     for (size_t o = 0; o < nf; ++o) {
       const int i = order[o];
       hslot[o] = front[i].slot;
@@ -774,17 +916,16 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       ks[o] = kk[i];
       for (int j = 0; j < nv; ++j) hu0[o * nv + j] = front[i].u[j];
     }
-    d_slot_.stage(hslot, stager_, st_);
-    d_vdir_.stage(hvdir, stager_, st_);
-    d_u0_.stage(hu0, stager_, st_);
-    d_k_.stage(ks, stager_, st_);
     auto hp3 = std::chrono::steady_clock::now();
-    led.matvecs += run_sweep(ks);
+    for (i64 k : ks) cmd->matvecs += k;  // run_sweep: one matvec per state per step
+    led.matvecs += cmd->matvecs;
     auto hp4 = std::chrono::steady_clock::now();
     led.startups += (i64)front.size();
     // land every state at pole P - k; a state landing on a key already there
     // is combined at once (reduction.hpp:502 combines after every sweep)
-    std::vector<int> fs, fc, fu;
+    std::vector<int>& fs = cmd->fs;
+    std::vector<int>& fc = cmd->fc;
+    std::vector<int>& fu = cmd->fu;
     std::vector<std::pair<int, int>> merges;  // (dst slot, src slot)
     for (int i : order) {
       HS h = front[i];
@@ -812,7 +953,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
     if (!merges.empty()) {
       std::sort(merges.begin(), merges.end());
-      std::vector<int> gptr{0}, mem;
+      std::vector<int>& gptr = cmd->gptr;
+      std::vector<int>& mem = cmd->mem;
+      gptr.assign(1, 0);
       for (size_t a = 0; a < merges.size();) {
         size_t b2 = a;
         mem.push_back(merges[a].first);
@@ -820,13 +963,6 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         gptr.push_back((int)mem.size());
         a = b2;
       }
-      d_mp.stage(gptr, stager_, st_);
-      d_mm.stage(mem, stager_, st_);
-      const size_t ng = gptr.size() - 1;
-      dim3 gm((unsigned)((T.side + 127) / 128) * ng);
-      timed(&clock.other_ms, [&] {
-        dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_mp.p, d_mm.p);
-      });
       for (auto& m : merges) free_slot(m.second);
     }
     auto hp5 = std::chrono::steady_clock::now();
@@ -835,22 +971,137 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       host_t_[0] += sec(hp0, hp1);
       host_t_[1] += sec(hp1, hp2);
       host_t_[2] += sec(hp2, hp3);
-      host_t_[3] += sec(hp3, hp4);
+      (void)hp4;  // launch time is accounted by the launcher
       host_t_[4] += sec(hp4, hp5);
     }
-    if (!fs.empty()) {
-      d_a.stage(fs, stager_, st_);
-      d_b.stage(fc, stager_, st_);
-      d_c.stage(fu, stager_, st_);
-      dim3 gf((unsigned)((T.side + 127) / 128) * fs.size());
-      timed(&clock.other_ms, [&] {
-        dev::floor_kernel<<<gf, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, nv, d_a.p, d_b.p, d_c.p,
-                                               mon_.p, btab_.p, dG.p, gsize_, d_err.p);
-      });
-      for (int s : fs) free_slot(s);
+    for (int s : fs) free_slot(s);
+    push(std::move(cmd));
+  }
+    } catch (...) {
+      perr = std::current_exception();
+    }
+    auto fin = std::make_unique<SweepCmd>();
+    fin->done = true;
+    push(std::move(fin));
+  });
+  // launcher: stage and launch every sweep's work in policy order
+  DevBuf<int> d_a, d_b, d_c, d_s2, d_p2, d_g2, d_mp, d_mm;
+  DevBuf<int8_t> d_dig, d_dig2;
+  try {
+    for (;;) {
+      std::unique_ptr<SweepCmd> cmd;
+      {
+        std::unique_lock<std::mutex> lk(qmu);
+        qcv.wait(lk, [&] { return !queue.empty(); });
+        cmd = std::move(queue.front());
+        queue.pop_front();
+      }
+      if (cmd->done) break;
+      auto hl0 = std::chrono::steady_clock::now();
+      // fresh slots are zeroed and written; absorbed groups add in place
+      if (!cmd->s_new.empty()) {
+        d_a.stage(cmd->s_new, stager_, st_);
+        d_b.stage(cmd->p_new, stager_, st_);
+        d_c.stage(cmd->g_new, stager_, st_);
+        d_dig.stage(cmd->d_new, stager_, st_);
+        const int ns = (int)cmd->s_new.size();
+        timed(&clock.other_ms, [&] {
+          dev::seed_kernel<<<ns, 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, d_a.p, d_b.p, d_c.p, d_dig.p, ns);
+        });
+      }
+      if (!cmd->s_add.empty()) {
+        d_s2.stage(cmd->s_add, stager_, st_);
+        d_p2.stage(cmd->p_add, stager_, st_);
+        d_g2.stage(cmd->g_add, stager_, st_);
+        d_dig2.stage(cmd->d_add, stager_, st_);
+        const int ns = (int)cmd->s_add.size();
+        timed(&clock.other_ms, [&] {
+          dev::add_entries_kernel<<<ns, 128, 0, st_>>>(pool_, slot_stride_, sidep_, Ld, T.dp.q, d_s2.p, d_p2.p,
+                                                      d_g2.p, d_dig2.p, ns);
+        });
+      }
+      if (!cmd->ks.empty()) {
+        d_slot_.stage(cmd->hslot, stager_, st_);
+        d_vdir_.stage(cmd->hvdir, stager_, st_);
+        d_u0_.stage(cmd->hu0, stager_, st_);
+        d_k_.stage(cmd->ks, stager_, st_);
+        if (timeline) {
+          cudaEvent_t e0, e1;
+          DRZG_CUDA(cudaEventCreate(&e0));
+          DRZG_CUDA(cudaEventCreate(&e1));
+          DRZG_CUDA(cudaEventRecord(e0, st_));
+          run_sweep(cmd->ks);
+          DRZG_CUDA(cudaEventRecord(e1, st_));
+          tl.push_back({e0, e1, cmd->pole, (i64)cmd->ks.size(), cmd->matvecs});
+        } else {
+          run_sweep(cmd->ks);
+        }
+      }
+      if (cmd->gptr.size() > 1) {
+        d_mp.stage(cmd->gptr, stager_, st_);
+        d_mm.stage(cmd->mem, stager_, st_);
+        const size_t ng = cmd->gptr.size() - 1;
+        dim3 gm((unsigned)((T.side + 127) / 128) * ng);
+        timed(&clock.other_ms, [&] {
+          dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_mp.p, d_mm.p);
+        });
+      }
+      if (!cmd->fs.empty()) {
+        d_a.stage(cmd->fs, stager_, st_);
+        d_b.stage(cmd->fc, stager_, st_);
+        d_c.stage(cmd->fu, stager_, st_);
+        dim3 gf((unsigned)((T.side + 127) / 128) * cmd->fs.size());
+        timed(&clock.other_ms, [&] {
+          dev::floor_kernel<<<gf, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, nv, d_a.p, d_b.p, d_c.p,
+                                                 mon_.p, btab_.p, dG.p, gsize_, d_err.p);
+        });
+      }
+      host_t_[3] += std::chrono::duration<double>(std::chrono::steady_clock::now() - hl0).count();
+    }
+  } catch (...) {
+    // drain: let the policy thread finish before unwinding
+    for (;;) {
+      std::unique_lock<std::mutex> lk(qmu);
+      qcv.wait(lk, [&] { return !queue.empty(); });
+      bool d = queue.back()->done;
+      queue.clear();
+      if (d) break;
+    }
+    policy.join();
+    throw;
+  }
+  policy.join();
+  if (perr) std::rethrow_exception(perr);
+  for (int c = 0; c < ncol; ++c) led.combines += floor_arrivals[c] - (i64)floor_keys[c].size();
+  if (timeline && !tl.empty()) {
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    double busy = 0, idle = 0, lead = 0;
+    float ms = 0;
+    DRZG_CUDA(cudaEventElapsedTime(&ms, run0, tl[0].e0));
+    lead = ms;
+    std::map<int, std::pair<double, double>> by_pole;  // pole -> (busy, idle before)
+    for (size_t i = 0; i < tl.size(); ++i) {
+      DRZG_CUDA(cudaEventElapsedTime(&ms, tl[i].e0, tl[i].e1));
+      busy += ms;
+      by_pole[tl[i].pole].first += ms;
+      if (i) {
+        float g2 = 0;
+        DRZG_CUDA(cudaEventElapsedTime(&g2, tl[i - 1].e1, tl[i].e0));
+        idle += g2;
+        by_pole[tl[i].pole].second += g2;
+      }
+    }
+    std::fprintf(stderr, "[drzg] timeline: %zu sweeps, before first %.1f ms, sweeps %.1f ms, between sweeps %.1f ms\n",
+                 tl.size(), lead, busy, idle);
+    for (auto& kv : by_pole)
+      if (kv.second.first + kv.second.second > 20)
+        std::fprintf(stderr, "[drzg]   pole %d: sweep %.1f ms, gap before %.1f ms\n", kv.first, kv.second.first,
+                     kv.second.second);
+    for (auto& m : tl) {
+      cudaEventDestroy(m.e0);
+      cudaEventDestroy(m.e1);
     }
   }
-  for (int c = 0; c < ncol; ++c) led.combines += floor_arrivals[c] - (i64)floor_keys[c].size();
   if (std::getenv("DRZG_VERBOSE"))
     std::fprintf(stderr, "[drzg] host s: seeds %.3f combine %.3f moves %.3f launch %.3f land %.3f\n", host_t_[0],
                  host_t_[1], host_t_[2], host_t_[3], host_t_[4]);

@@ -52,4 +52,10 @@ struct TcEpiArgs {
 void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB, int ldb, int K,
                 const TcEpiArgs& epi, cudaStream_t st);
 
+// the Dixon carry (epi.mode == carry, MN-major B = y_k with pitch ldb = P):
+// 128 x 128 tiles, block-sparse K when epi.kb_ptr is set, cp.async-staged
+// epilogue inputs (see carry_kernel)
+void tc_carry_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int ldb, int K, const TcEpiArgs& epi,
+                 cudaStream_t st);
+
 }  // namespace drzg
