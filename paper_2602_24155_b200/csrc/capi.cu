@@ -438,18 +438,18 @@ extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int3
   return guard_int([&] {
     const int nLp = (nL + 63) / 64 * 64, Ld = 12;
     DevBuf<int8_t> A, IN, Y, Bg;
-    DevBuf<int16_t> Cy;
+    DevBuf<int8_t> H;
     A.alloc((size_t)nLp * nLp);
     IN.alloc((size_t)states * nLp);
     Y.alloc((size_t)states * Ld * nLp);
     Bg.alloc((size_t)states * Ld * nLp);
     // state-contiguous layouts, pitch = states (multiple of 64)
-    Cy.alloc((size_t)states * nLp);
+    H.alloc((size_t)states * nLp);
     DRZG_CUDA(cudaMemset(A.p, 1, A.n));
     DRZG_CUDA(cudaMemset(IN.p, 1, IN.n));
     DRZG_CUDA(cudaMemset(Y.p, 0, Y.n));
     DRZG_CUDA(cudaMemset(Bg.p, 0, Bg.n));
-    DRZG_CUDA(cudaMemset(Cy.p, 0, Cy.n * 2));
+    DRZG_CUDA(cudaMemset(H.p, 0, H.n));
     TcEpiArgs e;
     e.mode = mode;
     e.M = nL;
@@ -462,7 +462,7 @@ extern "C" int drzg_bench_tc_gemm(int32_t nL, int32_t states, int32_t mode, int3
     e.nL = nL;
     e.Y = Y.p;
     e.Bg = Bg.p;
-    e.Cy = Cy.p;
+    e.H = H.p;
     e.IN = IN.p;
     e.a_unsigned = mode == 2;
     e.b_mn = 1;

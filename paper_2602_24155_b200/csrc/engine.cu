@@ -127,8 +127,6 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   const bool want_tc = !(g && std::string(g) == "dp4a");
   const char* so = std::getenv("DRZG_SPARSE_CARRY");
   sparse_carry_ = want_tc && !(so && std::string(so) == "0");
-  const char* ck = std::getenv("DRZG_CARRY");
-  carry_kernel_ = ck && std::string(ck) == "kernel";
   // block-sparse order of the system (identity unless the carry uses it)
   auto to0 = std::chrono::steady_clock::now();
   SysOrder ord = order_system(T, sparse_carry_ && T.nL > 2 * 128);
@@ -171,7 +169,8 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
       R = std::max(R, rs);
     }
     i64 cmax = (127 + R * (T.dp.q - 1) / 2) / (T.dp.q - 1) + 1;
-    DRZG_REQUIRE(cmax < 32767, "engine: Dixon carries exceed int16");
+    // the running residual r = b + c is stored as in + q h with h in int8
+    DRZG_REQUIRE((127 + cmax + T.dp.q) / T.dp.q < 127, "engine: Dixon residual high part exceeds int8");
     // multiply-high epilogues are exact when every operand is < 2^22:
     // digit GEMM |acc| <= nLp (q/2)^2, carry numerators <= 127 + cmax + R q/2,
     // T epilogue <= (terms per side row) (max weight) (q/2) + carry
@@ -333,7 +332,7 @@ void ReductionEngine::grow_pool(int need) {
     Bg_.release();
     Y_.release();
     IN_.release();
-    Cy_.release();
+    H_.release();
     W_.release();
     bcap_ = 0;
     DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -398,17 +397,17 @@ void ReductionEngine::ensure_batch(int B) {
   int nb = (int)std::min<size_t>(lim, (size_t)round_up(B, 64));
   if (nb <= bcap_) return;
   bcap_ = nb;
-  // state-contiguous layouts with pitch bcap_: Bg/Y Ld x nLp x P, IN/Cy nLp x P
+  // state-contiguous layouts with pitch bcap_: Bg/Y Ld x nLp x P, IN/H nLp x P
   Bg_.alloc((size_t)bcap_ * Ld * nLp_);
   Y_.alloc((size_t)bcap_ * Ld * nLp_);
   IN_.alloc((size_t)bcap_ * nLp_);
-  Cy_.alloc((size_t)bcap_ * nLp_);
+  H_.alloc((size_t)bcap_ * nLp_);
   W_.alloc((size_t)bcap_ * Ld * sidep_);
   // K padding of Bg / IN / Y must read as zero
   DRZG_CUDA(cudaMemsetAsync(Bg_.p, 0, Bg_.n, st_));
   DRZG_CUDA(cudaMemsetAsync(Y_.p, 0, Y_.n, st_));
   DRZG_CUDA(cudaMemsetAsync(IN_.p, 0, IN_.n, st_));
-  DRZG_CUDA(cudaMemsetAsync(Cy_.p, 0, Cy_.n * sizeof(int16_t), st_));
+  DRZG_CUDA(cudaMemsetAsync(H_.p, 0, H_.n, st_));
 }
 
 dev::StepArgs ReductionEngine::make_args(int b0, int nb, int y) {
@@ -445,7 +444,7 @@ dev::StepArgs ReductionEngine::make_args(int b0, int nb, int y) {
   a.P = bcap_;
   a.Bg = Bg_.p;
   a.IN = IN_.p;
-  a.Cy = Cy_.p;
+  a.H = H_.p;
   a.Y = Y_.p;
   a.W = W_.p;
   return a;
@@ -484,17 +483,14 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
         e.mode = (int)TcEpilogue::carry;
         e.a_unsigned = 1;
         e.Bg = Bg_.p;
-        e.Cy = Cy_.p;
+        e.H = H_.p;
         e.IN = IN_.p;
         if (sparse_carry_) {
           e.kb_ptr = kb_ptr_.p;
           e.kb_idx = kb_idx_.p;
         }
         timed(&clock.carry_ms, [&] {
-          if (carry_kernel_)
-            tc_carry_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, bcap_, nLp_, e, st_);
-          else
-            tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
+          tc_gemm_i8(Jd_.p, nLp_, nLp_, Y_.p + (size_t)k * nLp_ * bcap_, nb, bcap_, nLp_, e, st_);
         });
         ++clock.carry_launches;
         clock.carry_macs += sparse_carry_ ? (double)kblocks_ * 128 * 128 * nb : (double)T.nL * T.nL * nb;

@@ -188,7 +188,6 @@ class ReductionEngine {
   bool use_tc_ = false; // tcgen05 GEMMs (else the dp4a CUDA-core kernels)
   bool fast_ = false;   // fp32-reciprocal residues (host-checked operand bound)
   bool sparse_carry_ = false;  // carry GEMM over the nonzero K blocks of Jp only
-  bool carry_kernel_ = false;  // DRZG_CARRY=kernel: the cp.async-staged carry kernel (slower so far)
   long long kblocks_ = 0;      // nonzero 128 x 128 blocks of Jp (system order)
   DevBuf<int> kb_ptr_, kb_idx_;
   DevBuf<int> ginv_;
@@ -212,7 +211,7 @@ class ReductionEngine {
   // temporaries
   int bcap_ = 0;
   DevBuf<int8_t> Bg_, IN_, Y_;
-  DevBuf<int16_t> Cy_;
+  DevBuf<int8_t> H_;
   DevBuf<int8_t> W_;
   cudaEvent_t ev0_, ev1_;
   Stager stager_;

@@ -7,7 +7,7 @@
 // with all residues held as Ld balanced base-q int8 digit planes:
 //   gather_kernel     b = P_v w                      (per-v index table)
 //   dixon_gemm_kernel y_k = bal( Cq . in_k )         (int8 dot products)
-//   dixon_carry_kernel c_{k+1} = (b_k + c_k - Jp y_k) / q,  in_{k+1}
+//   dixon_carry_kernel c = (r_k - Jp y_k) / q, r_{k+1} = b_{k+1} + c = in_{k+1} + q h_{k+1}
 //   epilogue_kernel   w'[g] = carry-normalise( sum (x_i + mu_i) y[r] )
 // Setup/bookkeeping kernels: seed materialisation, state merge
 // (combine_states, reduction.hpp:426-451) and floor accumulation
@@ -53,6 +53,8 @@ __global__ void __launch_bounds__(256) gather_kernel(StepArgs a) {
       tile[tid][i] = g[i] >= 0 ? a.pool[base[i] + (size_t)t * a.sidep + g[i]] : (int8_t)0;
     __syncthreads();
     // 256 rows x 32 bytes = 2048 words; 8 per thread, row-contiguous
+    // (digit 0 of a pool state is balanced, so b_0 is the first digit GEMM's
+    // operand as it stands and the first carry's residual r_0)
     for (int e = tid; e < kGatherRows * kGatherStates / 4; e += 256) {
       int row = e >> 3, w = e & 7;
       int rr = r0 + row;
@@ -60,14 +62,6 @@ __global__ void __launch_bounds__(256) gather_kernel(StepArgs a) {
       uint32_t word = *reinterpret_cast<const uint32_t*>(&tile[row][w * 4]);
       size_t off = (size_t)rr * a.P + s0 + w * 4;
       *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * a.nLp * a.P + off) = word;
-      if (t == 0) {
-        uint32_t inw = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b)
-          inw |= (uint32_t)(uint8_t)(int8_t)a.fq.bal((int8_t)(word >> (8 * b))) << (8 * b);
-        *reinterpret_cast<uint32_t*>(a.IN + off) = inw;
-        *reinterpret_cast<uint2*>(a.Cy + off) = make_uint2(0, 0);
-      }
     }
     __syncthreads();
   }
@@ -115,6 +109,7 @@ __global__ void __launch_bounds__(256) dixon_gemm_kernel(StepArgs a, int k) {
   }
 }
 
+// c = (r_k - Jp y_k) / q with r_0 = b_0, r_k = in_k + q h_k; in_{k+1}, h_{k+1}
 __global__ void dixon_carry_kernel(StepArgs a, int k) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y;
@@ -123,37 +118,13 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
   int sum = 0;
   for (int e = a.jp_ptr[r]; e < a.jp_ptr[r + 1]; ++e) sum += a.jp_val[e] * (int)y[(size_t)a.jp_col[e] * a.P + s];
   size_t off = (size_t)r * a.P + s;
+  const int rk = k ? (int)a.IN[off] + a.q * (int)a.H[off] : (int)a.Bg[off];
   int rem;
-  int c = a.fq.divfloor((int)a.Bg[(size_t)k * a.nLp * a.P + off] + (k ? (int)a.Cy[off] : 0) - sum, rem);
-  a.Cy[off] = (int16_t)c;
-  if (k + 1 < a.Ld) a.IN[off] = (int8_t)a.fq.bal((int)a.Bg[(size_t)(k + 1) * a.nLp * a.P + off] + c);
-}
-
-// b = P_v W for the second and later steps of a chunk: lanes are states of
-// one (k, v)-sorted batch, so neighbouring lanes usually share v and read the
-// same W row: both sides state-contiguous
-__global__ void __launch_bounds__(256) gather_w_kernel(StepArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x * 32 + lane;
-  if (s >= a.B) return;
-  const int vd = a.vdir[s];
-  const size_t plane = (size_t)a.nLp * a.P, wplane = (size_t)a.sidep * a.P;
-  for (int r = blockIdx.y * 64 + warp; r < min(a.nL, (int)(blockIdx.y + 1) * 64); r += 8) {
-    const int g = a.gidx[(size_t)vd * a.nL + r];
-    const size_t off = (size_t)r * a.P + s;
-    int8_t b0 = 0;
-    for (int t = 0; t < a.Ld; ++t) {
-      int8_t bt = g >= 0 ? a.W[(size_t)t * wplane + (size_t)g * a.P + s] : (int8_t)0;
-      a.Bg[(size_t)t * plane + off] = bt;
-      if (t == 0) b0 = bt;
-    }
-    a.IN[off] = (int8_t)a.fq.bal(b0);
-    a.Cy[off] = 0;
-  }
-}
-
-__device__ __forceinline__ int pick6(int i, int x0, int x1, int x2, int x3, int x4, int x5) {
-  return i == 0 ? x0 : i == 1 ? x1 : i == 2 ? x2 : i == 3 ? x3 : i == 4 ? x4 : x5;
+  const int c = a.fq.divfloor(rk - sum, rem);  // exact
+  int hq = a.fq.divfloor((int)a.Bg[(size_t)(k + 1) * a.nLp * a.P + off] + c, rem);
+  if (rem > (a.q >> 1)) rem -= a.q, ++hq;
+  a.IN[off] = (int8_t)rem;
+  a.H[off] = (int8_t)hq;
 }
 
 // w' = T_x y into W (Ld x sidep x P) or the next step's gathered operand Bg,

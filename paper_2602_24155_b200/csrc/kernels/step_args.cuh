@@ -42,7 +42,7 @@ struct StepArgs {
   // temporaries, state-contiguous ("MN-major" GEMM operands)
   int8_t* Bg;             // Ld x nLp x P
   int8_t* IN;             // nLp x P
-  int16_t* Cy;            // nLp x P (|carry| < 2^15, checked on the host)
+  int8_t* H;              // nLp x P: high part of the running residual r = in + q h
   int8_t* W;              // Ld x sidep x P: the state between steps of a chunk
   int8_t* Y;              // Ld x nLp x P
 };

@@ -213,76 +213,69 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int acc = i & 1;
       const int m = m0 + quarter * 32 + lane;
       const bool mok = m < epi.M;
-      if (epi.b_mn && epi.mode == (int)TcEpilogue::carry && mok && n0 + half * (BN / 2) < epi.N) {
+      // carry operands: r_k = b_0 (k = 0) or in_k + q h_k, and b_{k+1}
+      const size_t P = (size_t)epi.P;
+      const bool carry = epi.b_mn && epi.mode == (int)TcEpilogue::carry;
+      const int8_t* rlo = epi.k ? epi.IN + (size_t)m * P : epi.Bg + (size_t)m * P;  // in_k, or b_0
+      const int8_t* rhi = epi.H + (size_t)m * P;                                      // h_k (k > 0)
+      const int8_t* bk1p = epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P;
+      if (carry && mok && n0 + half * (BN / 2) < epi.N) {
         // the carry inputs do not depend on the accumulator: pull this
         // thread's row segments into L2 while the mainloop runs
-        const size_t P = (size_t)epi.P;
         const size_t nb = (size_t)(n0 + half * (BN / 2));
-        const int8_t* bgk = epi.Bg + ((size_t)epi.k * epi.nLp + m) * P + nb;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(bgk));
-        if (epi.k + 1 < epi.Ld) asm volatile("prefetch.global.L2 [%0];" ::"l"(bgk + (size_t)epi.nLp * P));
-        if (epi.k) {
-          const int16_t* cy = epi.Cy + (size_t)m * P + nb;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(cy));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(cy + 64));
-        }
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rlo + nb));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(bk1p + nb));
+        if (epi.k) asm volatile("prefetch.global.L2 [%0];" ::"l"(rhi + nb));
       }
       mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (epi.b_mn && epi.mode == (int)TcEpilogue::carry) {
-        // carry on state-contiguous rows, software-pipelined: the 16-byte
-        // loads of chunk c+16 are in flight while chunk c is computed
-        const size_t P = (size_t)epi.P;
-        const bool last = epi.k + 1 >= epi.Ld;
+      if (carry) {
+        // c = (r_k - Jp y_k) / q (exact), r_{k+1} = b_{k+1} + c, stored as
+        // in_{k+1} = bal(r_{k+1}) (the next digit GEMM's operand, in place
+        // over in_k) and its quotient h_{k+1} (|h| <= 4); software-pipelined:
+        // the 16-byte loads of chunk c+16 are in flight while chunk c is computed
+        const bool wh = epi.k + 2 < epi.Ld;  // a later carry reads h_{k+1}
         const int cbeg = half * (BN / 2), cend = (half + 1) * (BN / 2);
-        const int8_t* bgk = epi.Bg + ((size_t)epi.k * epi.nLp + m) * P;
-        const int8_t* bgk1 = epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P;
-        uint4 nbk = make_uint4(0, 0, 0, 0), nbk1 = nbk, nc0 = nbk, nc1 = nbk;
+        uint4 nlo = make_uint4(0, 0, 0, 0), nhi = nlo, nb1 = nlo;
         auto fetch = [&](int c) {
           const int nb = n0 + c;
           if (!mok || nb >= epi.N) return;
-          nbk = __ldg(reinterpret_cast<const uint4*>(bgk + nb));
-          if (!last) nbk1 = __ldg(reinterpret_cast<const uint4*>(bgk1 + nb));
-          if (epi.k) {
-            const uint4* cyp = reinterpret_cast<const uint4*>(epi.Cy + (size_t)m * P + nb);
-            nc0 = cyp[0];
-            nc1 = cyp[1];
-          }
+          nlo = __ldg(reinterpret_cast<const uint4*>(rlo + nb));
+          nb1 = __ldg(reinterpret_cast<const uint4*>(bk1p + nb));
+          if (epi.k) nhi = __ldg(reinterpret_cast<const uint4*>(rhi + nb));
         };
         fetch(cbeg);
         for (int c = cbeg; c < cend; c += 16) {
-          const uint4 bk = nbk, bk1 = nbk1, c0 = nc0, c1 = nc1;
+          const uint4 lo = nlo, hi = nhi, b1 = nb1;
           if (c + 16 < cend) fetch(c + 16);
           int v[16];
           tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
           const int nb = n0 + c;
           if (!mok || nb >= epi.N) continue;
-          const uint32_t bw[4] = {bk.x, bk.y, bk.z, bk.w};
-          const uint32_t b1w[4] = {bk1.x, bk1.y, bk1.z, bk1.w};
-          const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          uint32_t cn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          uint32_t in4[4] = {0, 0, 0, 0};
+          const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
+          const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
+          const uint32_t b1w[4] = {b1.x, b1.y, b1.z, b1.w};
+          uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const int b0j = (int)(int8_t)(bw[j >> 2] >> (8 * (j & 3)));
-            const int b1j = (int)(int8_t)(b1w[j >> 2] >> (8 * (j & 3)));
-            const int ccj = epi.k ? (int)(int16_t)(cw[j >> 1] >> (16 * (j & 1))) : 0;
-            int cnew, inb;
+            const int sh = 8 * (j & 3);
+            const int r = (int)(int8_t)(low[j >> 2] >> sh) + (epi.k ? epi.q * (int)(int8_t)(hiw[j >> 2] >> sh) : 0);
+            const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
+            int cnew, inb, hq;
             if (epi.fast) {
-              cnew = epi.fq.div_exact_fast(b0j + ccj - v[j]);
-              inb = epi.fq.bal_fast(b1j + cnew);
+              cnew = epi.fq.div_exact_fast(r - v[j]);
+              inb = epi.fq.balq(b1j + cnew, hq);
             } else {
               int rem;
-              cnew = epi.fq.divfloor(b0j + ccj - v[j], rem);  // exact
-              inb = epi.fq.bal(b1j + cnew);
+              cnew = epi.fq.divfloor(r - v[j], rem);  // exact
+              hq = epi.fq.divfloor(b1j + cnew, inb);
+              if (inb > (epi.q >> 1)) inb -= epi.q, ++hq;
             }
-            cn[j >> 1] |= ((uint32_t)cnew & 0xFFFFu) << (16 * (j & 1));
-            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * (j & 3));
+            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
+            h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
           }
-          uint4* cyw = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
-          cyw[0] = make_uint4(cn[0], cn[1], cn[2], cn[3]);
-          cyw[1] = make_uint4(cn[4], cn[5], cn[6], cn[7]);
-          if (!last) *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+          *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+          if (wh) *reinterpret_cast<uint4*>(epi.H + (size_t)m * P + nb) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
         }
       } else
       for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
@@ -309,47 +302,6 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           *reinterpret_cast<uint4*>(epi.Y + ((size_t)epi.k * epi.nLp + m) * epi.P + nb) =
               make_uint4(w4[0], w4[1], w4[2], w4[3]);
-        } else if (epi.b_mn) {
-          // carry on state-contiguous rows: 16-byte vector loads and stores
-          const size_t P = (size_t)epi.P;
-          const bool last = epi.k + 1 >= epi.Ld;
-          uint4 bk = __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)epi.k * epi.nLp + m) * P + nb));
-          uint4 bk1 = last ? make_uint4(0, 0, 0, 0)
-                           : __ldg(reinterpret_cast<const uint4*>(epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P + nb));
-          uint4* cyp = reinterpret_cast<uint4*>(epi.Cy + (size_t)m * P + nb);
-          // c_0 = 0: digit 0 ignores whatever the previous step left in Cy
-          uint4 c0 = make_uint4(0, 0, 0, 0), c1 = make_uint4(0, 0, 0, 0);
-          if (epi.k) {
-            c0 = cyp[0];
-            c1 = cyp[1];
-          }
-          // unpack with shifts only (pointer views would spill to local memory)
-          const uint32_t bw[4] = {bk.x, bk.y, bk.z, bk.w};
-          const uint32_t b1w[4] = {bk1.x, bk1.y, bk1.z, bk1.w};
-          const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-          uint32_t cn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-          uint32_t in4[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int b0j = (int)(int8_t)(bw[j >> 2] >> (8 * (j & 3)));
-            const int b1j = (int)(int8_t)(b1w[j >> 2] >> (8 * (j & 3)));
-            const int ccj = (int)(int16_t)(cw[j >> 1] >> (16 * (j & 1)));
-            int cnew, inb;
-            if (epi.fast) {
-              cnew = epi.fq.div_exact_fast(b0j + ccj - v[j]);
-              inb = epi.fq.bal_fast(b1j + cnew);
-            } else {
-              int rem;
-              cnew = epi.fq.divfloor(b0j + ccj - v[j], rem);  // exact
-              inb = epi.fq.bal(b1j + cnew);
-            }
-            cn[j >> 1] |= ((uint32_t)cnew & 0xFFFFu) << (16 * (j & 1));
-            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * (j & 3));
-          }
-          cyp[0] = make_uint4(cn[0], cn[1], cn[2], cn[3]);
-          cyp[1] = make_uint4(cn[4], cn[5], cn[6], cn[7]);
-          if (!last)
-            *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
         }
       }
       // all of this warp's TMEM reads of buffer `acc` are complete
@@ -361,229 +313,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
-}
-
-// ---------------------------------------------------------------------------
-// Dixon carry step: D = Jp . y_k (block-sparse K), then per element
-//   c' = (b_k + c - D) / q   (exact),   in' = bal(b_{k+1} + c')
-// The carry is bound by its epilogue's memory traffic (7 bytes per element
-// against ~29% of a dense K loop), so this kernel is shaped for bytes in
-// flight rather than MMA rate: 128 x 128 tiles, a 2-stage operand ring, and
-// per-thread cp.async staging of the epilogue inputs (b_k, b_{k+1}, c rows),
-// double-buffered so that tile i+1's inputs stream in while tile i is being
-// finished.  warp 0: TMA producer, warp 1: MMA issuer, warp 2: TMEM
-// allocator, warps 4..11: epilogue (TMEM lane quarter e % 4, 64-state half e / 4).
-namespace cy {
-constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
-constexpr int EBUF = 1;  // epilogue staging buffers
-constexpr int A_BYTES = BM * BK, B_BYTES = BN * BK;
-constexpr int EPI_THREADS = 256;
-constexpr int ROW = 64 + 64 + 128;  // b_k, b_{k+1} (64 states int8), c (64 states int16)
-constexpr int ROW_PITCH = ROW + 16; // 4-bank skew between lanes
-constexpr int STAGE_BYTES = EBUF * EPI_THREADS * ROW_PITCH;
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + STAGE_BYTES + 1024 + 256;
-constexpr int THREADS = 128 + EPI_THREADS;
-}  // namespace cy
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;            // LBO unused (one 128-wide N atom)
-  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: next 8-row K group
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
-__global__ void __launch_bounds__(cy::THREADS, 1)
-    carry_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
-                 uint32_t idesc, TcEpiArgs epi) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = base;
-  uint8_t* sB = base + cy::STAGES * cy::A_BYTES;
-  uint8_t* sE = sB + cy::STAGES * cy::B_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sE + cy::STAGE_BYTES);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + cy::STAGES;
-  uint64_t* tfull = bars + 2 * cy::STAGES;       // [2]
-  uint64_t* tempty = bars + 2 * cy::STAGES + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * cy::STAGES + 4);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (K + cy::BK - 1) / cy::BK;
-  const int mt = (epi.M + cy::BM - 1) / cy::BM, ntl = (epi.N + cy::BN - 1) / cy::BN;
-  const int tiles = mt * ntl;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < cy::STAGES; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&tfull[b]), 1);
-      mbar_init(smem_u32(&tempty[b]), cy::EPI_THREADS / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * cy::BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int mi = t % mt;
-        const int m0 = mi * cy::BM, n0 = (t / mt) * cy::BN;
-        const int kb0 = epi.kb_ptr ? __ldg(epi.kb_ptr + mi) : 0;
-        const int nkt = epi.kb_ptr ? __ldg(epi.kb_ptr + mi + 1) - kb0 : nk;
-        for (int kb = 0; kb < nkt; ++kb, ++it) {
-          const int kc = (epi.kb_ptr ? __ldg(epi.kb_idx + kb0 + kb) : kb) * cy::BK;
-          const int s = it % cy::STAGES;
-          mbar_wait(smem_u32(&empty[s]), ((it / cy::STAGES) & 1) ^ 1);
-          const uint32_t fb = smem_u32(&full[s]);
-          mbar_expect_tx(fb, cy::A_BYTES + cy::B_BYTES);
-          tma_load_2d(smem_u32(sA + s * cy::A_BYTES), &tmA, fb, kc, m0);
-          tma_load_2d(smem_u32(sB + s * cy::B_BYTES), &tmB, fb, n0, kc);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int it = 0, i = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-        const int acc = i & 1;
-        mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t d = tmem + (uint32_t)(acc * cy::BN);
-        const int mi = t % mt;
-        const int nkt = epi.kb_ptr ? __ldg(epi.kb_ptr + mi + 1) - __ldg(epi.kb_ptr + mi) : nk;
-        for (int kb = 0; kb < nkt; ++kb, ++it) {
-          const int s = it % cy::STAGES;
-          mbar_wait(smem_u32(&full[s]), (it / cy::STAGES) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a0 = smem_u32(sA + s * cy::A_BYTES), b0 = smem_u32(sB + s * cy::B_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < cy::BK / 32; ++kk)
-            mma_i8(d, sw128_desc(a0 + kk * 32), sw128_mn_desc_1atom(b0 + kk * 4096), idesc, (kb | kk) != 0);
-          mma_commit(smem_u32(&empty[s]));
-        }
-        mma_commit(smem_u32(&tfull[acc]));
-      }
-    }
-  } else if (warp >= 4) {
-    const int e = warp - 4, et = threadIdx.x - 128;
-    const int quarter = e & 3, half = e >> 2;
-    const size_t P = (size_t)epi.P;
-    const int k = epi.k;
-    const bool last = k + 1 >= epi.Ld;
-    const int8_t* bgk = epi.Bg + (size_t)k * epi.nLp * P;
-    const int8_t* bgk1 = epi.Bg + (size_t)(k + 1) * epi.nLp * P;
-    const uint32_t stage0 = smem_u32(sE) + (uint32_t)(et * cy::ROW_PITCH);
-    // issue the epilogue inputs of tile t into buffer b (one commit group)
-    auto prefetch = [&](int t, int b) {
-      const int m = (t % mt) * cy::BM + quarter * 32 + lane;
-      const int nb = (t / mt) * cy::BN + half * 64;
-      const uint32_t dst = stage0 + (uint32_t)(b * cy::EPI_THREADS * cy::ROW_PITCH);
-      if (m < epi.M && nb < epi.N) {
-        const int8_t* s0 = bgk + (size_t)m * P + nb;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cp_async16(dst + c * 16, s0 + c * 16);
-        if (!last) {
-          const int8_t* s1 = bgk1 + (size_t)m * P + nb;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) cp_async16(dst + 64 + c * 16, s1 + c * 16);
-        }
-        if (k) {
-          const int16_t* s2 = epi.Cy + (size_t)m * P + nb;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) cp_async16(dst + 128 + c * 16, s2 + c * 8);
-        }
-      }
-      cp_async_commit();
-    };
-    int i = 0;
-    if (blockIdx.x < tiles) prefetch(blockIdx.x, 0);
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      const int acc = i & 1, b = cy::EBUF == 2 ? (i & 1) : 0;
-      const int m = (t % mt) * cy::BM + quarter * 32 + lane;
-      const int nb0 = (t / mt) * cy::BN + half * 64;
-      if (cy::EBUF == 2 && t + (int)gridDim.x < tiles) {
-        prefetch(t + gridDim.x, b ^ 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-      mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint8_t* row = sE + (size_t)(b * cy::EPI_THREADS + et) * cy::ROW_PITCH;
-      const bool ok = m < epi.M && nb0 < epi.N;
-#pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        int v[16];
-        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * cy::BN + half * 64 + ch * 16), v);
-        if (!ok) continue;
-        const uint4 bk = *reinterpret_cast<const uint4*>(row + ch * 16);
-        const uint4 bk1 = last ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4*>(row + 64 + ch * 16);
-        uint4 c0 = make_uint4(0, 0, 0, 0), c1 = c0;
-        if (k) {
-          c0 = *reinterpret_cast<const uint4*>(row + 128 + ch * 32);
-          c1 = *reinterpret_cast<const uint4*>(row + 128 + ch * 32 + 16);
-        }
-        const uint32_t bw[4] = {bk.x, bk.y, bk.z, bk.w};
-        const uint32_t b1w[4] = {bk1.x, bk1.y, bk1.z, bk1.w};
-        const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        uint32_t cn[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        uint32_t in4[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int b0j = (int)(int8_t)(bw[j >> 2] >> (8 * (j & 3)));
-          const int b1j = (int)(int8_t)(b1w[j >> 2] >> (8 * (j & 3)));
-          const int ccj = (int)(int16_t)(cw[j >> 1] >> (16 * (j & 1)));
-          int cnew, inb;
-          if (epi.fast) {
-            cnew = epi.fq.div_exact_fast(b0j + ccj - v[j]);
-            inb = epi.fq.bal_fast(b1j + cnew);
-          } else {
-            int rem;
-            cnew = epi.fq.divfloor(b0j + ccj - v[j], rem);  // exact
-            inb = epi.fq.bal(b1j + cnew);
-          }
-          cn[j >> 1] |= ((uint32_t)cnew & 0xFFFFu) << (16 * (j & 1));
-          in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * (j & 3));
-        }
-        const size_t off = (size_t)m * P + nb0 + ch * 16;
-        uint4* cyw = reinterpret_cast<uint4*>(epi.Cy + off);
-        cyw[0] = make_uint4(cn[0], cn[1], cn[2], cn[3]);
-        cyw[1] = make_uint4(cn[4], cn[5], cn[6], cn[7]);
-        if (!last) *reinterpret_cast<uint4*>(epi.IN + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
-      }
-      if (cy::EBUF == 1 && t + (int)gridDim.x < tiles) prefetch(t + gridDim.x, 0);
-      __syncwarp();
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * cy::BN));
 }
 
 }  // namespace tc
@@ -648,32 +377,5 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
   DRZG_REQUIRE(e == cudaSuccess, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
 }
 
-
-void tc_carry_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int ldb, int K, const TcEpiArgs& epi,
-                 cudaStream_t st) {
-  DRZG_REQUIRE(epi.b_mn && epi.mode == (int)TcEpilogue::carry, "tc_carry: carry epilogue on an MN-major B only");
-  DRZG_REQUIRE(lda % 16 == 0 && ldb % 64 == 0, "tc_carry: pitches must be multiples of 16 / 64 bytes");
-  CUtensorMap ma = make_map(A, rowsA, lda, K, tc::cy::BM);
-  CUtensorMap mb = make_map(B, K, ldb, ldb, tc::cy::BK);  // K rows x ldb states, box 128 x 128
-  uint32_t a_signed = epi.a_unsigned ? 0u : 1u;
-  uint32_t idesc = (2u << 4) | (a_signed << 7) | (1u << 10) | (1u << 16) | ((uint32_t)(tc::cy::BN >> 3) << 17) |
-                   ((uint32_t)(tc::cy::BM >> 4) << 24);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::carry_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::cy::SMEM_BYTES);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int tiles = ((epi.N + tc::cy::BN - 1) / tc::cy::BN) * ((epi.M + tc::cy::BM - 1) / tc::cy::BM);
-  dim3 grid(std::min(tiles, sms));
-  tc::carry_kernel<<<grid, tc::cy::THREADS, tc::cy::SMEM_BYTES, st>>>(ma, mb, K, idesc, epi);
-  cudaError_t e = cudaGetLastError();
-  DRZG_REQUIRE(e == cudaSuccess, std::string("tc_carry launch: ") + cudaGetErrorString(e));
-}
 
 }  // namespace drzg

@@ -8,7 +8,8 @@
 // four epilogue warps drain TMEM with tcgen05.ld and apply the Dixon step's
 // elementwise epilogue in registers:
 //   EPI_DIGIT  y_k = bal(D mod q) -> int8 Y plane          (D = Cq . in_k)
-//   EPI_CARRY  c'  = (b_k + c - D) / q,  in' = bal(b_{k+1} + c')  (D = Jp . y_k)
+//   EPI_CARRY  c = (r_k - D) / q, r_{k+1} = b_{k+1} + c -> in_{k+1} = bal(r_{k+1}), h_{k+1}
+//              with r_k = b_0 (k = 0) or in_k + q h_k                  (D = Jp . y_k)
 //   EPI_RAW    D as int32 (tests)
 #pragma once
 
@@ -37,9 +38,9 @@ struct TcEpiArgs {
   // digit
   int8_t* Y = nullptr;     // N x Ld x nLp
   // carry
-  const int8_t* Bg = nullptr;  // N x Ld x nLp
-  int16_t* Cy = nullptr;       // (b_mn) nLp x P carries
-  int8_t* IN = nullptr;        // N x nLp
+  const int8_t* Bg = nullptr;  // Ld x nLp x P gathered digits b_t
+  int8_t* H = nullptr;         // nLp x P: high part of the running residual r = in + q h
+  int8_t* IN = nullptr;        // nLp x P: in_k (read by carry k > 0, overwritten with in_{k+1})
   // block-sparse A (carry): M tile i runs over K blocks kb_idx[kb_ptr[i] ..
   // kb_ptr[i+1]) (128-wide) only; null = dense
   const int* kb_ptr = nullptr;
@@ -52,10 +53,5 @@ struct TcEpiArgs {
 void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB, int ldb, int K,
                 const TcEpiArgs& epi, cudaStream_t st);
 
-// the Dixon carry (epi.mode == carry, MN-major B = y_k with pitch ldb = P):
-// 128 x 128 tiles, block-sparse K when epi.kb_ptr is set, cp.async-staged
-// epilogue inputs (see carry_kernel)
-void tc_carry_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int ldb, int K, const TcEpiArgs& epi,
-                 cudaStream_t st);
 
 }  // namespace drzg
