@@ -857,121 +857,133 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
     auto hp1 = std::chrono::steady_clock::now();
     auto hp2 = hp1;
-    // moves (reduction.hpp:486-496) for every state, on host threads
-    const size_t nf = front.size();
-    std::vector<int> vd(nf);
-    std::vector<i64> kk(nf);
-    {
-      const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_, nf / 4096 + 1));
-      std::vector<std::thread> pool;
-      std::vector<std::exception_ptr> errs(nth);
-      for (int t = 0; t < nth; ++t)
-        pool.emplace_back([&, t] {
-          try {
-            for (size_t i = t * nf / nth; i < (t + 1) * nf / nth; ++i) {
-              Expo v;
-              i64 k;
-              pchunk_move(T.d, n_, (i64)p_, front[i].u, front[i].pole, T.S, &v, &k);
-              DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
-              DRZG_REQUIRE(legal(T.d, front[i].u, v, k, T.S), "reduce_chunk: illegal move");
-              vd[i] = (int)rank_of(v);
-              kk[i] = k;
+    // the front is handed to the launcher in chunks of states (each sorted
+    // by (k, v) on its own), so the device starts on a sweep before the
+    // policy has finished it; the seed work of pole P rides with chunk 0
+    const size_t nfront = front.size();
+    constexpr size_t kChunk = (size_t)1 << 17;
+    for (size_t f0 = 0; f0 < nfront; f0 += kChunk) {
+      if (f0) {
+        cmd = std::make_unique<SweepCmd>();
+        cmd->pole = P;
+      }
+      const size_t nf = std::min(nfront, f0 + kChunk) - f0;
+      // moves (reduction.hpp:486-496) for every state, on host threads
+      std::vector<int> vd(nf);
+      std::vector<i64> kk(nf);
+      {
+        const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_, nf / 4096 + 1));
+        std::vector<std::thread> pool;
+        std::vector<std::exception_ptr> errs(nth);
+        for (int t = 0; t < nth; ++t)
+          pool.emplace_back([&, t] {
+            try {
+              for (size_t i = t * nf / nth; i < (t + 1) * nf / nth; ++i) {
+                Expo v;
+                i64 k;
+                pchunk_move(T.d, n_, (i64)p_, front[f0 + i].u, front[f0 + i].pole, T.S, &v, &k);
+                DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
+                DRZG_REQUIRE(legal(T.d, front[f0 + i].u, v, k, T.S), "reduce_chunk: illegal move");
+                vd[i] = (int)rank_of(v);
+                kk[i] = k;
+              }
+            } catch (...) {
+              errs[t] = std::current_exception();
             }
-          } catch (...) {
-            errs[t] = std::current_exception();
-          }
-        });
-      for (auto& th : pool) th.join();
-      for (auto& e2 : errs)
-        if (e2) std::rethrow_exception(e2);
-    }
-    // longest chunks first, then by direction: counting sort on (k, v)
-    std::vector<int> order(nf);
-    {
-      const int ndir = T.ndir;
-      i64 kmx = 1;
-      for (i64 k : kk) kmx = std::max(kmx, k);
-      std::vector<int> cnt((size_t)(kmx + 1) * ndir + 1, 0);
-      auto bucket = [&](size_t i) { return (size_t)(kmx - kk[i]) * ndir + vd[i]; };
-      for (size_t i = 0; i < nf; ++i) ++cnt[bucket(i) + 1];
-      for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
-      for (size_t i = 0; i < nf; ++i) order[cnt[bucket(i)]++] = (int)i;
-    }
-    std::vector<int>& hslot = cmd->hslot;
-    std::vector<int>& hvdir = cmd->hvdir;
-    std::vector<int>& hu0 = cmd->hu0;
-    std::vector<i64>& ks = cmd->ks;
-    hslot.resize(nf);
-    hvdir.resize(nf);
-    hu0.resize(nf * nv);
-    ks.resize(nf);
-    for (size_t o = 0; o < nf; ++o) {
-      const int i = order[o];
-      hslot[o] = front[i].slot;
-      hvdir[o] = vd[i];
-      ks[o] = kk[i];
-      for (int j = 0; j < nv; ++j) hu0[o * nv + j] = front[i].u[j];
-    }
-    auto hp3 = std::chrono::steady_clock::now();
-    for (i64 k : ks) cmd->matvecs += k;  // run_sweep: one matvec per state per step
-    led.matvecs += cmd->matvecs;
-    auto hp4 = std::chrono::steady_clock::now();
-    led.startups += (i64)front.size();
-    // land every state at pole P - k; a state landing on a key already there
-    // is combined at once (reduction.hpp:502 combines after every sweep)
-    std::vector<int>& fs = cmd->fs;
-    std::vector<int>& fc = cmd->fc;
-    std::vector<int>& fu = cmd->fu;
-    std::vector<std::pair<int, int>> merges;  // (dst slot, src slot)
-    for (int i : order) {
-      HS h = front[i];
-      const Expo& v = dirs_host_[vd[i]];
-      for (int j = 0; j < nv; ++j) h.u[j] -= (int)(kk[i] * v[j]);
-      h.pole -= (int)kk[i];
-      const u64 kh = key(h.col, h.u);
-      if (h.pole == n_) {
-        fs.push_back(h.slot);
-        fc.push_back(h.col);
-        for (int j = 0; j < nv; ++j) fu.push_back(h.u[j]);
-        floor_arrivals[h.col]++;
-        floor_keys[h.col].insert(kh, 0);
-      } else {
-        auto& idx = landed_idx[h.pole];
-        auto& lst = landed[h.pole];
-        const int pos = idx.insert(kh, (int)lst.size());
-        if (pos == (int)lst.size()) {
-          lst.push_back(h);
+          });
+        for (auto& th : pool) th.join();
+        for (auto& e2 : errs)
+          if (e2) std::rethrow_exception(e2);
+      }
+      // longest chunks first, then by direction: counting sort on (k, v)
+      std::vector<int> order(nf);
+      {
+        const int ndir = T.ndir;
+        i64 kmx = 1;
+        for (i64 k : kk) kmx = std::max(kmx, k);
+        std::vector<int> cnt((size_t)(kmx + 1) * ndir + 1, 0);
+        auto bucket = [&](size_t i) { return (size_t)(kmx - kk[i]) * ndir + vd[i]; };
+        for (size_t i = 0; i < nf; ++i) ++cnt[bucket(i) + 1];
+        for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
+        for (size_t i = 0; i < nf; ++i) order[cnt[bucket(i)]++] = (int)i;
+      }
+      std::vector<int>& hslot = cmd->hslot;
+      std::vector<int>& hvdir = cmd->hvdir;
+      std::vector<int>& hu0 = cmd->hu0;
+      std::vector<i64>& ks = cmd->ks;
+      hslot.resize(nf);
+      hvdir.resize(nf);
+      hu0.resize(nf * nv);
+      ks.resize(nf);
+      for (size_t o = 0; o < nf; ++o) {
+        const int i = order[o];
+        hslot[o] = front[f0 + i].slot;
+        hvdir[o] = vd[i];
+        ks[o] = kk[i];
+        for (int j = 0; j < nv; ++j) hu0[o * nv + j] = front[f0 + i].u[j];
+      }
+      auto hp3 = std::chrono::steady_clock::now();
+      for (i64 k : ks) cmd->matvecs += k;  // run_sweep: one matvec per state per step
+      led.matvecs += cmd->matvecs;
+      auto hp4 = std::chrono::steady_clock::now();
+      led.startups += (i64)nf;
+      // land every state at pole P - k; a state landing on a key already there
+      // is combined at once (reduction.hpp:502 combines after every sweep)
+      std::vector<int>& fs = cmd->fs;
+      std::vector<int>& fc = cmd->fc;
+      std::vector<int>& fu = cmd->fu;
+      std::vector<std::pair<int, int>> merges;  // (dst slot, src slot)
+      for (int i : order) {
+        HS h = front[f0 + i];
+        const Expo& v = dirs_host_[vd[i]];
+        for (int j = 0; j < nv; ++j) h.u[j] -= (int)(kk[i] * v[j]);
+        h.pole -= (int)kk[i];
+        const u64 kh = key(h.col, h.u);
+        if (h.pole == n_) {
+          fs.push_back(h.slot);
+          fc.push_back(h.col);
+          for (int j = 0; j < nv; ++j) fu.push_back(h.u[j]);
+          floor_arrivals[h.col]++;
+          floor_keys[h.col].insert(kh, 0);
         } else {
-          merges.emplace_back(lst[pos].slot, h.slot);
-          led.combines += 1;
+          auto& idx = landed_idx[h.pole];
+          auto& lst = landed[h.pole];
+          const int pos = idx.insert(kh, (int)lst.size());
+          if (pos == (int)lst.size()) {
+            lst.push_back(h);
+          } else {
+            merges.emplace_back(lst[pos].slot, h.slot);
+            led.combines += 1;
+          }
         }
       }
-    }
-    if (!merges.empty()) {
-      std::sort(merges.begin(), merges.end());
-      std::vector<int>& gptr = cmd->gptr;
-      std::vector<int>& mem = cmd->mem;
-      gptr.assign(1, 0);
-      for (size_t a = 0; a < merges.size();) {
-        size_t b2 = a;
-        mem.push_back(merges[a].first);
-        while (b2 < merges.size() && merges[b2].first == merges[a].first) mem.push_back(merges[b2++].second);
-        gptr.push_back((int)mem.size());
-        a = b2;
+      if (!merges.empty()) {
+        std::sort(merges.begin(), merges.end());
+        std::vector<int>& gptr = cmd->gptr;
+        std::vector<int>& mem = cmd->mem;
+        gptr.assign(1, 0);
+        for (size_t a = 0; a < merges.size();) {
+          size_t b2 = a;
+          mem.push_back(merges[a].first);
+          while (b2 < merges.size() && merges[b2].first == merges[a].first) mem.push_back(merges[b2++].second);
+          gptr.push_back((int)mem.size());
+          a = b2;
+        }
+        for (auto& m : merges) free_slot(m.second);
       }
-      for (auto& m : merges) free_slot(m.second);
+      auto hp5 = std::chrono::steady_clock::now();
+      {
+        auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+        host_t_[0] += sec(hp0, hp1);
+        host_t_[1] += sec(hp1, hp2);
+        host_t_[2] += sec(hp2, hp3);
+        (void)hp4;  // launch time is accounted by the launcher
+        host_t_[4] += sec(hp4, hp5);
+      }
+      for (int s : fs) free_slot(s);
+      push(std::move(cmd));
     }
-    auto hp5 = std::chrono::steady_clock::now();
-    {
-      auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
-      host_t_[0] += sec(hp0, hp1);
-      host_t_[1] += sec(hp1, hp2);
-      host_t_[2] += sec(hp2, hp3);
-      (void)hp4;  // launch time is accounted by the launcher
-      host_t_[4] += sec(hp4, hp5);
-    }
-    for (int s : fs) free_slot(s);
-    push(std::move(cmd));
+    if (cmd) push(std::move(cmd));  // seeds of a pole with no states left (none expected)
   }
     } catch (...) {
       perr = std::current_exception();
