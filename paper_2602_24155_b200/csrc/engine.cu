@@ -118,8 +118,19 @@ SysOrder order_system(const RuvTables& T, bool search) {
 
 ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t st)
     : T_(&T), n_(n), p_(p), st_(st) {
+  {
+    // stream-ordered allocations stay mapped between zeta functions (the
+    // default pool would hand them back to the driver at every sync)
+    int dev = 0;
+    DRZG_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t mp;
+    DRZG_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+    uint64_t keep = UINT64_MAX;
+    DRZG_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   DRZG_REQUIRE(T.dp.Ld <= dev::kLdMax, "engine: too many digit planes");
-  nLp_ = round_up(T.nL, 64);
+  // small systems pad to whole 128-row tiles (the one-launch Dixon kernel)
+  nLp_ = T.nL <= 256 ? round_up(T.nL, 128) : round_up(T.nL, 64);
   sidep_ = round_up(T.side, 16);
   slot_stride_ = (long long)T.dp.Ld * sidep_;
   gsize_ = (int)mono_count(T.nv, T.D - 1);
@@ -191,6 +202,8 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     }
   }
   sparse_carry_ = sparse_carry_ && use_tc_;
+  const char* fz = std::getenv("DRZG_FUSED");
+  fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
   if (sparse_carry_) {
     kb_ptr_.upload(ord.kb_ptr, st_);
     kb_idx_.upload(ord.kb_idx, st_);
@@ -456,6 +469,25 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
   const int nb = a.B;
   dim3 gG((nb + 63) / 64, nLp_ / 64);
   dim3 gC((nb + 127) / 128, T.nL);
+  if (fused_) {
+    // small systems: the whole solve of every state in one launch
+    FusedArgs f;
+    f.nL = T.nL;
+    f.nLp = nLp_;
+    f.N = nb;
+    f.P = bcap_;
+    f.Ld = T.dp.Ld;
+    f.q = T.dp.q;
+    f.fq = FastQ::make(T.dp.q);
+    f.fast = fast_ ? 1 : 0;
+    f.Bg = Bg_.p;
+    f.Y = Y_.p;
+    timed(&clock.gemm_ms, [&] { dixon_fused(C_.p, Jd_.p, f, st_); });
+    ++clock.gemm_launches;
+    clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * nb;
+    clock.carry_macs += (double)(T.dp.Ld - 1) * T.nL * T.nL * nb;
+    return;
+  }
   for (int k = 0; k < T.dp.Ld; ++k) {
     if (use_tc_) {
       // y_k = bal(Cq . in_k): tcgen05 int8, digit epilogue

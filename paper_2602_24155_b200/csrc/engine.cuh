@@ -188,6 +188,7 @@ class ReductionEngine {
   bool use_tc_ = false; // tcgen05 GEMMs (else the dp4a CUDA-core kernels)
   bool fast_ = false;   // fp32-reciprocal residues (host-checked operand bound)
   bool sparse_carry_ = false;  // carry GEMM over the nonzero K blocks of Jp only
+  bool fused_ = false;         // whole solve in one launch (nLp <= 256; DRZG_FUSED=0 disables)
   long long kblocks_ = 0;      // nonzero 128 x 128 blocks of Jp (system order)
   DevBuf<int> kb_ptr_, kb_idx_;
   DevBuf<int> ginv_;
@@ -214,7 +215,14 @@ class ReductionEngine {
   DevBuf<int8_t> H_;
   DevBuf<int8_t> W_;
   cudaEvent_t ev0_, ev1_;
-  Stager stager_;
+  // pinned staging ring shared by every engine of the process: pinning and
+  // unpinning host memory costs milliseconds per megabyte, so it is paid once
+  // (never freed; the process exit releases it)
+  static Stager& shared_stager() {
+    static Stager* s = new Stager();
+    return *s;
+  }
+  Stager& stager_ = shared_stager();
   double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
   unsigned host_threads_ = std::max(1u, std::thread::hardware_concurrency());
   std::vector<Expo> dirs_host_;

@@ -2,6 +2,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -315,6 +316,242 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
 }
 
+__device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO unused (one 128-wide N atom)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: next 8-row K group
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// Whole Dixon solve of a 128-state block in one CTA, for systems with
+// nLp <= 256 (the K3 surface: nL = 220).  Cq and Jp stay in shared memory
+// for the kernel's lifetime; in_k, y_k and the residual high part h_k live in
+// shared memory in the 128B-swizzled MN-major layout the MMA reads; each
+// digit is two tcgen05 products (Cq . in_k into TMEM columns [0, 256), Jp .
+// y_k into [256, 512)) separated by epilogues that write y_k (to shared memory
+// and to the global Y plane for the T_x epilogue) and in_{k+1}, h_{k+1}.  One
+// launch per pole drop instead of 2 Ld - 1, no intermediate HBM traffic
+// except b_{k+1} in and y_k out.
+//   warp 0: TMA (Cq, Jp once; b_0 per block)   warp 1: MMA issuer
+//   warp 2: TMEM allocator                     warps 4..11: epilogue
+namespace fz {
+constexpr int NS = 128;      // states per block
+constexpr int TILE = 128 * 128;
+constexpr int THREADS = 384;
+__host__ __device__ constexpr int smem_bytes(int nt) { return (2 * nt * nt + 3 * nt) * TILE + 1024 + 256; }
+}  // namespace fz
+
+// byte offset of (K row r, state s) in a 128B-swizzled MN-major box set
+// (one 16 KB box per 128 K rows; rows of 128 states)
+__device__ __forceinline__ uint32_t swz(int r, int s) {
+  return (uint32_t)((r >> 7) * fz::TILE + (r & 127) * 128 + ((((s >> 4) ^ (r & 7)) & 7) << 4) + (s & 15));
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(fz::THREADS, 1)
+    dixon_fused_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
+                       const __grid_constant__ CUtensorMap tmB0, uint32_t idesc_c, uint32_t idesc_j, FusedArgs fa) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nt = fa.nLp / 128;
+  uint8_t* sC = base;                       // nt x nt tiles (M tile mt, K box kb) at (mt * nt + kb)
+  uint8_t* sJ = sC + nt * nt * fz::TILE;
+  uint8_t* sIn = sJ + nt * nt * fz::TILE;   // nt boxes
+  uint8_t* sY = sIn + nt * fz::TILE;
+  uint8_t* sH = sY + nt * fz::TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + nt * fz::TILE);
+  uint64_t* barA = bars;      // Cq, Jp loaded
+  uint64_t* barB0 = bars + 1; // b_0 of the block loaded
+  uint64_t* barD = bars + 2;  // digit product done
+  uint64_t* barC = bars + 3;  // carry product done
+  uint64_t* barY = bars + 4;  // y_k drained (8 warps)
+  uint64_t* barIn = bars + 5; // in_{k+1}, h_{k+1} written (8 warps)
+  uint64_t* barFree = bars + 6;  // a block's last digit product done: sIn may be refilled
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Ld = fa.Ld;
+  const int nblk = (fa.N + fz::NS - 1) / fz::NS;
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(barA), 1);
+    mbar_init(smem_u32(barB0), 1);
+    mbar_init(smem_u32(barD), 1);
+    mbar_init(smem_u32(barC), 1);
+    mbar_init(smem_u32(barY), 8);
+    mbar_init(smem_u32(barIn), 8);
+    mbar_init(smem_u32(barFree), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmJ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB0) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(smem_u32(barA), (uint32_t)(2 * nt * nt * fz::TILE));
+      for (int mt = 0; mt < nt; ++mt)
+        for (int kb = 0; kb < nt; ++kb) {
+          tma_load_2d(smem_u32(sC + (mt * nt + kb) * fz::TILE), &tmC, smem_u32(barA), kb * 128, mt * 128);
+          tma_load_2d(smem_u32(sJ + (mt * nt + kb) * fz::TILE), &tmJ, smem_u32(barA), kb * 128, mt * 128);
+        }
+      int i = 0;
+      for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
+        // the previous block's last digit product has consumed sIn (a
+        // barrier of its own: barD runs Ld phases per block, and a parity
+        // wait only tells the current phase from the one before it)
+        if (i) mbar_wait(smem_u32(barFree), (uint32_t)((i - 1) & 1));
+        mbar_expect_tx(smem_u32(barB0), (uint32_t)(nt * fz::TILE));
+        for (int kb = 0; kb < nt; ++kb)
+          tma_load_2d(smem_u32(sIn + kb * fz::TILE), &tmB0, smem_u32(barB0), b * fz::NS, kb * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(smem_u32(barA), 0);
+      int i = 0;
+      for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
+        if (i) mbar_wait(smem_u32(barY), (uint32_t)((i * Ld - 1) & 1));  // last digit drained
+        mbar_wait(smem_u32(barB0), (uint32_t)(i & 1));
+        for (int k = 0; k < Ld; ++k) {
+          const int d = i * Ld + k;
+          if (k) mbar_wait(smem_u32(barIn), (uint32_t)((i * (Ld - 1) + k - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          for (int mt = 0; mt < nt; ++mt)
+            for (int kb = 0; kb < nt; ++kb) {
+              const uint32_t a0 = smem_u32(sC + (mt * nt + kb) * fz::TILE), b0 = smem_u32(sIn + kb * fz::TILE);
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_i8(tmem + (uint32_t)(mt * 128), sw128_desc(a0 + kk * 32), sw128_mn_desc_1atom(b0 + kk * 4096),
+                       idesc_c, (kb | kk) != 0);
+            }
+          mma_commit(smem_u32(barD));
+          if (k + 1 == Ld) mma_commit(smem_u32(barFree));
+          if (k + 1 < Ld) {
+            mbar_wait(smem_u32(barY), (uint32_t)(d & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int mt = 0; mt < nt; ++mt)
+              for (int kb = 0; kb < nt; ++kb) {
+                const uint32_t a0 = smem_u32(sJ + (mt * nt + kb) * fz::TILE), b0 = smem_u32(sY + kb * fz::TILE);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_i8(tmem + (uint32_t)(256 + mt * 128), sw128_desc(a0 + kk * 32),
+                         sw128_mn_desc_1atom(b0 + kk * 4096), idesc_j, (kb | kk) != 0);
+              }
+            mma_commit(smem_u32(barC));
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4, quarter = e & 3, mt = e >> 2;
+    const int m = mt * 128 + quarter * 32 + lane;  // K row of in / y, M row of the products
+    const bool active = mt < nt;
+    const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
+    const size_t P = (size_t)fa.P;
+    int i = 0;
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
+      const int n0 = b * fz::NS;
+      for (int k = 0; k < Ld; ++k) {
+        const int d = i * Ld + k;
+        const bool carry = k + 1 < Ld;
+        // b_{k+1} for this thread's row: independent of the products, in flight early
+        uint4 b1[8];
+        if (carry && active) {
+          const int8_t* src = fa.Bg + ((size_t)(k + 1) * fa.nLp + m) * P + n0;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            b1[ch] = n0 + ch * 16 < fa.N ? __ldg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
+        }
+        mbar_wait(smem_u32(barD), (uint32_t)(d & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (active) {
+          int8_t* yg = fa.Y + ((size_t)k * fa.nLp + m) * P + n0;
+#pragma unroll 1
+          for (int ch = 0; ch < 8; ++ch) {
+            int v[16];
+            tmem_ld16(lanebase + (uint32_t)(mt * 128 + ch * 16), v);
+            uint32_t w4[4];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t word = 0;
+#pragma unroll
+              for (int bb = 0; bb < 4; ++bb)
+                word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_fast(v[q4 * 4 + bb]) : fa.fq.bal(v[q4 * 4 + bb]))
+                        << (8 * bb);
+              w4[q4] = word;
+            }
+            const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            if (carry) *reinterpret_cast<uint4*>(sY + swz(m, ch * 16)) = y4;
+            if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
+          }
+        }
+        fence_async_smem();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(barY));
+        if (!carry) continue;
+        if (k == 0) mbar_wait(smem_u32(barB0), (uint32_t)(i & 1));  // b_0 (TMA) is r_0
+        mbar_wait(smem_u32(barC), (uint32_t)((i * (Ld - 1) + k) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (active) {
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            int v[16];
+            tmem_ld16(lanebase + (uint32_t)(256 + mt * 128 + ch * 16), v);
+            const uint32_t off = swz(m, ch * 16);
+            const uint4 lo = *reinterpret_cast<const uint4*>(sIn + off);
+            const uint4 hi = k ? *reinterpret_cast<const uint4*>(sH + off) : make_uint4(0, 0, 0, 0);
+            const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
+            const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
+            const uint32_t b1w[4] = {b1[ch].x, b1[ch].y, b1[ch].z, b1[ch].w};
+            uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int sh = 8 * (j & 3);
+              const int r = (int)(int8_t)(low[j >> 2] >> sh) + fa.q * (int)(int8_t)(hiw[j >> 2] >> sh);
+              const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
+              int cnew, inb, hq;
+              if (fa.fast) {
+                cnew = fa.fq.div_exact_fast(r - v[j]);
+                inb = fa.fq.balq(b1j + cnew, hq);
+              } else {
+                int rem;
+                cnew = fa.fq.divfloor(r - v[j], rem);
+                hq = fa.fq.divfloor(b1j + cnew, inb);
+                if (inb > (fa.q >> 1)) inb -= fa.q, ++hq;
+              }
+              in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
+              h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
+            }
+            *reinterpret_cast<uint4*>(sIn + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+            *reinterpret_cast<uint4*>(sH + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+          }
+        }
+        fence_async_smem();
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(barIn));
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 }  // namespace tc
 
 namespace {
@@ -377,5 +614,38 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
   DRZG_REQUIRE(e == cudaSuccess, std::string("tc_gemm launch: ") + cudaGetErrorString(e));
 }
 
+
+
+bool dixon_fused_ok(int nLp) { return nLp % 128 == 0 && nLp <= 256; }
+
+void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st) {
+  DRZG_REQUIRE(dixon_fused_ok(fa.nLp), "dixon_fused: system order must be 128 or 256");
+  DRZG_REQUIRE(fa.P % 64 == 0, "dixon_fused: state pitch must be a multiple of 64");
+  const int nt = fa.nLp / 128;
+  CUtensorMap mc = make_map(C, fa.nLp, fa.nLp, fa.nLp, 128);
+  CUtensorMap mj = make_map(Jd, fa.nLp, fa.nLp, fa.nLp, 128);
+  CUtensorMap mb = make_map(fa.Bg, fa.nLp, fa.P, fa.P, 128);  // plane 0: nLp K rows x P states
+  // kind::i8, D s32, B signed MN-major, N = 128, M = 128; A signed (Cq) / unsigned (Jp)
+  const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
+  const int smem = tc::fz::smem_bytes(nt);
+  static int attr_for = -1;
+  if (attr_for != smem) {
+    cudaFuncSetAttribute(tc::dixon_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_for = smem;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int nblk = (fa.N + tc::fz::NS - 1) / tc::fz::NS;
+  static const bool one_block = std::getenv("DRZG_FUSED_ONEBLOCK") != nullptr;  // debug: one block per CTA
+  tc::dixon_fused_kernel<<<one_block ? nblk : std::min(nblk, sms), tc::fz::THREADS, smem, st>>>(mc, mj, mb, idesc_c,
+                                                                                              idesc_j, fa);
+  cudaError_t e = cudaGetLastError();
+  DRZG_REQUIRE(e == cudaSuccess, std::string("dixon_fused launch: ") + cudaGetErrorString(e));
+}
 
 }  // namespace drzg

@@ -54,4 +54,18 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
                 const TcEpiArgs& epi, cudaStream_t st);
 
 
+
+// whole Dixon solve of every state of a batch in one launch, for systems of
+// order nLp in {128, 256}: Cq, Jp resident in shared memory, one CTA per
+// 128-state block (see dixon_fused_kernel)
+struct FusedArgs {
+  int nL = 0, nLp = 0, N = 0, P = 0, Ld = 0, q = 0;
+  FastQ fq;
+  int fast = 0;
+  const int8_t* Bg = nullptr;  // Ld x nLp x P gathered digits (plane 0 is read through TMA)
+  int8_t* Y = nullptr;         // Ld x nLp x P: y_k out
+};
+bool dixon_fused_ok(int nLp);
+void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st);
+
 }  // namespace drzg

@@ -84,8 +84,11 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   // live states stay below ~60% of a group's seeds (SURVEY 8a peaks), and a
   // group may use half of the free memory
   std::vector<std::vector<i64>> G(cols.size());
+  double td0 = 0;
   {
+    const double te0 = now_s();
     ReductionEngine eng(T, n, p, st);
+    if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] engine setup %.3f s\n", now_s() - te0);
     eng.clock.on = opt.profile;
     size_t fr = 0, tot = 0;
     DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
@@ -116,8 +119,10 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     }
     eng.clock.peak_live = eng.peak_live();
     out.clk = eng.clock;
+    td0 = now_s();
   }
   double t3 = now_s();
+  if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] engine teardown %.3f s\n", t3 - td0);
   out.t.device = t3 - t2;
 
   const int gsize = (int)mono_count(X.nv(), T.D - 1);
