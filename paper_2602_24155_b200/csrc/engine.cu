@@ -202,6 +202,9 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     }
   }
   sparse_carry_ = sparse_carry_ && use_tc_;
+  DRZG_REQUIRE((size_t)dev::kGatherStates * sidep_ <= 200 * 1024, "engine: side too large for the gather staging");
+  DRZG_CUDA(cudaFuncSetAttribute(dev::gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)std::min<size_t>((size_t)dev::kGatherStates * sidep_, 200 * 1024)));
   const char* fz = std::getenv("DRZG_FUSED");
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
   if (sparse_carry_) {
@@ -555,8 +558,9 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
     for (i64 y = 1; y <= kmax; ++y) {
       dev::StepArgs a = make_args(b0, By, (int)y);
       if (y == 1) {
-        dim3 gL((T.nL + dev::kGatherRows - 1) / dev::kGatherRows, (By + dev::kGatherStates - 1) / dev::kGatherStates);
-        timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gL, 256, 0, st_>>>(a); });
+        const int gb = (By + dev::kGatherStates - 1) / dev::kGatherStates;
+        const size_t gsm = (size_t)dev::kGatherStates * sidep_;
+        timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gb, dev::kGatherThreads, gsm, st_>>>(a); });
       }  // later steps: the previous epilogue already wrote this step's operand
       dixon(a);
       dim3 gE((By + 127) / 128, (T.side + dev::kEpiRows - 1) / dev::kEpiRows);

@@ -30,40 +30,74 @@ __device__ __forceinline__ int balmod(int x, int q) {
   return r;
 }
 
-// b = P_v w for 32 states x 256 rows per block, transposed through shared
-// memory so the Bg / IN / Cy writes are state-contiguous
-__global__ void __launch_bounds__(256) gather_kernel(StepArgs a) {
-  __shared__ int8_t tile[kGatherRows][kGatherStates + 4];
+// b = P_v w at the first step of a chunk, from the slot pool into the
+// state-contiguous operand Bg.  A block owns 32 states: for each digit plane
+// it stages the 32 states' plane (32 x sidep bytes, coalesced 16-byte loads
+// of each slot) in shared memory, then every thread assembles rows r: 32
+// bytes b[t][r][s0..s0+31] = w_s[t][gidx[v_s][r]] as two 16-byte stores.
+// (Digit 0 of a pool state is balanced, so b_0 is the first digit GEMM's
+// operand as it stands and the first carry's residual r_0.)
+constexpr int kGatherStates = 32, kGatherThreads = 512;
+__global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepArgs a) {
+  extern __shared__ int8_t planes[];  // kGatherStates x sidep
   __shared__ int vd[kGatherStates];
   __shared__ long long base[kGatherStates];
-  const int r0 = blockIdx.x * kGatherRows, s0 = blockIdx.y * kGatherStates;
-  const int tid = threadIdx.x, r = r0 + tid;
+  __shared__ int uniform_v;
+  const int s0 = blockIdx.x * kGatherStates, tid = threadIdx.x;
+  const int sidep = a.sidep, nL = a.nL;
   if (tid < kGatherStates) {
-    int s = s0 + tid;
+    const int s = s0 + tid;
     vd[tid] = s < a.B ? a.vdir[s] : -1;
-    base[tid] = s < a.B ? (long long)a.slot[s] * a.slot_stride : 0;
+    base[tid] = s < a.B ? (long long)a.slot[s] * a.slot_stride : -1;
   }
   __syncthreads();
-  int g[kGatherStates];
-#pragma unroll
-  for (int i = 0; i < kGatherStates; ++i) g[i] = (r < a.nL && vd[i] >= 0) ? a.gidx[(size_t)vd[i] * a.nL + r] : -1;
+  if (tid == 0) {
+    int u = vd[0];
+    for (int i = 1; i < kGatherStates; ++i)
+      if (vd[i] != u && vd[i] >= 0) u = -2;
+    uniform_v = u;
+  }
+  const size_t P = (size_t)a.P, plane = (size_t)a.nLp * P;
+  const int words = sidep / 16;
   for (int t = 0; t < a.Ld; ++t) {
-#pragma unroll
-    for (int i = 0; i < kGatherStates; ++i)
-      tile[tid][i] = g[i] >= 0 ? a.pool[base[i] + (size_t)t * a.sidep + g[i]] : (int8_t)0;
-    __syncthreads();
-    // 256 rows x 32 bytes = 2048 words; 8 per thread, row-contiguous
-    // (digit 0 of a pool state is balanced, so b_0 is the first digit GEMM's
-    // operand as it stands and the first carry's residual r_0)
-    for (int e = tid; e < kGatherRows * kGatherStates / 4; e += 256) {
-      int row = e >> 3, w = e & 7;
-      int rr = r0 + row;
-      if (rr >= a.nL) continue;
-      uint32_t word = *reinterpret_cast<const uint32_t*>(&tile[row][w * 4]);
-      size_t off = (size_t)rr * a.P + s0 + w * 4;
-      *reinterpret_cast<uint32_t*>(a.Bg + (size_t)t * a.nLp * a.P + off) = word;
+    __syncthreads();  // the previous plane is consumed (and uniform_v is set)
+    for (int e = tid; e < kGatherStates * words; e += kGatherThreads) {
+      const int i = e / words, w = e - i * words;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (base[i] >= 0) v = __ldg(reinterpret_cast<const uint4*>(a.pool + base[i] + (size_t)t * sidep) + w);
+      reinterpret_cast<uint4*>(planes + (size_t)i * sidep)[w] = v;
     }
     __syncthreads();
+    const int uv = uniform_v;
+    for (int r = tid; r < nL; r += kGatherThreads) {
+      uint32_t wd[8];
+      if (uv >= 0) {
+        const int g = __ldg(a.gidx + (size_t)uv * nL + r);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            word |= (uint32_t)(uint8_t)(g >= 0 ? planes[(size_t)(q * 4 + b) * sidep + g] : 0) << (8 * b);
+          wd[q] = word;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t word = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int i = q * 4 + b;
+            const int g = vd[i] >= 0 ? __ldg(a.gidx + (size_t)vd[i] * nL + r) : -1;
+            word |= (uint32_t)(uint8_t)(g >= 0 ? planes[(size_t)i * sidep + g] : 0) << (8 * b);
+          }
+          wd[q] = word;
+        }
+      }
+      uint4* dst = reinterpret_cast<uint4*>(a.Bg + (size_t)t * plane + (size_t)r * P + s0);
+      dst[0] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+      dst[1] = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+    }
   }
 }
 

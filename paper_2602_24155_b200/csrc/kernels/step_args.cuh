@@ -47,7 +47,6 @@ struct StepArgs {
   int8_t* Y;              // Ld x nLp x P
 };
 
-constexpr int kGatherRows = 256, kGatherStates = 32;
 constexpr int kFlushRows = 64, kFlushStates = 32;
 
 }  // namespace dev

@@ -93,6 +93,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ int balmod(int x, int q) {
   int r = x % q;
   if (r < 0) r += q;
@@ -341,7 +353,8 @@ __device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
 namespace fz {
 constexpr int NS = 128;      // states per block
 constexpr int TILE = 128 * 128;
-constexpr int THREADS = 384;
+constexpr int EPI_WARPS = 16;  // lane quarter x M tile x 64-state half
+constexpr int THREADS = 128 + 32 * EPI_WARPS;
 __host__ __device__ constexpr int smem_bytes(int nt) { return (2 * nt * nt + 3 * nt) * TILE + 1024 + 256; }
 }  // namespace fz
 
@@ -368,8 +381,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
   uint64_t* barB0 = bars + 1; // b_0 of the block loaded
   uint64_t* barD = bars + 2;  // digit product done
   uint64_t* barC = bars + 3;  // carry product done
-  uint64_t* barY = bars + 4;  // y_k drained (8 warps)
-  uint64_t* barIn = bars + 5; // in_{k+1}, h_{k+1} written (8 warps)
+  uint64_t* barY = bars + 4;  // y_k drained (every epilogue warp)
+  uint64_t* barIn = bars + 5; // in_{k+1}, h_{k+1} written (every epilogue warp)
   uint64_t* barFree = bars + 6;  // a block's last digit product done: sIn may be refilled
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -381,8 +394,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     mbar_init(smem_u32(barB0), 1);
     mbar_init(smem_u32(barD), 1);
     mbar_init(smem_u32(barC), 1);
-    mbar_init(smem_u32(barY), 8);
-    mbar_init(smem_u32(barIn), 8);
+    mbar_init(smem_u32(barY), fz::EPI_WARPS);
+    mbar_init(smem_u32(barIn), fz::EPI_WARPS);
     mbar_init(smem_u32(barFree), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
@@ -456,46 +469,54 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int e = warp - 4, quarter = e & 3, mt = e >> 2;
+    // epilogue warp e: TMEM lane quarter e % 4, M tile (e / 4) % 2, states
+    // [64 (e / 8), +64); every phase drains 64 accumulators per thread with
+    // two 32-column TMEM loads
+    const int e = warp - 4, quarter = e & 3, mt = (e >> 2) & 1, half = e >> 3;
     const int m = mt * 128 + quarter * 32 + lane;  // K row of in / y, M row of the products
     const bool active = mt < nt;
     const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
     const size_t P = (size_t)fa.P;
     int i = 0;
     for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
-      const int n0 = b * fz::NS;
+      const int n0 = b * fz::NS + half * 64;
       for (int k = 0; k < Ld; ++k) {
         const int d = i * Ld + k;
         const bool carry = k + 1 < Ld;
         // b_{k+1} for this thread's row: independent of the products, in flight early
-        uint4 b1[8];
+        uint4 b1[4];
         if (carry && active) {
           const int8_t* src = fa.Bg + ((size_t)(k + 1) * fa.nLp + m) * P + n0;
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch)
+          for (int ch = 0; ch < 4; ++ch)
             b1[ch] = n0 + ch * 16 < fa.N ? __ldg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
         }
         mbar_wait(smem_u32(barD), (uint32_t)(d & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
           int8_t* yg = fa.Y + ((size_t)k * fa.nLp + m) * P + n0;
-#pragma unroll 1
-          for (int ch = 0; ch < 8; ++ch) {
-            int v[16];
-            tmem_ld16(lanebase + (uint32_t)(mt * 128 + ch * 16), v);
-            uint32_t w4[4];
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint32_t word = 0;
+          for (int hh = 0; hh < 2; ++hh) {
+            int v[32];
+            tmem_ld32(lanebase + (uint32_t)(mt * 128 + half * 64 + hh * 32), v);
 #pragma unroll
-              for (int bb = 0; bb < 4; ++bb)
-                word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_fast(v[q4 * 4 + bb]) : fa.fq.bal(v[q4 * 4 + bb]))
-                        << (8 * bb);
-              w4[q4] = word;
+            for (int c2 = 0; c2 < 2; ++c2) {
+              const int ch = hh * 2 + c2;
+              uint32_t w4[4];
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                uint32_t word = 0;
+#pragma unroll
+                for (int bb = 0; bb < 4; ++bb) {
+                  const int x = v[c2 * 16 + q4 * 4 + bb];
+                  word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_fast(x) : fa.fq.bal(x)) << (8 * bb);
+                }
+                w4[q4] = word;
+              }
+              const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+              if (carry) *reinterpret_cast<uint4*>(sY + swz(m, half * 64 + ch * 16)) = y4;
+              if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
             }
-            const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            if (carry) *reinterpret_cast<uint4*>(sY + swz(m, ch * 16)) = y4;
-            if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
           }
         }
         fence_async_smem();
@@ -508,36 +529,41 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
-            int v[16];
-            tmem_ld16(lanebase + (uint32_t)(256 + mt * 128 + ch * 16), v);
-            const uint32_t off = swz(m, ch * 16);
-            const uint4 lo = *reinterpret_cast<const uint4*>(sIn + off);
-            const uint4 hi = k ? *reinterpret_cast<const uint4*>(sH + off) : make_uint4(0, 0, 0, 0);
-            const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
-            const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
-            const uint32_t b1w[4] = {b1[ch].x, b1[ch].y, b1[ch].z, b1[ch].w};
-            uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+          for (int hh = 0; hh < 2; ++hh) {
+            int v[32];
+            tmem_ld32(lanebase + (uint32_t)(256 + mt * 128 + half * 64 + hh * 32), v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int sh = 8 * (j & 3);
-              const int r = (int)(int8_t)(low[j >> 2] >> sh) + fa.q * (int)(int8_t)(hiw[j >> 2] >> sh);
-              const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
-              int cnew, inb, hq;
-              if (fa.fast) {
-                cnew = fa.fq.div_exact_fast(r - v[j]);
-                inb = fa.fq.balq(b1j + cnew, hq);
-              } else {
-                int rem;
-                cnew = fa.fq.divfloor(r - v[j], rem);
-                hq = fa.fq.divfloor(b1j + cnew, inb);
-                if (inb > (fa.q >> 1)) inb -= fa.q, ++hq;
+            for (int c2 = 0; c2 < 2; ++c2) {
+              const int ch = hh * 2 + c2;
+              const uint32_t off = swz(m, half * 64 + ch * 16);
+              const uint4 lo = *reinterpret_cast<const uint4*>(sIn + off);
+              const uint4 hi = k ? *reinterpret_cast<const uint4*>(sH + off) : make_uint4(0, 0, 0, 0);
+              const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
+              const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
+              const uint32_t b1w[4] = {b1[ch].x, b1[ch].y, b1[ch].z, b1[ch].w};
+              uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int sh = 8 * (j & 3);
+                const int r = (int)(int8_t)(low[j >> 2] >> sh) + fa.q * (int)(int8_t)(hiw[j >> 2] >> sh);
+                const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
+                const int x = v[c2 * 16 + j];
+                int cnew, inb, hq;
+                if (fa.fast) {
+                  cnew = fa.fq.div_exact_fast(r - x);
+                  inb = fa.fq.balq(b1j + cnew, hq);
+                } else {
+                  int rem;
+                  cnew = fa.fq.divfloor(r - x, rem);
+                  hq = fa.fq.divfloor(b1j + cnew, inb);
+                  if (inb > (fa.q >> 1)) inb -= fa.q, ++hq;
+                }
+                in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
+                h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
               }
-              in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
-              h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
+              *reinterpret_cast<uint4*>(sIn + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+              *reinterpret_cast<uint4*>(sH + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
             }
-            *reinterpret_cast<uint4*>(sIn + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
-            *reinterpret_cast<uint4*>(sH + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
           }
         }
         fence_async_smem();
