@@ -485,7 +485,26 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     f.fast = fast_ ? 1 : 0;
     f.Bg = Bg_.p;
     f.Y = Y_.p;
+    static int traces = std::getenv("DRZG_FUSED_TRACE") ? 6 : 0;
+    DevBuf<long long> tb;
+    if (traces > 0 && nb <= 2048) {
+      tb.alloc(4 * T.dp.Ld + 2);
+      DRZG_CUDA(cudaMemsetAsync(tb.p, 0, tb.n * 8, st_));
+      f.trace = tb.p;
+    }
     timed(&clock.gemm_ms, [&] { dixon_fused(C_.p, Jd_.p, f, st_); });
+    if (f.trace) {
+      --traces;
+      std::vector<long long> h(tb.n);
+      DRZG_CUDA(cudaMemcpyAsync(h.data(), tb.p, tb.n * 8, cudaMemcpyDeviceToHost, st_));
+      DRZG_CUDA(cudaStreamSynchronize(st_));
+      std::fprintf(stderr, "[drzg] fused trace N=%d (us from epilogue start):", nb);
+      for (int k = 0; k < T.dp.Ld; ++k)
+        std::fprintf(stderr, " k%d[D %.1f Y %.1f C %.1f I %.1f]", k, (h[1 + 4 * k] - h[0]) / 1e3,
+                     (h[2 + 4 * k] - h[0]) / 1e3, h[3 + 4 * k] ? (h[3 + 4 * k] - h[0]) / 1e3 : 0.0,
+                     h[4 + 4 * k] ? (h[4 + 4 * k] - h[0]) / 1e3 : 0.0);
+      std::fprintf(stderr, "\n");
+    }
     ++clock.gemm_launches;
     clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * nb;
     clock.carry_macs += (double)(T.dp.Ld - 1) * T.nL * T.nL * nb;

@@ -477,6 +477,15 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     const bool active = mt < nt;
     const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
     const size_t P = (size_t)fa.P;
+    const bool tr = fa.trace && blockIdx.x == 0 && threadIdx.x == 128;
+    auto stamp = [&](int slot) {
+      if (tr) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        fa.trace[slot] = (long long)t;
+      }
+    };
+    stamp(0);
     int i = 0;
     for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
       const int n0 = b * fz::NS + half * 64;
@@ -492,6 +501,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
             b1[ch] = n0 + ch * 16 < fa.N ? __ldg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
         }
         mbar_wait(smem_u32(barD), (uint32_t)(d & 1));
+        if (i == 0) stamp(1 + 4 * k);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
           int8_t* yg = fa.Y + ((size_t)k * fa.nLp + m) * P + n0;
@@ -523,9 +533,11 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(barY));
+        if (i == 0) stamp(2 + 4 * k);
         if (!carry) continue;
         if (k == 0) mbar_wait(smem_u32(barB0), (uint32_t)(i & 1));  // b_0 (TMA) is r_0
         mbar_wait(smem_u32(barC), (uint32_t)((i * (Ld - 1) + k) & 1));
+        if (i == 0) stamp(3 + 4 * k);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
 #pragma unroll
@@ -570,6 +582,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(barIn));
+        if (i == 0) stamp(4 + 4 * k);
       }
     }
   }

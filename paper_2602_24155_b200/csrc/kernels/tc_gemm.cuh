@@ -64,6 +64,7 @@ struct FusedArgs {
   int fast = 0;
   const int8_t* Bg = nullptr;  // Ld x nLp x P gathered digits (plane 0 is read through TMA)
   int8_t* Y = nullptr;         // Ld x nLp x P: y_k out
+  long long* trace = nullptr;  // debug: %globaltimer stamps of CTA 0's first epilogue thread
 };
 bool dixon_fused_ok(int nLp);
 void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st);
