@@ -19,6 +19,7 @@ struct FastQ {
   long long off = 0;  // q * 2^30
   unsigned m32 = 0;   // ceil(2^32 / q)
   int k22 = 0;        // ceil(2^22 / q)
+  unsigned qinv = 0;  // q^{-1} mod 2^32 (q odd): exact division is one multiply
   static FastQ make(int q) {
     FastQ f;
     f.q = q;
@@ -26,6 +27,9 @@ struct FastQ {
     f.off = (long long)q << 30;
     f.m32 = (unsigned)(((1ull << 32) + (unsigned long long)q - 1) / (unsigned long long)q);
     f.k22 = (int)(((1 << 22) + q - 1) / q);
+    unsigned inv = 1;  // Newton iteration for the inverse mod 2^32 (q odd)
+    for (int i = 0; i < 5; ++i) inv *= 2u - (unsigned)q * inv;
+    f.qinv = (q & 1) ? inv : 0u;
     return f;
   }
 #ifdef __CUDACC__
@@ -54,6 +58,17 @@ struct FastQ {
   __device__ __forceinline__ int bal_fast(int x) const {
     int t;
     return balq(x, t);
+  }
+  // x / q for x divisible by q (any int32 x, q odd): one multiply
+  __device__ __forceinline__ int div_exact_inv(int x) const { return (int)((unsigned)x * qinv); }
+  // balanced digit d = x - q t with |d| <= q/2 and its quotient t, for
+  // |x| < 2^22, q odd: one add, a multiply-high and a multiply-add
+  __device__ __forceinline__ int bal_split(int x, int& t) const {
+    const int h = q >> 1;
+    const unsigned xp = (unsigned)(x + h + q * k22);
+    const int tq = (int)__umulhi(xp, m32);
+    t = tq - k22;
+    return (int)xp - tq * q - h;
   }
   // x / q for x divisible by q, |x| < 2^22
   __device__ __forceinline__ int div_exact_fast(int x) const {

@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
             int cnew, inb, hq;
             if (epi.fast) {
-              cnew = epi.fq.div_exact_fast(r - v[j]);
-              inb = epi.fq.balq(b1j + cnew, hq);
+              cnew = epi.fq.div_exact_inv(r - v[j]);
+              inb = epi.fq.bal_split(b1j + cnew, hq);
             } else {
               int rem;
               cnew = epi.fq.divfloor(r - v[j], rem);  // exact
@@ -304,12 +304,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else if (epi.b_mn && epi.mode == (int)TcEpilogue::digit) {
           // Y[k][m][n0..n0+15]: one 16-byte store
           uint32_t w4[4];
+          int tdrop;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
             uint32_t word = 0;
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-              word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_fast(v[q4 * 4 + b]) : epi.fq.bal(v[q4 * 4 + b]))
+              word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_split(v[q4 * 4 + b], tdrop) : epi.fq.bal(v[q4 * 4 + b]))
                       << (8 * b);
             w4[q4] = word;
           }
@@ -519,7 +520,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
 #pragma unroll
                 for (int bb = 0; bb < 4; ++bb) {
                   const int x = v[c2 * 16 + q4 * 4 + bb];
-                  word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_fast(x) : fa.fq.bal(x)) << (8 * bb);
+                  int tdrop;
+                  word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_split(x, tdrop) : fa.fq.bal(x)) << (8 * bb);
                 }
                 w4[q4] = word;
               }
@@ -562,8 +564,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
                 const int x = v[c2 * 16 + j];
                 int cnew, inb, hq;
                 if (fa.fast) {
-                  cnew = fa.fq.div_exact_fast(r - x);
-                  inb = fa.fq.balq(b1j + cnew, hq);
+                  cnew = fa.fq.div_exact_inv(r - x);
+                  inb = fa.fq.bal_split(b1j + cnew, hq);
                 } else {
                   int rem;
                   cnew = fa.fq.divfloor(r - x, rem);
