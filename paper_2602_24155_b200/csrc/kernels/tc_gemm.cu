@@ -121,6 +121,13 @@ __device__ __forceinline__ int balmod(int x, int q) {
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 
+// M tile of persistent tile t: the M tiles of one N column are a
+// contiguous run of t (so concurrently running CTAs share the B tile in L2),
+// rotated by the column index so that a CTA, which sees t = c + grid * i,
+// meets every M tile over its rounds (with block-sparse K the M tiles differ
+// in cost; a fixed t % mt would pin each CTA to one cost class)
+__device__ __forceinline__ int tile_m(int t, int mt) { return (t + t / mt) % mt; }
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -171,7 +178,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       int it = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int mi = t % mt;
+        const int mi = tile_m(t, mt);
         const int m0 = mi * BM, n0 = (t / mt) * BN;
         const int kb0 = epi.kb_ptr ? __ldg(epi.kb_ptr + mi) : 0;
         const int nkt = epi.kb_ptr ? __ldg(epi.kb_ptr + mi + 1) - kb0 : nk;
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        const int mi = t % mt;
+        const int mi = tile_m(t, mt);
         const int nkt = epi.kb_ptr ? __ldg(epi.kb_ptr + mi + 1) - __ldg(epi.kb_ptr + mi) : nk;
         for (int kb = 0; kb < nkt; ++kb, ++it) {
           int s = it % STAGES;
@@ -222,7 +229,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int quarter = e & 3, half = e >> 2;
     int i = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-      const int m0 = (t % mt) * BM, n0 = (t / mt) * BN;
+      const int m0 = tile_m(t, mt) * BM, n0 = (t / mt) * BN;
       const int acc = i & 1;
       const int m = m0 + quarter * 32 + lane;
       const bool mok = m < epi.M;
