@@ -130,7 +130,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   }
   DRZG_REQUIRE(T.dp.Ld <= dev::kLdMax, "engine: too many digit planes");
   // small systems pad to whole 128-row tiles (the one-launch Dixon kernel)
-  nLp_ = T.nL <= 256 ? round_up(T.nL, 128) : round_up(T.nL, 64);
+  nLp_ = round_up(T.nL, 128);  // whole 128-row tiles (the one-launch kernels)
   sidep_ = round_up(T.side, 16);
   slot_stride_ = (long long)T.dp.Ld * sidep_;
   gsize_ = (int)mono_count(T.nv, T.D - 1);
@@ -207,6 +207,8 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
                                  (int)std::min<size_t>((size_t)dev::kGatherStates * sidep_, 200 * 1024)));
   const char* fz = std::getenv("DRZG_FUSED");
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
+  const char* fl = std::getenv("DRZG_FLOW");
+  flow_ = use_tc_ && sparse_carry_ && !fused_ && nLp_ % 128 == 0 && !(fl && std::string(fl) == "0");
   if (sparse_carry_) {
     kb_ptr_.upload(ord.kb_ptr, st_);
     kb_idx_.upload(ord.kb_idx, st_);
@@ -508,6 +510,35 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     ++clock.gemm_launches;
     clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * nb;
     clock.carry_macs += (double)(T.dp.Ld - 1) * T.nL * T.nL * nb;
+    return;
+  }
+  if (flow_) {
+    // larger systems: every digit and carry product of the batch in one
+    // persistent dataflow launch
+    FlowArgs f;
+    TcEpiArgs& e = f.epi;
+    e.M = T.nL;
+    e.N = nb;
+    e.q = T.dp.q;
+    e.fq = FastQ::make(T.dp.q);
+    e.fast = fast_ ? 1 : 0;
+    e.Ld = T.dp.Ld;
+    e.nLp = nLp_;
+    e.nL = T.nL;
+    e.P = bcap_;
+    e.Y = Y_.p;
+    e.Bg = Bg_.p;
+    e.H = H_.p;
+    e.IN = IN_.p;
+    e.kb_ptr = kb_ptr_.p;
+    e.kb_idx = kb_idx_.p;
+    const size_t nctr = (size_t)(2 * T.dp.Ld - 1) * ((nb + 255) / 256);
+    flow_ctr_.alloc(std::max<size_t>(nctr, (size_t)(2 * T.dp.Ld - 1) * ((bcap_ + 255) / 256)));
+    f.counters = flow_ctr_.p;
+    timed(&clock.gemm_ms, [&] { dixon_flow(C_.p, Jd_.p, f, st_); });
+    ++clock.gemm_launches;
+    clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * nb;
+    clock.carry_macs += (double)(T.dp.Ld - 1) * kblocks_ * 128 * 128 * nb;
     return;
   }
   for (int k = 0; k < T.dp.Ld; ++k) {

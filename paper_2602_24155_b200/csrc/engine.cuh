@@ -189,6 +189,8 @@ class ReductionEngine {
   bool fast_ = false;   // fp32-reciprocal residues (host-checked operand bound)
   bool sparse_carry_ = false;  // carry GEMM over the nonzero K blocks of Jp only
   bool fused_ = false;         // whole solve in one launch (nLp <= 256; DRZG_FUSED=0 disables)
+  bool flow_ = false;          // whole solve as one dataflow launch (larger systems; DRZG_FLOW=0 disables)
+  DevBuf<int> flow_ctr_;       // its per-column phase counters
   long long kblocks_ = 0;      // nonzero 128 x 128 blocks of Jp (system order)
   DevBuf<int> kb_ptr_, kb_idx_;
   DevBuf<int> ginv_;

@@ -132,6 +132,100 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Dixon carry epilogue of one tile row segment: c = (r_k - Jp y_k) / q
+// (exact), r_{k+1} = b_{k+1} + c, stored as in_{k+1} = bal(r_{k+1}) (the
+// next digit product's operand, in place over in_k) and its quotient h_{k+1}
+// (|h| <= 4), with r_k = b_0 (k = 0) or in_k + q h_k.  Software-pipelined:
+// the 16-byte loads of chunk c+16 are in flight while chunk c is computed.
+// COHERENT: in_k / h_k were written by other CTAs of the same launch (the
+// dataflow kernel), so they are read through L2 (ld.global.cg), not the
+// non-coherent read-only path.
+__device__ __forceinline__ void epi_carry_prefetch(const TcEpiArgs& epi, int k, int m, bool mok, int nb) {
+  if (!mok || nb >= epi.N) return;
+  const size_t P = (size_t)epi.P;
+  const int8_t* rlo = (k ? epi.IN : epi.Bg) + (size_t)m * P;
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(rlo + nb));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(epi.Bg + ((size_t)(k + 1) * epi.nLp + m) * P + nb));
+  if (k) asm volatile("prefetch.global.L2 [%0];" ::"l"(epi.H + (size_t)m * P + nb));
+}
+
+template <bool COHERENT>
+__device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
+                                               int cend, uint32_t tb) {
+  const size_t P = (size_t)epi.P;
+  const int8_t* rlo = (k ? epi.IN : epi.Bg) + (size_t)m * P;  // in_k, or b_0
+  const int8_t* rhi = epi.H + (size_t)m * P;                    // h_k (k > 0)
+  const int8_t* bk1p = epi.Bg + ((size_t)(k + 1) * epi.nLp + m) * P;
+  const bool wh = k + 2 < epi.Ld;  // a later carry reads h_{k+1}
+  auto ld = [&](const int8_t* p) {
+    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
+  };
+  uint4 nlo = make_uint4(0, 0, 0, 0), nhi = nlo, nb1 = nlo;
+  auto fetch = [&](int c) {
+    const int nb = n0 + c;
+    if (!mok || nb >= epi.N) return;
+    nlo = ld(rlo + nb);
+    nb1 = __ldg(reinterpret_cast<const uint4*>(bk1p + nb));
+    if (k) nhi = ld(rhi + nb);
+  };
+  fetch(cbeg);
+  for (int c = cbeg; c < cend; c += 16) {
+    const uint4 lo = nlo, hi = nhi, b1 = nb1;
+    if (c + 16 < cend) fetch(c + 16);
+    int v[16];
+    tmem_ld16(tb + (uint32_t)c, v);
+    const int nb = n0 + c;
+    if (!mok || nb >= epi.N) continue;
+    const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
+    const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
+    const uint32_t b1w[4] = {b1.x, b1.y, b1.z, b1.w};
+    uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int sh = 8 * (j & 3);
+      const int r = (int)(int8_t)(low[j >> 2] >> sh) + (k ? epi.q * (int)(int8_t)(hiw[j >> 2] >> sh) : 0);
+      const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
+      int cnew, inb, hq;
+      if (epi.fast) {
+        cnew = epi.fq.div_exact_inv(r - v[j]);
+        inb = epi.fq.bal_split(b1j + cnew, hq);
+      } else {
+        int rem;
+        cnew = epi.fq.divfloor(r - v[j], rem);  // exact
+        hq = epi.fq.divfloor(b1j + cnew, inb);
+        if (inb > (epi.q >> 1)) inb -= epi.q, ++hq;
+      }
+      in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
+      h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
+    }
+    *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+    if (wh) *reinterpret_cast<uint4*>(epi.H + (size_t)m * P + nb) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+  }
+}
+
+// Dixon digit epilogue: Y[k][m][n0 + c ..] = bal(D), one 16-byte store per chunk
+__device__ __forceinline__ void epi_digit_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
+                                               int cend, uint32_t tb) {
+  for (int c = cbeg; c < cend; c += 16) {
+    int v[16];
+    tmem_ld16(tb + (uint32_t)c, v);
+    const int nb = n0 + c;
+    if (!mok || nb >= epi.N) continue;
+    uint32_t w4[4];
+    int tdrop;
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_split(v[q4 * 4 + b], tdrop) : epi.fq.bal(v[q4 * 4 + b]))
+                << (8 * b);
+      w4[q4] = word;
+    }
+    *reinterpret_cast<uint4*>(epi.Y + ((size_t)k * epi.nLp + m) * epi.P + nb) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K,
                 uint32_t idesc, TcEpiArgs epi) {
@@ -233,102 +327,204 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int acc = i & 1;
       const int m = m0 + quarter * 32 + lane;
       const bool mok = m < epi.M;
-      // carry operands: r_k = b_0 (k = 0) or in_k + q h_k, and b_{k+1}
-      const size_t P = (size_t)epi.P;
       const bool carry = epi.b_mn && epi.mode == (int)TcEpilogue::carry;
-      const int8_t* rlo = epi.k ? epi.IN + (size_t)m * P : epi.Bg + (size_t)m * P;  // in_k, or b_0
-      const int8_t* rhi = epi.H + (size_t)m * P;                                      // h_k (k > 0)
-      const int8_t* bk1p = epi.Bg + ((size_t)(epi.k + 1) * epi.nLp + m) * P;
-      if (carry && mok && n0 + half * (BN / 2) < epi.N) {
-        // the carry inputs do not depend on the accumulator: pull this
-        // thread's row segments into L2 while the mainloop runs
-        const size_t nb = (size_t)(n0 + half * (BN / 2));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(rlo + nb));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(bk1p + nb));
-        if (epi.k) asm volatile("prefetch.global.L2 [%0];" ::"l"(rhi + nb));
-      }
+      if (carry) epi_carry_prefetch(epi, epi.k, m, mok, n0 + half * (BN / 2));
       mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
       if (carry) {
-        // c = (r_k - Jp y_k) / q (exact), r_{k+1} = b_{k+1} + c, stored as
-        // in_{k+1} = bal(r_{k+1}) (the next digit GEMM's operand, in place
-        // over in_k) and its quotient h_{k+1} (|h| <= 4); software-pipelined:
-        // the 16-byte loads of chunk c+16 are in flight while chunk c is computed
-        const bool wh = epi.k + 2 < epi.Ld;  // a later carry reads h_{k+1}
-        const int cbeg = half * (BN / 2), cend = (half + 1) * (BN / 2);
-        uint4 nlo = make_uint4(0, 0, 0, 0), nhi = nlo, nb1 = nlo;
-        auto fetch = [&](int c) {
-          const int nb = n0 + c;
-          if (!mok || nb >= epi.N) return;
-          nlo = __ldg(reinterpret_cast<const uint4*>(rlo + nb));
-          nb1 = __ldg(reinterpret_cast<const uint4*>(bk1p + nb));
-          if (epi.k) nhi = __ldg(reinterpret_cast<const uint4*>(rhi + nb));
-        };
-        fetch(cbeg);
-        for (int c = cbeg; c < cend; c += 16) {
-          const uint4 lo = nlo, hi = nhi, b1 = nb1;
-          if (c + 16 < cend) fetch(c + 16);
+        epi_carry_tile<false>(epi, epi.k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      } else if (epi.b_mn && epi.mode == (int)TcEpilogue::digit) {
+        epi_digit_tile(epi, epi.k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      } else {
+        for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
           int v[16];
-          tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
+          tmem_ld16(tb + (uint32_t)c, v);
           const int nb = n0 + c;
           if (!mok || nb >= epi.N) continue;
-          const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
-          const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
-          const uint32_t b1w[4] = {b1.x, b1.y, b1.z, b1.w};
-          uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int sh = 8 * (j & 3);
-            const int r = (int)(int8_t)(low[j >> 2] >> sh) + (epi.k ? epi.q * (int)(int8_t)(hiw[j >> 2] >> sh) : 0);
-            const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
-            int cnew, inb, hq;
-            if (epi.fast) {
-              cnew = epi.fq.div_exact_inv(r - v[j]);
-              inb = epi.fq.bal_split(b1j + cnew, hq);
-            } else {
-              int rem;
-              cnew = epi.fq.divfloor(r - v[j], rem);  // exact
-              hq = epi.fq.divfloor(b1j + cnew, inb);
-              if (inb > (epi.q >> 1)) inb -= epi.q, ++hq;
-            }
-            in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
-            h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
-          }
-          *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
-          if (wh) *reinterpret_cast<uint4*>(epi.H + (size_t)m * P + nb) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
-        }
-      } else
-      for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
-        int v[16];
-        tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), v);
-        const int nb = n0 + c;
-        if (!mok || nb >= epi.N) continue;
-        const int cnt = min(16, epi.N - nb);
-        if (epi.mode == (int)TcEpilogue::raw) {
+          const int cnt = min(16, epi.N - nb);
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             if (j < cnt) epi.out[(size_t)(nb + j) * epi.M + m] = v[j];
-        } else if (epi.b_mn && epi.mode == (int)TcEpilogue::digit) {
-          // Y[k][m][n0..n0+15]: one 16-byte store
-          uint32_t w4[4];
-          int tdrop;
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_split(v[q4 * 4 + b], tdrop) : epi.fq.bal(v[q4 * 4 + b]))
-                      << (8 * b);
-            w4[q4] = word;
-          }
-          *reinterpret_cast<uint4*>(epi.Y + ((size_t)epi.k * epi.nLp + m) * epi.P + nb) =
-              make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
       }
       // all of this warp's TMEM reads of buffer `acc` are complete
       __syncwarp();
       asm volatile("tcgen05.fence::before_thread_sync;");
       if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+}
+
+// ---------------------------------------------------------------------------
+// The whole Dixon solve of a batch as ONE persistent dataflow launch (nLp >
+// 256).  Tiles are (phase p, 256-state column, 128-row M tile): phase 2k is
+// the digit product of digit k, phase 2k+1 the block-sparse carry of digit k.
+// A tile may start when every M tile of phase p-1 of its column is done
+// (global counters, acquire/release); tiles are ordered group by group
+// (G columns, all phases, all M tiles) so the dependencies of a tile were
+// issued ~G*mt tiles earlier and are normally complete.  Digit tiles keep
+// the tensor pipe busy while carry tiles (short K loop, memory-heavy
+// epilogue) interleave with them on every SM, instead of the two
+// alternating as separate launches.  No deadlock: each CTA takes its tiles
+// in increasing order and a tile depends only on earlier tiles.
+struct FlowTile {
+  int p, col, mi;
+};
+__device__ __forceinline__ FlowTile flow_tile(int t, int mt, int ncol, int G, int nph) {
+  const int TG = nph * G * mt;
+  const int gi = t / TG;
+  const int r = t - gi * TG;
+  const int Gc = min(G, ncol - gi * G);
+  const int per = Gc * mt;
+  FlowTile f;
+  f.p = r / per;
+  const int r2 = r - f.p * per;
+  const int j = r2 / mt;
+  f.col = gi * G + j;
+  f.mi = (r2 - j * mt + j + f.p) % mt;  // rotate: a CTA meets every M tile
+  return f;
+}
+
+__device__ __forceinline__ void flow_wait(const int* ctr, int target) {
+  for (uint32_t spin = 0;; ++spin) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    if (v >= target) break;
+    __nanosleep(64);
+    if (spin > (1u << 26)) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    dixon_flow_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
+                      const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmIn,
+                      const __grid_constant__ CUtensorMap tmY, FlowArgs fa) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + STAGES * A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;       // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  const TcEpiArgs& epi = fa.epi;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = epi.nLp / BK;
+  const int mt = (epi.M + BM - 1) / BM;
+  const int nph = 2 * epi.Ld - 1;
+  const int tiles = nph * fa.ncol * mt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmJ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB0) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmIn) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmY) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const FlowTile f = flow_tile(t, mt, fa.ncol, fa.G, nph);
+        const int k = f.p >> 1;
+        const bool digit = !(f.p & 1);
+        const int m0 = f.mi * BM, n0 = f.col * BN;
+        if (f.p) flow_wait(fa.counters + (size_t)(f.p - 1) * fa.ncol + f.col, mt * EPI_WARPS);
+        const int kb0 = digit ? 0 : __ldg(epi.kb_ptr + f.mi);
+        const int nkt = digit ? nk : __ldg(epi.kb_ptr + f.mi + 1) - kb0;
+        const CUtensorMap* ma = digit ? &tmC : &tmJ;
+        const CUtensorMap* mb = digit ? (k ? &tmIn : &tmB0) : &tmY;
+        const int rowoff = digit ? 0 : k * epi.nLp;
+        for (int kb = 0; kb < nkt; ++kb, ++it) {
+          const int kc = (digit ? kb : __ldg(epi.kb_idx + kb0 + kb)) * BK;
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&empty[s]), ((it / STAGES) & 1) ^ 1);
+          const uint32_t fb = smem_u32(&full[s]);
+          mbar_expect_tx(fb, A_BYTES + B_BYTES);
+          tma_load_2d(smem_u32(sA + s * A_BYTES), ma, fb, kc, m0);
+          tma_load_2d(smem_u32(sB + s * B_BYTES), mb, fb, n0, rowoff + kc);
+          tma_load_2d(smem_u32(sB + s * B_BYTES + BN / 2 * BK), mb, fb, n0 + BN / 2, rowoff + kc);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+        const FlowTile f = flow_tile(t, mt, fa.ncol, fa.G, nph);
+        const bool digit = !(f.p & 1);
+        const int acc = i & 1;
+        mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        const int nkt = digit ? nk : __ldg(epi.kb_ptr + f.mi + 1) - __ldg(epi.kb_ptr + f.mi);
+        const uint32_t idesc = digit ? fa.idesc_d : fa.idesc_c;
+        for (int kb = 0; kb < nkt; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8(d, sw128_desc(a0 + kk * 32), sw128_mn_desc(b0 + kk * 4096), idesc, (kb | kk) != 0);
+          mma_commit(smem_u32(&empty[s]));
+        }
+        mma_commit(smem_u32(&tfull[acc]));
+      }
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    const int quarter = e & 3, half = e >> 2;
+    int i = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+      const FlowTile f = flow_tile(t, mt, fa.ncol, fa.G, nph);
+      const int k = f.p >> 1;
+      const bool digit = !(f.p & 1);
+      const int m0 = f.mi * BM, n0 = f.col * BN;
+      const int acc = i & 1;
+      const int m = m0 + quarter * 32 + lane;
+      const bool mok = m < epi.M;
+      if (!digit) epi_carry_prefetch(epi, k, m, mok, n0 + half * (BN / 2));
+      mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+      if (digit)
+        epi_digit_tile(epi, k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      else
+        epi_carry_tile<true>(epi, k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      __syncwarp();
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+      // publish: this warp's rows of the tile are in global memory
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(fa.counters + (size_t)f.p * fa.ncol + f.col, 1);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -694,6 +890,49 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
                                                                                               idesc_j, fa);
   cudaError_t e = cudaGetLastError();
   DRZG_REQUIRE(e == cudaSuccess, std::string("dixon_fused launch: ") + cudaGetErrorString(e));
+}
+
+
+void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st) {
+  TcEpiArgs& e = fa.epi;
+  DRZG_REQUIRE(e.kb_ptr && e.kb_idx, "dixon_flow: the carry needs its K-block lists");
+  DRZG_REQUIRE(e.nLp % tc::BK == 0 && e.P % 64 == 0, "dixon_flow: system order / pitch alignment");
+  e.b_mn = 1;
+  fa.ncol = (e.N + tc::BN - 1) / tc::BN;
+  CUtensorMap mc = make_map(C, e.nLp, e.nLp, e.nLp, tc::BM);
+  CUtensorMap mj = make_map(Jd, e.nLp, e.nLp, e.nLp, tc::BM);
+  // MN-major B operands: K rows x P states, box 128 states x 128 rows
+  CUtensorMap mb0 = make_map(e.Bg, e.nLp, e.P, e.P, tc::BK);             // b_0 = in_0
+  CUtensorMap min_ = make_map(e.IN, e.nLp, e.P, e.P, tc::BK);            // in_k
+  CUtensorMap my = make_map(e.Y, e.Ld * e.nLp, e.P, e.P, tc::BK);        // y_k at row k * nLp
+  const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(tc::BN >> 3) << 17) |
+                          ((uint32_t)(tc::BM >> 4) << 24);
+  fa.idesc_d = common | (1u << 7);  // Cq signed
+  fa.idesc_c = common;              // Jp unsigned
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc::dixon_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    attr = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int mt = (e.M + tc::BM - 1) / tc::BM;
+  const int nph = 2 * e.Ld - 1;
+  // columns per group: enough tiles per phase (~2 rounds of the grid) that a
+  // tile's dependencies were issued a round earlier
+  fa.G = std::max(1, std::min(fa.ncol, (2 * sms + mt - 1) / mt));
+  {
+    cudaError_t me = cudaMemsetAsync(fa.counters, 0, sizeof(int) * (size_t)nph * fa.ncol, st);
+    DRZG_REQUIRE(me == cudaSuccess, std::string("dixon_flow counters: ") + cudaGetErrorString(me));
+  }
+  const int tiles = nph * fa.ncol * mt;
+  tc::dixon_flow_kernel<<<std::min(tiles, sms), tc::THREADS, tc::SMEM_BYTES, st>>>(mc, mj, mb0, min_, my, fa);
+  cudaError_t err = cudaGetLastError();
+  DRZG_REQUIRE(err == cudaSuccess, std::string("dixon_flow launch: ") + cudaGetErrorString(err));
 }
 
 }  // namespace drzg

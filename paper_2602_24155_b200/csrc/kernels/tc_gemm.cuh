@@ -69,4 +69,16 @@ struct FusedArgs {
 bool dixon_fused_ok(int nLp);
 void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st);
 
+
+// whole Dixon solve of a batch in one persistent dataflow launch (nLp > 256,
+// block-sparse carry): digit and carry tiles of all Ld digits, ordered by
+// per-column phase counters (see dixon_flow_kernel)
+struct FlowArgs {
+  TcEpiArgs epi;             // M, N, P, q, fq, fast, Ld, nLp, nL, Bg, IN, H, Y, kb_ptr, kb_idx
+  int ncol = 0, G = 0;       // 256-state columns, columns per group (set by dixon_flow)
+  int* counters = nullptr;   // (2 Ld - 1) x ncol ints of device scratch
+  uint32_t idesc_d = 0, idesc_c = 0;
+};
+void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st);
+
 }  // namespace drzg
