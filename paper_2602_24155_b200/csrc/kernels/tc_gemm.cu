@@ -152,6 +152,7 @@ __device__ __forceinline__ void epi_carry_prefetch(const TcEpiArgs& epi, int k, 
 template <bool COHERENT>
 __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
                                                int cend, uint32_t tb) {
+  // 32 states per step: every global access is a whole 32-byte sector
   const size_t P = (size_t)epi.P;
   const int8_t* rlo = (k ? epi.IN : epi.Bg) + (size_t)m * P;  // in_k, or b_0
   const int8_t* rhi = epi.H + (size_t)m * P;                    // h_k (k > 0)
@@ -160,69 +161,91 @@ __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int 
   auto ld = [&](const int8_t* p) {
     return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
   };
-  uint4 nlo = make_uint4(0, 0, 0, 0), nhi = nlo, nb1 = nlo;
+  uint4 nlo[2], nhi[2], nb1[2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x) nlo[x] = nhi[x] = nb1[x] = make_uint4(0, 0, 0, 0);
   auto fetch = [&](int c) {
     const int nb = n0 + c;
     if (!mok || nb >= epi.N) return;
-    nlo = ld(rlo + nb);
-    nb1 = __ldg(reinterpret_cast<const uint4*>(bk1p + nb));
-    if (k) nhi = ld(rhi + nb);
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      nlo[x] = ld(rlo + nb + 16 * x);
+      nb1[x] = __ldg(reinterpret_cast<const uint4*>(bk1p + nb + 16 * x));
+      if (k) nhi[x] = ld(rhi + nb + 16 * x);
+    }
   };
   fetch(cbeg);
-  for (int c = cbeg; c < cend; c += 16) {
-    const uint4 lo = nlo, hi = nhi, b1 = nb1;
-    if (c + 16 < cend) fetch(c + 16);
-    int v[16];
-    tmem_ld16(tb + (uint32_t)c, v);
+  for (int c = cbeg; c < cend; c += 32) {
+    uint4 lo[2], hi[2], b1[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) lo[x] = nlo[x], hi[x] = nhi[x], b1[x] = nb1[x];
+    if (c + 32 < cend) fetch(c + 32);
+    int v[32];
+    tmem_ld32(tb + (uint32_t)c, v);
     const int nb = n0 + c;
     if (!mok || nb >= epi.N) continue;
-    const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
-    const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
-    const uint32_t b1w[4] = {b1.x, b1.y, b1.z, b1.w};
-    uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+    uint4 o_in[2], o_h[2];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int sh = 8 * (j & 3);
-      const int r = (int)(int8_t)(low[j >> 2] >> sh) + (k ? epi.q * (int)(int8_t)(hiw[j >> 2] >> sh) : 0);
-      const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
-      int cnew, inb, hq;
-      if (epi.fast) {
-        cnew = epi.fq.div_exact_inv(r - v[j]);
-        inb = epi.fq.bal_split(b1j + cnew, hq);
-      } else {
-        int rem;
-        cnew = epi.fq.divfloor(r - v[j], rem);  // exact
-        hq = epi.fq.divfloor(b1j + cnew, inb);
-        if (inb > (epi.q >> 1)) inb -= epi.q, ++hq;
+    for (int x = 0; x < 2; ++x) {
+      const uint32_t low[4] = {lo[x].x, lo[x].y, lo[x].z, lo[x].w};
+      const uint32_t hiw[4] = {hi[x].x, hi[x].y, hi[x].z, hi[x].w};
+      const uint32_t b1w[4] = {b1[x].x, b1[x].y, b1[x].z, b1[x].w};
+      uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int sh = 8 * (j & 3);
+        const int r = (int)(int8_t)(low[j >> 2] >> sh) + (k ? epi.q * (int)(int8_t)(hiw[j >> 2] >> sh) : 0);
+        const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
+        const int acc = v[16 * x + j];
+        int cnew, inb, hq;
+        if (epi.fast) {
+          cnew = epi.fq.div_exact_inv(r - acc);
+          inb = epi.fq.bal_split(b1j + cnew, hq);
+        } else {
+          int rem;
+          cnew = epi.fq.divfloor(r - acc, rem);  // exact
+          hq = epi.fq.divfloor(b1j + cnew, inb);
+          if (inb > (epi.q >> 1)) inb -= epi.q, ++hq;
+        }
+        in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
+        h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
       }
-      in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
-      h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
+      o_in[x] = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+      o_h[x] = make_uint4(h4[0], h4[1], h4[2], h4[3]);
     }
-    *reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
-    if (wh) *reinterpret_cast<uint4*>(epi.H + (size_t)m * P + nb) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+    uint4* di = reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb);
+    di[0] = o_in[0];
+    di[1] = o_in[1];
+    if (wh) {
+      uint4* dh = reinterpret_cast<uint4*>(epi.H + (size_t)m * P + nb);
+      dh[0] = o_h[0];
+      dh[1] = o_h[1];
+    }
   }
 }
 
-// Dixon digit epilogue: Y[k][m][n0 + c ..] = bal(D), one 16-byte store per chunk
+// Dixon digit epilogue: Y[k][m][n0 + c ..] = bal(D), 32 states (one sector) per step
 __device__ __forceinline__ void epi_digit_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
                                                int cend, uint32_t tb) {
-  for (int c = cbeg; c < cend; c += 16) {
-    int v[16];
-    tmem_ld16(tb + (uint32_t)c, v);
+  for (int c = cbeg; c < cend; c += 32) {
+    int v[32];
+    tmem_ld32(tb + (uint32_t)c, v);
     const int nb = n0 + c;
     if (!mok || nb >= epi.N) continue;
-    uint32_t w4[4];
+    uint32_t w8[8];
     int tdrop;
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
+    for (int q4 = 0; q4 < 8; ++q4) {
       uint32_t word = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_split(v[q4 * 4 + b], tdrop) : epi.fq.bal(v[q4 * 4 + b]))
                 << (8 * b);
-      w4[q4] = word;
+      w8[q4] = word;
     }
-    *reinterpret_cast<uint4*>(epi.Y + ((size_t)k * epi.nLp + m) * epi.P + nb) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    uint4* dy = reinterpret_cast<uint4*>(epi.Y + ((size_t)k * epi.nLp + m) * epi.P + nb);
+    dy[0] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+    dy[1] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
   }
 }
 
