@@ -578,20 +578,39 @@ __device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
 //   warp 0: TMA (Cq, Jp once; b_0 per block)   warp 1: MMA issuer
 //   warp 2: TMEM allocator                     warps 4..11: epilogue
 namespace fz {
-constexpr int NS = 128;      // states per block
-constexpr int TILE = 128 * 128;
-constexpr int EPI_WARPS = 16;  // lane quarter x M tile x 64-state half
+constexpr int TILE = 128 * 128;  // a 128 x 128 tile of Cq / Jp
+constexpr int EPI_WARPS = 16;    // lane quarter x M tile x state half
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
-__host__ __device__ constexpr int smem_bytes(int nt) { return (2 * nt * nt + 3 * nt) * TILE + 1024 + 256; }
+// NS states per block: 128 (128B-swizzled in/y/h rows) or 64 (64B-swizzled,
+// twice the CTAs for small batches, whose launches are latency-bound)
+__host__ __device__ constexpr int box_bytes(int NS) { return NS * 128; }
+__host__ __device__ constexpr int smem_bytes(int nt, int NS) {
+  return 2 * nt * nt * TILE + 3 * nt * box_bytes(NS) + 1024 + 256;
+}
 }  // namespace fz
 
 // byte offset of (K row r, state s) in a 128B-swizzled MN-major box set
 // (one 16 KB box per 128 K rows; rows of 128 states)
+template <int NS>
 __device__ __forceinline__ uint32_t swz(int r, int s) {
-  return (uint32_t)((r >> 7) * fz::TILE + (r & 127) * 128 + ((((s >> 4) ^ (r & 7)) & 7) << 4) + (s & 15));
+  if (NS == 128)
+    return (uint32_t)((r >> 7) * fz::box_bytes(NS) + (r & 127) * 128 + ((((s >> 4) ^ (r & 7)) & 7) << 4) + (s & 15));
+  return (uint32_t)((r >> 7) * fz::box_bytes(NS) + (r & 127) * 64 + ((((s >> 4) ^ (r >> 1)) & 3) << 4) + (s & 15));
+}
+// MN-major B operand descriptor for one NS-wide atom (SBO: next 8-row K group)
+template <int NS>
+__device__ __forceinline__ uint64_t mn_desc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * NS) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(NS == 128 ? 2 : 4) << 61;  // SWIZZLE_128B / SWIZZLE_64B
+  return d;
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+template <int NS>
 __global__ void __launch_bounds__(fz::THREADS, 1)
     dixon_fused_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
                        const __grid_constant__ CUtensorMap tmB0, uint32_t idesc_c, uint32_t idesc_j, FusedArgs fa) {
@@ -601,9 +620,9 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
   uint8_t* sC = base;                       // nt x nt tiles (M tile mt, K box kb) at (mt * nt + kb)
   uint8_t* sJ = sC + nt * nt * fz::TILE;
   uint8_t* sIn = sJ + nt * nt * fz::TILE;   // nt boxes
-  uint8_t* sY = sIn + nt * fz::TILE;
-  uint8_t* sH = sY + nt * fz::TILE;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + nt * fz::TILE);
+  uint8_t* sY = sIn + nt * fz::box_bytes(NS);
+  uint8_t* sH = sY + nt * fz::box_bytes(NS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + nt * fz::box_bytes(NS));
   uint64_t* barA = bars;      // Cq, Jp loaded
   uint64_t* barB0 = bars + 1; // b_0 of the block loaded
   uint64_t* barD = bars + 2;  // digit product done
@@ -614,7 +633,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Ld = fa.Ld;
-  const int nblk = (fa.N + fz::NS - 1) / fz::NS;
+  const int nblk = (fa.N + NS - 1) / NS;
 
   if (threadIdx.x == 0) {
     mbar_init(smem_u32(barA), 1);
@@ -653,9 +672,9 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         // barrier of its own: barD runs Ld phases per block, and a parity
         // wait only tells the current phase from the one before it)
         if (i) mbar_wait(smem_u32(barFree), (uint32_t)((i - 1) & 1));
-        mbar_expect_tx(smem_u32(barB0), (uint32_t)(nt * fz::TILE));
+        mbar_expect_tx(smem_u32(barB0), (uint32_t)(nt * fz::box_bytes(NS)));
         for (int kb = 0; kb < nt; ++kb)
-          tma_load_2d(smem_u32(sIn + kb * fz::TILE), &tmB0, smem_u32(barB0), b * fz::NS, kb * 128);
+          tma_load_2d(smem_u32(sIn + kb * fz::box_bytes(NS)), &tmB0, smem_u32(barB0), b * NS, kb * 128);
       }
     }
   } else if (warp == 1) {
@@ -671,11 +690,12 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           for (int mt = 0; mt < nt; ++mt)
             for (int kb = 0; kb < nt; ++kb) {
-              const uint32_t a0 = smem_u32(sC + (mt * nt + kb) * fz::TILE), b0 = smem_u32(sIn + kb * fz::TILE);
+              const uint32_t a0 = smem_u32(sC + (mt * nt + kb) * fz::TILE),
+                             b0 = smem_u32(sIn + kb * fz::box_bytes(NS));
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
-                mma_i8(tmem + (uint32_t)(mt * 128), sw128_desc(a0 + kk * 32), sw128_mn_desc_1atom(b0 + kk * 4096),
-                       idesc_c, (kb | kk) != 0);
+                mma_i8(tmem + (uint32_t)(mt * NS), sw128_desc(a0 + kk * 32), mn_desc<NS>(b0 + kk * 32 * NS), idesc_c,
+                       (kb | kk) != 0);
             }
           mma_commit(smem_u32(barD));
           if (k + 1 == Ld) mma_commit(smem_u32(barFree));
@@ -684,11 +704,12 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
             asm volatile("tcgen05.fence::after_thread_sync;");
             for (int mt = 0; mt < nt; ++mt)
               for (int kb = 0; kb < nt; ++kb) {
-                const uint32_t a0 = smem_u32(sJ + (mt * nt + kb) * fz::TILE), b0 = smem_u32(sY + kb * fz::TILE);
+                const uint32_t a0 = smem_u32(sJ + (mt * nt + kb) * fz::TILE),
+                               b0 = smem_u32(sY + kb * fz::box_bytes(NS));
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)
-                  mma_i8(tmem + (uint32_t)(256 + mt * 128), sw128_desc(a0 + kk * 32),
-                         sw128_mn_desc_1atom(b0 + kk * 4096), idesc_j, (kb | kk) != 0);
+                  mma_i8(tmem + (uint32_t)(256 + mt * NS), sw128_desc(a0 + kk * 32), mn_desc<NS>(b0 + kk * 32 * NS),
+                         idesc_j, (kb | kk) != 0);
               }
             mma_commit(smem_u32(barC));
           }
@@ -697,8 +718,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     }
   } else if (warp >= 4) {
     // epilogue warp e: TMEM lane quarter e % 4, M tile (e / 4) % 2, states
-    // [64 (e / 8), +64); every phase drains 64 accumulators per thread with
-    // two 32-column TMEM loads
+    // [NS/2 (e / 8), +NS/2); every phase drains NS/2 accumulators per thread
+    // with 32-column TMEM loads
     const int e = warp - 4, quarter = e & 3, mt = (e >> 2) & 1, half = e >> 3;
     const int m = mt * 128 + quarter * 32 + lane;  // K row of in / y, M row of the products
     const bool active = mt < nt;
@@ -715,16 +736,17 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     stamp(0);
     int i = 0;
     for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
-      const int n0 = b * fz::NS + half * 64;
+      const int n0 = b * NS + half * (NS / 2);
+      constexpr int NCH = NS / 32;  // 16-state chunks per thread
       for (int k = 0; k < Ld; ++k) {
         const int d = i * Ld + k;
         const bool carry = k + 1 < Ld;
         // b_{k+1} for this thread's row: independent of the products, in flight early
-        uint4 b1[4];
+        uint4 b1[NCH];
         if (carry && active) {
           const int8_t* src = fa.Bg + ((size_t)(k + 1) * fa.nLp + m) * P + n0;
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch)
+          for (int ch = 0; ch < NCH; ++ch)
             b1[ch] = n0 + ch * 16 < fa.N ? __ldg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
         }
         mbar_wait(smem_u32(barD), (uint32_t)(d & 1));
@@ -733,9 +755,9 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         if (active) {
           int8_t* yg = fa.Y + ((size_t)k * fa.nLp + m) * P + n0;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int hh = 0; hh < NCH / 2; ++hh) {
             int v[32];
-            tmem_ld32(lanebase + (uint32_t)(mt * 128 + half * 64 + hh * 32), v);
+            tmem_ld32(lanebase + (uint32_t)(mt * NS + half * (NS / 2) + hh * 32), v);
 #pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) {
               const int ch = hh * 2 + c2;
@@ -752,7 +774,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
                 w4[q4] = word;
               }
               const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-              if (carry) *reinterpret_cast<uint4*>(sY + swz(m, half * 64 + ch * 16)) = y4;
+              if (carry) *reinterpret_cast<uint4*>(sY + swz<NS>(m, half * (NS / 2) + ch * 16)) = y4;
               if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
             }
           }
@@ -769,13 +791,13 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int hh = 0; hh < NCH / 2; ++hh) {
             int v[32];
-            tmem_ld32(lanebase + (uint32_t)(256 + mt * 128 + half * 64 + hh * 32), v);
+            tmem_ld32(lanebase + (uint32_t)(256 + mt * NS + half * (NS / 2) + hh * 32), v);
 #pragma unroll
             for (int c2 = 0; c2 < 2; ++c2) {
               const int ch = hh * 2 + c2;
-              const uint32_t off = swz(m, half * 64 + ch * 16);
+              const uint32_t off = swz<NS>(m, half * (NS / 2) + ch * 16);
               const uint4 lo = *reinterpret_cast<const uint4*>(sIn + off);
               const uint4 hi = k ? *reinterpret_cast<const uint4*>(sH + off) : make_uint4(0, 0, 0, 0);
               const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
@@ -883,38 +905,66 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
 
 
 
+
+namespace {
+CUtensorMap make_map_box(const int8_t* ptr, int rows, int ld, int inner, int box_inner, int box_rows,
+                         CUtensorMapSwizzle sw) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DRZG_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+template <int NS>
+void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs& fa, int sms, cudaStream_t st) {
+  const int nt = fa.nLp / 128;
+  CUtensorMap mb = make_map_box(fa.Bg, fa.nLp, fa.P, fa.P, NS, 128,
+                                NS == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+  // kind::i8, D s32, B signed MN-major, N = NS, M = 128; A signed (Cq) / unsigned (Jp)
+  const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
+  const int smem = tc::fz::smem_bytes(nt, NS);
+  static int attr_for = -1;
+  if (attr_for != smem) {
+    cudaFuncSetAttribute(tc::dixon_fused_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr_for = smem;
+  }
+  const int nblk = (fa.N + NS - 1) / NS;
+  static const bool one_block = std::getenv("DRZG_FUSED_ONEBLOCK") != nullptr;  // debug: one block per CTA
+  tc::dixon_fused_kernel<NS><<<one_block ? nblk : std::min(nblk, sms), tc::fz::THREADS, smem, st>>>(
+      mc, mj, mb, idesc_c, idesc_j, fa);
+}
+}  // namespace
+
 bool dixon_fused_ok(int nLp) { return nLp % 128 == 0 && nLp <= 256; }
 
 void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st) {
   DRZG_REQUIRE(dixon_fused_ok(fa.nLp), "dixon_fused: system order must be 128 or 256");
   DRZG_REQUIRE(fa.P % 64 == 0, "dixon_fused: state pitch must be a multiple of 64");
-  const int nt = fa.nLp / 128;
   CUtensorMap mc = make_map(C, fa.nLp, fa.nLp, fa.nLp, 128);
   CUtensorMap mj = make_map(Jd, fa.nLp, fa.nLp, fa.nLp, 128);
-  CUtensorMap mb = make_map(fa.Bg, fa.nLp, fa.P, fa.P, 128);  // plane 0: nLp K rows x P states
-  // kind::i8, D s32, B signed MN-major, N = 128, M = 128; A signed (Cq) / unsigned (Jp)
-  const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
-  const int smem = tc::fz::smem_bytes(nt);
-  static int attr_for = -1;
-  if (attr_for != smem) {
-    cudaFuncSetAttribute(tc::dixon_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_for = smem;
-  }
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int nblk = (fa.N + tc::fz::NS - 1) / tc::fz::NS;
-  static const bool one_block = std::getenv("DRZG_FUSED_ONEBLOCK") != nullptr;  // debug: one block per CTA
-  tc::dixon_fused_kernel<<<one_block ? nblk : std::min(nblk, sms), tc::fz::THREADS, smem, st>>>(mc, mj, mb, idesc_c,
-                                                                                              idesc_j, fa);
+  // small batches (fewer 128-state blocks than SMs) run 64-state blocks
+  static const char* ns_env = std::getenv("DRZG_FUSED_NS");
+  const int ns = ns_env ? std::atoi(ns_env) : ((fa.N + 127) / 128 < sms ? 64 : 128);
+  if (ns == 64)
+    launch_fused<64>(mc, mj, fa, sms, st);
+  else
+    launch_fused<128>(mc, mj, fa, sms, st);
   cudaError_t e = cudaGetLastError();
   DRZG_REQUIRE(e == cudaSuccess, std::string("dixon_fused launch: ") + cudaGetErrorString(e));
 }
-
 
 void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st) {
   TcEpiArgs& e = fa.epi;
