@@ -844,7 +844,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   // (descending pole): key sort, grouping by (column, u) and by side row g,
   // and the carried digit sums of each group's entries
   SeedPreparer prep(cols, top0, [&](int c, const Expo& u) { return key(c, u); }, nv, Ld, T.dp.q,
-                    std::max(1u, std::min(host_threads_, 8u)));
+                    std::max(1u, std::min(host_threads_ / 4, 4u)));
   // The policy (moves, landing, combines, seeds, slot bookkeeping) never
   // needs a device result, so it runs on its own thread as far ahead as it
   // likes and hands every sweep to this thread as a command; this thread only
@@ -958,7 +958,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       std::vector<int> vd(nf);
       std::vector<i64> kk(nf);
       {
-        const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_, nf / 4096 + 1));
+        // leave cores to the launcher and the seed preparers (an oversubscribed
+        // launcher starves the device)
+        const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_ > 6 ? host_threads_ - 4 : 2, nf / 4096 + 1));
         std::vector<std::thread> pool;
         std::vector<std::exception_ptr> errs(nth);
         for (int t = 0; t < nth; ++t)

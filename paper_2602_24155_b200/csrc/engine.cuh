@@ -64,6 +64,7 @@ class Stager {
       if (b.h) cudaFreeHost(b.h);
       if (b.ev) cudaEventDestroy(b.ev);
     }
+    for (void* h : retired_) cudaFreeHost(h);
   }
   void copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (!bytes) return;
@@ -72,8 +73,10 @@ class Stager {
     if (!b.ev) DRZG_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
     if (b.used) DRZG_CUDA(cudaEventSynchronize(b.ev));
     if (b.cap < bytes) {
-      if (b.h) DRZG_CUDA(cudaFreeHost(b.h));
-      b.cap = std::max<size_t>(bytes + bytes / 2, (size_t)1 << 20);
+      // the old buffer is retired, not freed: cudaFreeHost synchronises the
+      // whole device, which would stall the launcher behind queued work
+      if (b.h) retired_.push_back(b.h);
+      b.cap = std::max<size_t>(2 * bytes, (size_t)1 << 20);
       DRZG_CUDA(cudaMallocHost(&b.h, b.cap));
     }
     std::memcpy(b.h, src, bytes);
@@ -92,6 +95,7 @@ class Stager {
   };
   Buf bufs_[kRing];
   int next_ = 0;
+  std::vector<void*> retired_;
 };
 
 template <class T>
