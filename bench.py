@@ -270,8 +270,12 @@ def main():
         carry = {"kernel": "tc::gemm_kernel (block-sparse carry product + residual epilogue)",
                  "achieved_tops": carry_tops, "frac": carry_tops / peak if peak else None,
                  "share_of_kernel_time": kern["carry_ms"] / ksum if ksum else None}
-    kname = ("tc::dixon_fused_kernel (digit + carry products of every digit, one launch per pole drop)" if fused
-             else "tc::gemm_kernel (digit product y_k = bal(Cq . in_k))")
+    if not fused:
+        kname = "tc::gemm_kernel (digit product y_k = bal(Cq . in_k))"
+    elif fr["nL"] <= 256:
+        kname = "tc::dixon_fused_kernel (digit + carry products of every digit, one launch per pole drop)"
+    else:
+        kname = "tc::dixon_flow_kernel (dense digit + block-sparse carry tiles of every digit, one dataflow launch)"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     total_matvecs = fr["matvecs"] if world == 1 else None
     if world == 1:
