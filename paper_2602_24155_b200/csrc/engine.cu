@@ -1015,6 +1015,12 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       led.matvecs += cmd->matvecs;
       auto hp4 = std::chrono::steady_clock::now();
       led.startups += (i64)nf;
+      // the sweep goes to the launcher now; its landing (merges, floor
+      // arrivals) follows as a second command, so the device starts on the
+      // chunk while the policy lands it
+      push(std::move(cmd));
+      cmd = std::make_unique<SweepCmd>();
+      cmd->pole = P;
       // land every state at pole P - k; a state landing on a key already there
       // is combined at once (reduction.hpp:502 combines after every sweep)
       std::vector<int>& fs = cmd->fs;

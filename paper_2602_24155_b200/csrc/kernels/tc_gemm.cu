@@ -956,7 +956,7 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   // small batches (fewer 128-state blocks than SMs) run 64-state blocks
-  static const char* ns_env = std::getenv("DRZG_FUSED_NS");
+  const char* ns_env = std::getenv("DRZG_FUSED_NS");
   const int ns = ns_env ? std::atoi(ns_env) : ((fa.N + 127) / 128 < sms ? 64 : 128);
   if (ns == 64)
     launch_fused<64>(mc, mj, fa, sms, st);

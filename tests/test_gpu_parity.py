@@ -115,3 +115,27 @@ def test_zeta_matches_reference(name):
     z = drzg.zeta(g["p"], g["n"], g["d"], g["coeffs"])
     assert [z["Q"]] == g["Q_candidates"][:1]
     assert all(ok for (_, _, ok) in z["counts"])
+
+
+# Every device path gives the same bits: the one-launch small-system kernel at
+# both block widths, the dataflow kernel, the separate digit/carry launches
+# with dense or block-sparse carry, and the dp4a CUDA-core fallback.  The
+# switches are read when the engine is built (once per call).
+PATH_ENVS = [
+    {"DRZG_FUSED_NS": "64"},
+    {"DRZG_FUSED_NS": "128"},
+    {"DRZG_FUSED": "0", "DRZG_FLOW": "0"},
+    {"DRZG_FUSED": "0", "DRZG_FLOW": "0", "DRZG_SPARSE_CARRY": "0"},
+    {"DRZG_GEMM": "dp4a"},
+]
+
+
+@pytest.mark.parametrize("env", PATH_ENVS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+@pytest.mark.parametrize("name", ["k3_f11_s1_r1.json", "threefold_f13_s1_r1.json", "quintic_f7_s1.json"])
+def test_device_paths_agree(name, env, monkeypatch):
+    g = golden(name)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    fr = drzg.frobenius(g["p"], g["n"], g["d"], g["coeffs"], r_uniform=g["r_uniform"], nm=g["nm_override"])
+    assert fr["F"] == g["F"]
+    assert fr["matvecs"] == g["ledger"]["matvecs"]
