@@ -26,6 +26,9 @@ for c in cases:
         elif c == "threefold_zeta":
             co = drzg.random_hypersurface(13, 4, 3, 1); r = drzg.zeta(13, 4, 3, co)
             r.pop("frobenius", None)
+        elif c == "qsurf_zeta":
+            co = drzg.random_hypersurface(7, 3, 5, 1); r = drzg.zeta(7, 3, 5, co, profile=False)
+            r = {k: r[k] for k in r if k not in ("F", "charpoly")}
         elif c == "qsurf_r1":
             co = drzg.random_hypersurface(7, 3, 5, 1); r = drzg.frobenius(7, 3, 5, co, r_uniform=1, nm=3, profile=bool(int(os.environ.get("DRZG_PROFILE", "1"))))
         r.pop("F", None); r.pop("charpoly", None)
