@@ -69,6 +69,8 @@ class ClockSampler:
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        if os.environ.get("DRZG_NO_CLOCKS"):  # diagnostics only: no sampling
+            return self
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
@@ -77,6 +79,23 @@ class ClockSampler:
         except OSError:
             self.proc = None
         return self
+
+    def mark(self):
+        """start of the timed region: waits until nvidia-smi is sampling
+        (its start-up is over), then summary() keeps the samples after it"""
+        t0 = time.time()
+        while self.proc and time.time() - t0 < 15:
+            try:
+                if sum(1 for _ in open(self.path)) >= 2:
+                    break
+            except OSError:
+                break
+            time.sleep(0.05)
+        try:
+            self.f.flush()
+            self.skip = sum(1 for _ in open(self.path))
+        except (OSError, AttributeError):
+            self.skip = 0
 
     def __exit__(self, *a):
         if self.proc:
@@ -87,7 +106,9 @@ class ClockSampler:
     def summary(self):
         rows = []
         try:
-            for line in open(self.path):
+            for ln, line in enumerate(open(self.path)):
+                if ln < getattr(self, "skip", 0):
+                    continue
                 parts = [x.strip() for x in line.split(",")]
                 if len(parts) >= 9:
                     rows.append(parts)
@@ -217,13 +238,17 @@ def main():
         z = drzg.charpoly(p, n, d, [str(x) for x in F], b, r_uniform=r_uniform) if rank == 0 else None
         return fr["kernels"]["device_ms"] / 1e3, z, fr
 
-    for _ in range(args.warmup):
-        step()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    dev_times, e2e_times, last = [], [], None
+    dev_times, e2e_times, zeta_times, last = [], [], [], None
+    # the sampler starts before the warm-up: nvidia-smi's start-up (NVML
+    # init) stalls CUDA calls of this process for up to seconds, which must
+    # not land in a timed step; it keeps sampling through the timed region
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark()
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
@@ -241,6 +266,8 @@ def main():
                 dev_s, e2e_s = tt.tolist()
             dev_times.append(dev_s)
             e2e_times.append(e2e_s)
+            if z and "seconds" in z:
+                zeta_times.append(z["seconds"])
             last = (z, fr)
     if dist:
         dist.barrier()
@@ -314,6 +341,8 @@ def main():
         "carry_gemm": carry,
         "ledger": {"matvecs": fr["matvecs"], "startups": fr["startups"], "combines": fr["combines"],
                    "terms": fr["terms"]},
+        "per_step_s": {"device": [round(x, 4) for x in dev_times], "e2e": [round(x, 4) for x in e2e_times],
+                       "zeta_call": [round(x, 4) for x in zeta_times]},
         "stage_seconds": fr["times"], "kernels_ms": kern,
         "cpu_baseline": cpu, "clocks": clocks,
         "Q_head": (z["Q"][:4] if z and "Q" in z else (z["candidates"][0][:4] if z else None)),

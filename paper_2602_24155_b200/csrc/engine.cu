@@ -127,6 +127,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     DRZG_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
     uint64_t keep = UINT64_MAX;
     DRZG_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &keep));
+    DRZG_CUDA(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, dev));
   }
   DRZG_REQUIRE(T.dp.Ld <= dev::kLdMax, "engine: too many digit planes");
   // small systems pad to whole 128-row tiles (the one-launch Dixon kernel)
@@ -205,6 +206,10 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   DRZG_REQUIRE((size_t)dev::kGatherStates * sidep_ <= 200 * 1024, "engine: side too large for the gather staging");
   DRZG_CUDA(cudaFuncSetAttribute(dev::gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)std::min<size_t>((size_t)dev::kGatherStates * sidep_, 200 * 1024)));
+  // the flush transpose stages Ld x 64 rows x 32 states (50 KB at the quintic
+  // surface's 25 digit planes: above the 48 KB default)
+  DRZG_CUDA(cudaFuncSetAttribute(dev::flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 T.dp.Ld * dev::kFlushRows * dev::kFlushStates));
   const char* fz = std::getenv("DRZG_FUSED");
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
   const char* fl = std::getenv("DRZG_FLOW");
@@ -613,7 +618,8 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
         timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gb, dev::kGatherThreads, gsm, st_>>>(a); });
       }  // later steps: the previous epilogue already wrote this step's operand
       dixon(a);
-      dim3 gE((By + 127) / 128, (T.side + dev::kEpiRows - 1) / dev::kEpiRows);
+      a.epi_rows = dev::epi_rows_for(By, T.side, sms_);
+      dim3 gE((By + 127) / 128, (T.side + a.epi_rows - 1) / a.epi_rows);
       timed(&clock.epi_ms, [&] { dev::launch_epilogue(a, gE, st_); });
       mv += By;
       const int Bn = count_ge(y + 1);

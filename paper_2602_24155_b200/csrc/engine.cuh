@@ -217,6 +217,7 @@ class ReductionEngine {
   DevBuf<i64> d_k_;
   // temporaries
   int bcap_ = 0;
+  int sms_ = 148;  // SM count of the engine device (set at construction)
   DevBuf<int8_t> Bg_, IN_, Y_;
   DevBuf<int8_t> H_;
   DevBuf<int8_t> W_;

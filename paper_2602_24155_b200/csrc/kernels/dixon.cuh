@@ -16,6 +16,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 
 #include "fastq.cuh"
 #include "step_args.cuh"
@@ -173,6 +174,22 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
 // the work per digit and state is NT byte-extract + multiply-adds and one
 // balanced division by q (multiply-high, bias folded into the running carry).
 constexpr int kEpiRows = 64, kEpiTermCap = 512, kEpiMaxNT = 6;
+static_assert(kEpiRows == StepArgs{}.epi_rows, "StepArgs::epi_rows defaults to kEpiRows");
+// rows per block for a batch of B states: kEpiRows when the batch fills the
+// GPU, else halved (down to one row per warp) until there are >= 8 blocks per
+// SM -- small batches are latency-bound, one warp per row in flight at once
+inline int epi_rows_for(int B, int side, int sms) {
+  static const int fixed = [] {
+    const char* e = std::getenv("DRZG_EPI_ROWS");  // A/B override: 8, 16, 32 or 64
+    const int r = e ? std::atoi(e) : 0;
+    return (r == 8 || r == 16 || r == 32 || r == 64) ? r : 0;
+  }();
+  if (fixed) return fixed;
+  const int bx = (B + 127) / 128;
+  int rows = kEpiRows;
+  while (rows > 8 && bx * ((side + rows - 1) / rows) < 8 * sms) rows >>= 1;
+  return rows;
+}
 
 // sign-extended byte j of w (one PRMT)
 // (PTX prmt default mode: a selector nibble with bit 3 set replicates the
@@ -240,7 +257,7 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int sb = blockIdx.x * 128;
   const int side = a.side;
-  const int g0 = blockIdx.y * kEpiRows, g1 = min(side, g0 + kEpiRows);
+  const int g0 = blockIdx.y * a.epi_rows, g1 = min(side, g0 + a.epi_rows);
   if (tid < 128) {
     const int s = sb + tid;
     const bool valid = s < a.B;

@@ -39,6 +39,7 @@ struct StepArgs {
   int y;                  // step index within the chunk: x = u0 - y v
   int B;
   int P;                  // state pitch of the temporaries (>= B, multiple of 64)
+  int epi_rows = 64;      // side rows per T_x-epilogue block (<= kEpiRows; fewer for small batches)
   // temporaries, state-contiguous ("MN-major" GEMM operands)
   int8_t* Bg;             // Ld x nLp x P
   int8_t* IN;             // nLp x P
