@@ -325,10 +325,37 @@ struct Vmm {
   } while (0)
 }  // namespace
 
+// A released pool stays mapped for the next engine on the same device (like
+// a caching allocator): unmapping and re-creating gigabytes of physical
+// memory costs tens to hundreds of milliseconds per zeta function, with a
+// long tail.  Slots carry no state between engines (seed_kernel writes every
+// fresh slot in full).
+namespace {
+struct CachedPool {
+  int8_t* base = nullptr;
+  size_t reserved = 0, mapped = 0;
+  std::vector<std::pair<size_t, std::pair<size_t, unsigned long long>>> chunks;  // off, (bytes, handle)
+};
+std::mutex g_pool_mu;
+std::map<int, CachedPool> g_pool_cache;
+}  // namespace
+
 void ReductionEngine::grow_pool(int need) {
   const Vmm& V = Vmm::get();
   int dev = 0;
   DRZG_CUDA(cudaGetDevice(&dev));
+  if (!pool_) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool_cache.find(dev);
+    if (it != g_pool_cache.end() && it->second.base) {
+      pool_ = it->second.base;
+      vmm_reserved_ = it->second.reserved;
+      vmm_mapped_ = it->second.mapped;
+      for (auto& c : it->second.chunks) vmm_chunks_.push_back({c.first, c.second.first, c.second.second});
+      g_pool_cache.erase(it);
+      pool_dev_ = dev;
+    }
+  }
   CUmemAllocationProp prop = {};
   prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
@@ -344,6 +371,7 @@ void ReductionEngine::grow_pool(int need) {
     DRZG_CU(V.reserve(&base, vmm_reserved_, gran, 0, 0));
     pool_ = reinterpret_cast<int8_t*>(base);
     vmm_mapped_ = 0;
+    pool_dev_ = dev;
   }
   int ncap = std::max(need, cap_ + std::max(1024, cap_ / 2));
   size_t want = (size_t)ncap * slot_stride_;
@@ -388,6 +416,19 @@ void ReductionEngine::grow_pool(int need) {
 void ReductionEngine::release_pool() {
   if (!pool_) return;
   cudaStreamSynchronize(st_);
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    CachedPool& c = g_pool_cache[pool_dev_];
+    if (!c.base && !std::getenv("DRZG_NO_POOL_CACHE")) {
+      c.base = pool_;
+      c.reserved = vmm_reserved_;
+      c.mapped = vmm_mapped_;
+      for (auto& k : vmm_chunks_) c.chunks.push_back({k.off, {k.bytes, k.handle}});
+      vmm_chunks_.clear();
+      pool_ = nullptr;
+      return;
+    }
+  }
   const Vmm& V = Vmm::get();
   for (auto& c : vmm_chunks_) {
     V.unmap(reinterpret_cast<CUdeviceptr>(pool_) + c.off, c.bytes);

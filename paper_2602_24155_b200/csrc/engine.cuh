@@ -203,6 +203,7 @@ class ReductionEngine {
   // pool
   int8_t* pool_ = nullptr;
   size_t vmm_reserved_ = 0, vmm_mapped_ = 0;
+  int pool_dev_ = 0;
   struct VmmChunk {
     size_t off, bytes;
     unsigned long long handle;

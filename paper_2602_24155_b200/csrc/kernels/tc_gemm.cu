@@ -105,6 +105,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 16 columns (the first 16 entries of v)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ int balmod(int x, int q) {
   int r = x % q;
   if (r < 0) r += q;
@@ -581,8 +591,9 @@ namespace fz {
 constexpr int TILE = 128 * 128;  // a 128 x 128 tile of Cq / Jp
 constexpr int EPI_WARPS = 16;    // lane quarter x M tile x state half
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
-// NS states per block: 128 (128B-swizzled in/y/h rows) or 64 (64B-swizzled,
-// twice the CTAs for small batches, whose launches are latency-bound)
+// NS states per block: 128 (128B-swizzled in/y/h rows), 64 (64B-swizzled)
+// or 32 (32B-swizzled): smaller blocks give small batches, whose launches
+// are latency-bound, more CTAs and shorter per-digit epilogue phases
 __host__ __device__ constexpr int box_bytes(int NS) { return NS * 128; }
 __host__ __device__ constexpr int smem_bytes(int nt, int NS) {
   return 2 * nt * nt * TILE + 3 * nt * box_bytes(NS) + 1024 + 256;
@@ -595,7 +606,9 @@ template <int NS>
 __device__ __forceinline__ uint32_t swz(int r, int s) {
   if (NS == 128)
     return (uint32_t)((r >> 7) * fz::box_bytes(NS) + (r & 127) * 128 + ((((s >> 4) ^ (r & 7)) & 7) << 4) + (s & 15));
-  return (uint32_t)((r >> 7) * fz::box_bytes(NS) + (r & 127) * 64 + ((((s >> 4) ^ (r >> 1)) & 3) << 4) + (s & 15));
+  if (NS == 64)
+    return (uint32_t)((r >> 7) * fz::box_bytes(NS) + (r & 127) * 64 + ((((s >> 4) ^ (r >> 1)) & 3) << 4) + (s & 15));
+  return (uint32_t)((r >> 7) * fz::box_bytes(NS) + (r & 127) * 32 + ((((s >> 4) ^ (r >> 2)) & 1) << 4) + (s & 15));
 }
 // MN-major B operand descriptor for one NS-wide atom (SBO: next 8-row K group)
 template <int NS>
@@ -605,7 +618,7 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t addr) {
   d |= (uint64_t)1 << 16;
   d |= (uint64_t)((8 * NS) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)(NS == 128 ? 2 : 4) << 61;  // SWIZZLE_128B / SWIZZLE_64B
+  d |= (uint64_t)(NS == 128 ? 2 : NS == 64 ? 4 : 6) << 61;  // SWIZZLE_128B / 64B / 32B
   return d;
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -737,7 +750,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     int i = 0;
     for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
       const int n0 = b * NS + half * (NS / 2);
-      constexpr int NCH = NS / 32;  // 16-state chunks per thread
+      constexpr int NCH = NS / 32;           // 16-state chunks per thread
+      constexpr int PER = NCH >= 2 ? 2 : 1;  // chunks per TMEM load (32 or 16 columns)
       for (int k = 0; k < Ld; ++k) {
         const int d = i * Ld + k;
         const bool carry = k + 1 < Ld;
@@ -755,12 +769,15 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         if (active) {
           int8_t* yg = fa.Y + ((size_t)k * fa.nLp + m) * P + n0;
 #pragma unroll
-          for (int hh = 0; hh < NCH / 2; ++hh) {
+          for (int hh = 0; hh < NCH / PER; ++hh) {
             int v[32];
-            tmem_ld32(lanebase + (uint32_t)(mt * NS + half * (NS / 2) + hh * 32), v);
+            if constexpr (PER == 2)
+              tmem_ld32(lanebase + (uint32_t)(mt * NS + half * (NS / 2) + hh * 32), v);
+            else
+              tmem_ld16(lanebase + (uint32_t)(mt * NS + half * (NS / 2) + hh * 16), v);
 #pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {
-              const int ch = hh * 2 + c2;
+            for (int c2 = 0; c2 < PER; ++c2) {
+              const int ch = hh * PER + c2;
               uint32_t w4[4];
 #pragma unroll
               for (int q4 = 0; q4 < 4; ++q4) {
@@ -791,12 +808,15 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (active) {
 #pragma unroll
-          for (int hh = 0; hh < NCH / 2; ++hh) {
+          for (int hh = 0; hh < NCH / PER; ++hh) {
             int v[32];
-            tmem_ld32(lanebase + (uint32_t)(256 + mt * NS + half * (NS / 2) + hh * 32), v);
+            if constexpr (PER == 2)
+              tmem_ld32(lanebase + (uint32_t)(256 + mt * NS + half * (NS / 2) + hh * 32), v);
+            else
+              tmem_ld16(lanebase + (uint32_t)(256 + mt * NS + half * (NS / 2) + hh * 16), v);
 #pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {
-              const int ch = hh * 2 + c2;
+            for (int c2 = 0; c2 < PER; ++c2) {
+              const int ch = hh * PER + c2;
               const uint32_t off = swz<NS>(m, half * (NS / 2) + ch * 16);
               const uint4 lo = *reinterpret_cast<const uint4*>(sIn + off);
               const uint4 hi = k ? *reinterpret_cast<const uint4*>(sH + off) : make_uint4(0, 0, 0, 0);
@@ -925,7 +945,9 @@ template <int NS>
 void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs& fa, int sms, cudaStream_t st) {
   const int nt = fa.nLp / 128;
   CUtensorMap mb = make_map_box(fa.Bg, fa.nLp, fa.P, fa.P, NS, 128,
-                                NS == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+                                NS == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : NS == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_32B);
   // kind::i8, D s32, B signed MN-major, N = NS, M = 128; A signed (Cq) / unsigned (Jp)
   const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
@@ -957,8 +979,12 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
   }
   // small batches (fewer 128-state blocks than SMs) run 64-state blocks
   const char* ns_env = std::getenv("DRZG_FUSED_NS");
-  const int ns = ns_env ? std::atoi(ns_env) : ((fa.N + 127) / 128 < sms ? 64 : 128);
-  if (ns == 64)
+  // (32-state blocks when the whole batch fits one round of them: the
+  // per-digit epilogue phases halve, which is what a small batch waits on)
+  const int ns = ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : (fa.N + 127) / 128 < sms ? 64 : 128);
+  if (ns == 32)
+    launch_fused<32>(mc, mj, fa, sms, st);
+  else if (ns == 64)
     launch_fused<64>(mc, mj, fa, sms, st);
   else
     launch_fused<128>(mc, mj, fa, sms, st);

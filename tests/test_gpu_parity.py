@@ -118,10 +118,11 @@ def test_zeta_matches_reference(name):
 
 
 # Every device path gives the same bits: the one-launch small-system kernel at
-# both block widths, the dataflow kernel, the separate digit/carry launches
+# all three block widths, the dataflow kernel, the separate digit/carry launches
 # with dense or block-sparse carry, and the dp4a CUDA-core fallback.  The
 # switches are read when the engine is built (once per call).
 PATH_ENVS = [
+    {"DRZG_FUSED_NS": "32"},
     {"DRZG_FUSED_NS": "64"},
     {"DRZG_FUSED_NS": "128"},
     {"DRZG_FUSED": "0", "DRZG_FLOW": "0"},
