@@ -340,6 +340,15 @@ std::mutex g_pool_mu;
 std::map<int, CachedPool> g_pool_cache;
 }  // namespace
 
+// the retained mempool keeps freed stream-ordered memory reserved (fast
+// reuse across zeta functions); cudaMemGetInfo does not count it as free, so
+// memory planning trims it first
+void ReductionEngine::trim_mempool(int dev) {
+  cudaMemPool_t mp;
+  DRZG_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+  DRZG_CUDA(cudaMemPoolTrimTo(mp, 0));
+}
+
 void ReductionEngine::grow_pool(int need) {
   const Vmm& V = Vmm::get();
   int dev = 0;
@@ -376,6 +385,7 @@ void ReductionEngine::grow_pool(int need) {
   int ncap = std::max(need, cap_ + std::max(1024, cap_ / 2));
   size_t want = (size_t)ncap * slot_stride_;
   DRZG_CUDA(cudaStreamSynchronize(st_));
+  if (want > vmm_mapped_) trim_mempool(dev);  // unused stream-ordered reserve back to the driver
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   size_t margin = (size_t)2 << 30;
   if (want > vmm_mapped_ + (fr > margin ? fr - margin : 0) && bcap_ > 0) {
@@ -386,6 +396,8 @@ void ReductionEngine::grow_pool(int need) {
     H_.release();
     W_.release();
     bcap_ = 0;
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    trim_mempool(dev);
     DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   }
   size_t room = vmm_mapped_ + (fr > margin ? fr - margin : 0);
@@ -453,6 +465,13 @@ void ReductionEngine::ensure_batch(int B) {
   size_t per = (size_t)(2 * Ld + 1) * nLp_ + sizeof(int16_t) * nLp_ + (size_t)Ld * sidep_;
   size_t fr = 0, tot = 0;
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (fr * 0.8 < tot * 0.12) {
+    int dev = 0;
+    DRZG_CUDA(cudaGetDevice(&dev));
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    trim_mempool(dev);
+    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  }
   // temporaries get at most half of what is free, in multiples of 64 states
   // temporaries: at most 80% of what is free and 12% of the device, so the
   // state pool keeps room to grow
@@ -462,11 +481,11 @@ void ReductionEngine::ensure_batch(int B) {
   if (nb <= bcap_) return;
   bcap_ = nb;
   // state-contiguous layouts with pitch bcap_: Bg/Y Ld x nLp x P, IN/H nLp x P
-  Bg_.alloc((size_t)bcap_ * Ld * nLp_);
-  Y_.alloc((size_t)bcap_ * Ld * nLp_);
-  IN_.alloc((size_t)bcap_ * nLp_);
-  H_.alloc((size_t)bcap_ * nLp_);
-  W_.alloc((size_t)bcap_ * Ld * sidep_);
+  Bg_.alloc((size_t)bcap_ * Ld * nLp_, st_);
+  Y_.alloc((size_t)bcap_ * Ld * nLp_, st_);
+  IN_.alloc((size_t)bcap_ * nLp_, st_);
+  H_.alloc((size_t)bcap_ * nLp_, st_);
+  W_.alloc((size_t)bcap_ * Ld * sidep_, st_);
   // K padding of Bg / IN / Y must read as zero
   DRZG_CUDA(cudaMemsetAsync(Bg_.p, 0, Bg_.n, st_));
   DRZG_CUDA(cudaMemsetAsync(Y_.p, 0, Y_.n, st_));

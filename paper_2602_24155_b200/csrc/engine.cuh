@@ -105,40 +105,47 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() {
-    if (p) cudaFree(p);  // also valid for stream-ordered allocations
-  }
-  void alloc(size_t count) {
+  // stream-ordered buffers (the engine's) come from the device's retained
+  // mempool and go back to it without synchronising the device; the stream
+  // outlives the engine that owns the buffer
+  ~DevBuf() { release(); }
+  void alloc(size_t count, cudaStream_t st = nullptr) {
     if (count <= n) return;
-    if (p) DRZG_CUDA(cudaFree(p));
-    p = nullptr;
-    DRZG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    release();
+    if (st) {
+      DRZG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), st));
+      async_ = true;
+      ast_ = st;
+    } else {
+      DRZG_CUDA(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    }
     n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (async_)
+        cudaFreeAsync(p, ast_);
+      else
+        cudaFree(p);
+    }
     p = nullptr;
     n = 0;
+    async_ = false;
   }
   void upload(const std::vector<T>& v, cudaStream_t st) {
-    alloc(v.size());
+    alloc(v.size(), st);
     if (!v.empty()) DRZG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
     g_traffic.h2d += (long long)(v.size() * sizeof(T));
   }
   // stream-ordered growth and a pinned-staged copy: never blocks the host on
   // earlier device work
   void stage(const std::vector<T>& v, Stager& sg, cudaStream_t st) {
-    if (v.size() > n) {
-      if (p) DRZG_CUDA(cudaFreeAsync(p, st));
-      size_t cnt = std::max<size_t>(v.size() + v.size() / 2, 1024);
-      DRZG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cnt * sizeof(T), st));
-      n = cnt;
-      async_ = true;
-    }
+    if (v.size() > n) alloc(std::max<size_t>(v.size() + v.size() / 2, 1024), st);
     sg.copy(p, v.data(), v.size() * sizeof(T), st);
     g_traffic.h2d += (long long)(v.size() * sizeof(T));
   }
   bool async_ = false;
+  cudaStream_t ast_ = nullptr;
 };
 
 class ReductionEngine {
@@ -210,6 +217,7 @@ class ReductionEngine {
   };
   std::vector<VmmChunk> vmm_chunks_;
   void release_pool();
+  void trim_mempool(int dev);
   int cap_ = 0;
   i64 peak_live_ = 0;
   std::vector<int> free_;
