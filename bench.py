@@ -123,6 +123,18 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+def committed_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed `ncu --set full` capture of this config
+    (profiles/r01/traffic_<config>.json, written from the .ncu-rep by hand;
+    bench.py cannot run ncu itself), else null"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", f"traffic_{config}.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
 def int8_peak_tops(torch):
     """measured dense int8 tensor throughput (cuBLASLt via torch._int_mm)"""
     n = 8192
@@ -322,6 +334,7 @@ def main():
             cpu = {"value": None, "unit": "s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
     # mod-p^N reduction Gop/s = 2 side^2 per matvec x matvecs / s
     gops = 2.0 * fr["side"] ** 2 * fr["matvecs"] / value / 1e9 if world == 1 else None
+    traffic = committed_traffic(args.config)
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
@@ -333,7 +346,8 @@ def main():
                 "d2h_bytes_per_step": fr["traffic"]["d2h_bytes"]},
         "gpu_launches": fr["traffic"]["launches"] * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, "traffic": (traffic or {}).get("bytes_per_launch"),
+                     "traffic_source": (traffic or {}).get("source"),
                      "kernel": kname, "avg_launch_ms": gemm_avg_ms,
                      "share_of_kernel_time": kern["gemm_ms"] / ksum if ksum else None,
                      "peak_source": "measured on this box: torch._int_mm 8192^3 int8 (cuBLASLt), best of 5"},

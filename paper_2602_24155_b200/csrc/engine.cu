@@ -845,6 +845,10 @@ class SeedPreparer {
 void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led) {
   const RuvTables& T = *T_;
   const int nv = T.nv, Ld = T.dp.Ld, ncol = (int)cols.size();
+  // DRZG_VERBOSE: wall-clock marks of the run's stages (long-tail hunting)
+  const auto wm0 = std::chrono::steady_clock::now();
+  double wmark[5] = {0, 0, 0, 0, 0};
+  auto wsince = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - wm0).count(); };
   // key packing for combine_states' (u, pole) identity, per column
   i64 maxpole = 0;
   size_t total_seeds = 0;
@@ -867,6 +871,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   DRZG_CUDA(cudaEventCreate(&run0));
   DRZG_CUDA(cudaEventCreate(&run1));
   DRZG_CUDA(cudaEventRecord(run0, st_));
+  wmark[0] = wsince();
   DevBuf<long long> dG;
   dG.alloc((size_t)ncol * Ld * gsize_);
   DRZG_CUDA(cudaMemsetAsync(dG.p, 0, dG.n * sizeof(long long), st_));
@@ -1238,7 +1243,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     policy.join();
     throw;
   }
+  wmark[1] = wsince();
   policy.join();
+  wmark[2] = wsince();
   if (perr) std::rethrow_exception(perr);
   for (int c = 0; c < ncol; ++c) led.combines += floor_arrivals[c] - (i64)floor_keys[c].size();
   if (timeline && !tl.empty()) {
@@ -1277,7 +1284,12 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
   g_traffic.d2h += (long long)(dG.n * sizeof(long long));
   DRZG_CUDA(cudaEventRecord(run1, st_));
+  wmark[3] = wsince();
   DRZG_CUDA(cudaStreamSynchronize(st_));
+  wmark[4] = wsince();
+  if (std::getenv("DRZG_VERBOSE"))
+    std::fprintf(stderr, "[drzg] pchunk wall: run0 %.3f loop %.3f join %.3f run1 %.3f sync %.3f\n", wmark[0], wmark[1],
+                 wmark[2], wmark[3], wmark[4]);
   {
     float ms = 0;
     DRZG_CUDA(cudaEventElapsedTime(&ms, run0, run1));
