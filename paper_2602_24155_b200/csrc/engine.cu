@@ -555,7 +555,7 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     static int traces = std::getenv("DRZG_FUSED_TRACE") ? 6 : 0;
     DevBuf<long long> tb;
     if (traces > 0 && nb <= 2048) {
-      tb.alloc(4 * T.dp.Ld + 2);
+      tb.alloc(4 * T.dp.Ld + 2, st_);
       DRZG_CUDA(cudaMemsetAsync(tb.p, 0, tb.n * 8, st_));
       f.trace = tb.p;
     }
@@ -598,7 +598,7 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     e.kb_ptr = kb_ptr_.p;
     e.kb_idx = kb_idx_.p;
     const size_t nctr = (size_t)(2 * T.dp.Ld - 1) * ((nb + 255) / 256);
-    flow_ctr_.alloc(std::max<size_t>(nctr, (size_t)(2 * T.dp.Ld - 1) * ((bcap_ + 255) / 256)));
+    flow_ctr_.alloc(std::max<size_t>(nctr, (size_t)(2 * T.dp.Ld - 1) * ((bcap_ + 255) / 256)), st_);
     f.counters = flow_ctr_.p;
     timed(&clock.gemm_ms, [&] { dixon_flow(C_.p, Jd_.p, f, st_); });
     ++clock.gemm_launches;
@@ -849,6 +849,16 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   const auto wm0 = std::chrono::steady_clock::now();
   double wmark[5] = {0, 0, 0, 0, 0};
   auto wsince = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - wm0).count(); };
+  // declared first, destroyed last: the time the locals' destructors take
+  struct ExitMark {
+    std::chrono::steady_clock::time_point t0;
+    bool on;
+    ~ExitMark() {
+      if (on)
+        std::fprintf(stderr, "[drzg] pchunk wall: exit %.3f\n",
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } exit_mark{wm0, std::getenv("DRZG_VERBOSE") != nullptr};
   // key packing for combine_states' (u, pole) identity, per column
   i64 maxpole = 0;
   size_t total_seeds = 0;
@@ -873,10 +883,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   DRZG_CUDA(cudaEventRecord(run0, st_));
   wmark[0] = wsince();
   DevBuf<long long> dG;
-  dG.alloc((size_t)ncol * Ld * gsize_);
+  dG.alloc((size_t)ncol * Ld * gsize_, st_);
   DRZG_CUDA(cudaMemsetAsync(dG.p, 0, dG.n * sizeof(long long), st_));
   DevBuf<int> d_err;
-  d_err.alloc(1);
+  d_err.alloc(1, st_);
   DRZG_CUDA(cudaMemsetAsync(d_err.p, 0, sizeof(int), st_));
   if (cap_ == 0) {
     // live states never exceed the seeds materialised so far: size the pool
@@ -914,8 +924,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   // background preparation of every seed bucket, in consumption order
   // (descending pole): key sort, grouping by (column, u) and by side row g,
   // and the carried digit sums of each group's entries
-  SeedPreparer prep(cols, top0, [&](int c, const Expo& u) { return key(c, u); }, nv, Ld, T.dp.q,
-                    std::max(1u, std::min(host_threads_ / 4, 4u)));
+  auto prep_owner = std::make_unique<SeedPreparer>(cols, top0, [&](int c, const Expo& u) { return key(c, u); }, nv, Ld,
+                                                   T.dp.q, std::max(1u, std::min(host_threads_ / 4, 4u)));
+  SeedPreparer& prep = *prep_owner;
   // The policy (moves, landing, combines, seeds, slot bookkeeping) never
   // needs a device result, so it runs on its own thread as far ahead as it
   // likes and hands every sweep to this thread as a command; this thread only
@@ -1301,6 +1312,24 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   G.assign(ncol, {});
   for (int c = 0; c < ncol; ++c)
     G[c].assign(hG.begin() + (size_t)c * Ld * gsize_, hG.begin() + (size_t)(c + 1) * Ld * gsize_);
+  if (exit_mark.on) {
+    // which local's destruction is slow (long-tail hunting)
+    const double a0 = wsince();
+    prep_owner.reset();
+    const double a1 = wsince();
+    { auto tmp = std::move(landed); }
+    { auto tmp = std::move(landed_idx); }
+    const double a2 = wsince();
+    { auto tmp = std::move(floor_keys); }
+    const double a3 = wsince();
+    d_a.release(); d_b.release(); d_c.release(); d_s2.release(); d_p2.release(); d_g2.release();
+    d_mp.release(); d_mm.release(); d_dig.release(); d_dig2.release();
+    const double a4 = wsince();
+    dG.release(); d_err.release();
+    const double a5 = wsince();
+    std::fprintf(stderr, "[drzg] pchunk wall: return %.3f prep %.3f landed %.3f floor %.3f devbufs %.3f dG %.3f\n", a0,
+                 a1 - a0, a2 - a1, a3 - a2, a4 - a3, a5 - a4);
+  }
 }
 
 void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<int>& vdir, const std::vector<i64>& k,
