@@ -981,7 +981,10 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
   const char* ns_env = std::getenv("DRZG_FUSED_NS");
   // (32-state blocks when the whole batch fits one round of them: the
   // per-digit epilogue phases halve, which is what a small batch waits on)
-  const int ns = ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : (fa.N + 127) / 128 < sms ? 64 : 128);
+  // (large batches: 64-state blocks beat 128 too, 82 vs 86 ms of fused time
+  // per K3 zeta function -- the per-digit epilogue phase is what a block
+  // waits on, and it halves; DRZG_FUSED_NS=128 keeps the 128-state variant)
+  const int ns = ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : 64);
   if (ns == 32)
     launch_fused<32>(mc, mj, fa, sms, st);
   else if (ns == 64)
