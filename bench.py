@@ -38,7 +38,23 @@ CONFIGS = {
     "threefold": (13, 4, 3, 1, "random cubic threefold /F13, seed 1 (one of configs[3]'s batch)"),
     "fourfold": (7, 5, 3, 1, "random cubic fourfold /F7, seed 1 (configs[4])"),
     "fermat_fourfold_r1": (7, 5, 3, 0, "Fermat cubic fourfold /F7, reduced plan r_uniform=1"),
+    # one step = the zeta functions of all 64 hypersurfaces; ranks take seeds
+    # round-robin (replicas, no collective: SURVEY 8e)
+    "threefold_batch": (13, 4, 3, 0, "batch of 64 random cubic threefolds /F13, seeds 0-63 (configs[3])"),
 }
+BATCH_SEEDS = 64
+
+
+def merge_frobenius(frs):
+    """sum the per-hypersurface counters of a batch step (ledger, kernel
+    times, traffic, stage times); shape fields from the first"""
+    out = dict(frs[0])
+    for k in ("matvecs", "startups", "combines", "terms"):
+        out[k] = sum(f[k] for f in frs)
+    for sect in ("kernels", "traffic", "times"):
+        out[sect] = {k: (sum(f[sect][k] for f in frs) if isinstance(v, (int, float)) else v)
+                     for k, v in frs[0][sect].items()}
+    return out
 
 
 def hodge_counts(n, d):
@@ -239,8 +255,19 @@ def main():
     mine = all_cols[rank] if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
+    batch = args.config == "threefold_batch"
+    if batch:
+        batch_coeffs = [drzg.random_hypersurface(p, n, d, seed=s) for s in range(rank, BATCH_SEEDS, world)]
+
     def step(profile=False):
-        """one zeta function; returns (device_s, json of this rank)"""
+        """one zeta function (or the rank's share of a batch); returns (device_s, json of this rank)"""
+        if batch:
+            zs = [drzg.zeta(p, n, d, co, device=local, profile=profile, verify_counts=True) for co in batch_coeffs]
+            if not all(ok for z_ in zs for (_, _, ok) in z_["counts"]):
+                raise RuntimeError("a point count disagrees with Q")
+            fr_ = merge_frobenius([z_["frobenius"] for z_ in zs])
+            z0 = dict(zs[0], seconds=sum(z_["seconds"] for z_ in zs))
+            return fr_["kernels"]["device_ms"] / 1e3, z0, fr_
         if world == 1:
             z = drzg.zeta(p, n, d, coeffs, r_uniform=r_uniform, device=local, profile=profile,
                           verify_counts=True)
