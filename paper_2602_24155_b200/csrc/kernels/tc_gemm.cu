@@ -941,13 +941,35 @@ CUtensorMap make_map_box(const int8_t* ptr, int rows, int ld, int inner, int box
   return m;
 }
 
+// Tensor maps of the one-launch solve, kept per launching thread: a map is a
+// pure function of (address, dims, pitch), and re-encoding three of them for
+// every ~40 us launch put the launcher behind the device on small batches
+struct MapCache {
+  const void* p = nullptr;
+  int a = -1, b = -1;
+  CUtensorMap m;
+};
+template <class F>
+const CUtensorMap& cached_map(MapCache& c, const void* p, int a, int b, F make) {
+  if (c.p != p || c.a != a || c.b != b) {
+    c.m = make();
+    c.p = p;
+    c.a = a;
+    c.b = b;
+  }
+  return c.m;
+}
+
 template <int NS>
 void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs& fa, int sms, cudaStream_t st) {
   const int nt = fa.nLp / 128;
-  CUtensorMap mb = make_map_box(fa.Bg, fa.nLp, fa.P, fa.P, NS, 128,
-                                NS == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                : NS == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                           : CU_TENSOR_MAP_SWIZZLE_32B);
+  thread_local MapCache bcache;
+  const CUtensorMap& mb = cached_map(bcache, fa.Bg, fa.nLp, fa.P, [&] {
+    return make_map_box(fa.Bg, fa.nLp, fa.P, fa.P, NS, 128,
+                        NS == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                        : NS == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                   : CU_TENSOR_MAP_SWIZZLE_32B);
+  });
   // kind::i8, D s32, B signed MN-major, N = NS, M = 128; A signed (Cq) / unsigned (Jp)
   const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
@@ -969,8 +991,9 @@ bool dixon_fused_ok(int nLp) { return nLp % 128 == 0 && nLp <= 256; }
 void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st) {
   DRZG_REQUIRE(dixon_fused_ok(fa.nLp), "dixon_fused: system order must be 128 or 256");
   DRZG_REQUIRE(fa.P % 64 == 0, "dixon_fused: state pitch must be a multiple of 64");
-  CUtensorMap mc = make_map(C, fa.nLp, fa.nLp, fa.nLp, 128);
-  CUtensorMap mj = make_map(Jd, fa.nLp, fa.nLp, fa.nLp, 128);
+  thread_local MapCache ccache, jcache;
+  const CUtensorMap& mc = cached_map(ccache, C, fa.nLp, 0, [&] { return make_map(C, fa.nLp, fa.nLp, fa.nLp, 128); });
+  const CUtensorMap& mj = cached_map(jcache, Jd, fa.nLp, 0, [&] { return make_map(Jd, fa.nLp, fa.nLp, fa.nLp, 128); });
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -978,7 +1001,7 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   // small batches (fewer 128-state blocks than SMs) run 64-state blocks
-  const char* ns_env = std::getenv("DRZG_FUSED_NS");
+  const char* ns_env = std::getenv("DRZG_FUSED_NS");  // per launch: the path tests switch it
   // (32-state blocks when the whole batch fits one round of them: the
   // per-digit epilogue phases halve, which is what a small batch waits on)
   // (large batches: 64-state blocks beat 128 too, 82 vs 86 ms of fused time
