@@ -7,18 +7,28 @@ implementation timed beside it.
 
 One step = one zeta function of the configured synthetic hypersurface
 (reference generator rule: mt19937_64(seed), rng() % p per grevlex monomial,
-smooth for both working sets).  `value` is the device-resident reduction
-engine (seeds -> floor numerators for every Frobenius column, CUDA-event timed
-on the engine stream); `e2e` is the whole zeta function through the public
-C ABI (host coefficients in, Q out: setup, engine, final reduction, Frobenius
-assembly, charpoly, Q recovery, point-count checks).  For N > 1 (torchrun),
-Frobenius columns are partitioned across ranks, each rank reduces its columns
-on its own GPU, and the per-rank column blocks are gathered over NCCL before
-rank 0 recovers Q; times are the max over ranks.
+smooth for both working sets), through the public C ABI (drzg_zeta): setup,
+seeds, the device engine, the final reduction, Frobenius assembly, charpoly,
+Q recovery and the point-count checks.
+  value  the zeta call's own wall time (run_zeta, zeta.hpp:438-549), every stage
+  e2e    the same call timed from Python with CUDA events around it: host
+         coefficients in, JSON (Q) out; h2d/d2h count every byte it copies
+For N > 1 (torchrun), Frobenius columns are partitioned across ranks, each
+rank reduces its columns on its own GPU, the column blocks are gathered over
+NCCL, and rank 0 runs run_zeta's battery on the gathered F (drzg_zeta_from_F);
+times are the max over ranks.
+
+The default config is the K3 surface (configs[1]): the metric's cubic
+fourfold (configs[4]) takes minutes per zeta function on one B200, so 5 + 20
+of them do not fit the driver's run.  At N = 1 the default run therefore also
+times ONE complete fourfold zeta function (key "fourfold": warm-up on one
+column, then the whole zeta function with both point-count checks, clocks,
+ledger against the reference's replayed ledger, Q hash, per-kernel roofline).
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -29,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "seconds per zeta function (cubic fourfold p=7); mod-p^N reduction Gop/s vs roofline"
+GOLD = os.path.join(ROOT, "tests", "golden")
 
 CONFIGS = {
     # name: (p, n, d, seed, description)
@@ -43,6 +54,15 @@ CONFIGS = {
     "threefold_batch": (13, 4, 3, 0, "batch of 64 random cubic threefolds /F13, seeds 0-63 (configs[3])"),
 }
 BATCH_SEEDS = 64
+# the reference's full ledger of each config (tests/golden: real reference
+# runs; ledger_replay_*: the reference's value-free replay, which equals the
+# real ledger on every fixture -- tests/test_oracle.py)
+LEDGER_SOURCE = {"quintic": "quintic_f7_s1.json", "k3": "k3_f11_s1.json", "threefold": "threefold_f13_s1.json",
+                 "fourfold": "ledger_replay_fourfold.json", "quintic_surface": "ledger_replay_quintic_surface.json"}
+# series truncation of the reference's bounded sample (same hypersurface, same
+# limb count, every column and pole; scaled by the ledger ratio)
+SAMPLE_NM = {"k3": 4, "threefold": 4}
+FOURFOLD_COUNT_BUDGET = 1_000_000_000  # both count checks: #P^5(F_49) = 2.9e8 points
 
 
 def merge_frobenius(frs):
@@ -75,10 +95,10 @@ def hodge_counts(n, d):
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons during the timed region"""
 
-    def __init__(self, index):
+    def __init__(self, index, tag=""):
         self.index = index
         self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}{tag}.csv")
 
     def __enter__(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
@@ -143,13 +163,23 @@ class ClockSampler:
 def committed_traffic(config):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel, from the committed `ncu --set full` capture of this config
-    (profiles/r01/traffic_<config>.json, written from the .ncu-rep by hand;
+    (profiles/<round>/traffic_<config>.json, written from the .ncu-rep by hand;
     bench.py cannot run ncu itself), else null"""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, f"traffic_{config}.json")) as f:
+                return json.load(f)
+        except (OSError, ValueError):
+            continue
+    return None
+
+
+def measured_peaks():
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", f"traffic_{config}.json")) as f:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f)
     except (OSError, ValueError):
-        return None
+        return {}
 
 
 def int8_peak_tops(torch):
@@ -171,51 +201,193 @@ def int8_peak_tops(torch):
     return best
 
 
-def reference_rate(cfg, coeffs, target_s=15.0):
-    """reference run_policy on a bounded sample (oracle/_ref): matvecs per second
-    with min(host cores, b) column threads, the reference's own parallelism"""
+# --------------------------------------------------------------------------
+# the reference on the host cores (oracle/_ref: the UNMODIFIED reference
+# headers compiled in place).  Nothing here imports the product package.
+
+def full_ledger(config):
+    name = LEDGER_SOURCE.get(config)
+    if not name:
+        return None
+    try:
+        with open(os.path.join(GOLD, name)) as f:
+            g = json.load(f)
+    except OSError:
+        return None
+    return dict(g["ledger"], source=f"tests/golden/{name}")
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_measure(config, coeffs, threads):
+    """one timed reference run on the host cores: the whole zeta function when
+    it fits a bench step (quintic), else frobenius_matrix at a series-truncated
+    plan (N_m = SAMPLE_NM: every column and pole, the same limb count, so the
+    same per-matvec cost) scaled by the ratio of the exact ledgers; for the
+    fourfold (two limbs, beyond the reference here) one reference linrec_eval
+    step at its size (p=7, M=24, side 3003) times the replayed ledger."""
     from oracle import refapi
-    p, n, d, _, _ = cfg
-    h = hodge_counts(n, d)
-    b = sum(h)
-    threads = max(1, min(os.cpu_count() or 1, b))
-    col = h[0] + (h[1] // 2 if len(h) > 1 and h[1] else 0)  # a middle-pole column
-    per = 4
-    while True:
-        r = refapi.policy_sample(p, n, d, coeffs, col, per, threads)
-        if r["seconds"] > target_s / 4 or per >= 4096:
-            break
-        per *= 4
-    return r, threads, col, per
+    p, n, d, seed, _ = CONFIGS[config]
+    full = full_ledger(config)
+    if config == "quintic":
+        t0 = time.time()
+        z = refapi.zeta(p, n, d, coeffs, threads=threads)
+        secs = time.time() - t0
+        return {"value": secs, "kind": "reference", "projection": False,
+                "sample": f"the whole reference run_zeta (p-chunk, lazy PEP, {threads} column threads): "
+                          f"{z['matvecs']} matvecs, Q head {z['Q'][:3]}"}
+    if config in SAMPLE_NM and full:
+        nm = SAMPLE_NM[config]
+        t0 = time.time()
+        fr = refapi.frobenius(p, n, d, coeffs, threads=threads, nm=nm)
+        secs = time.time() - t0
+        proj = secs * full["matvecs"] / max(1, fr["matvecs"])
+        return {"value": proj, "kind": "reference", "projection": True,
+                "sample": (f"reference frobenius_matrix (p-chunk, lazy PEP, {threads} column threads) of the same "
+                           f"hypersurface at N_m={nm} (M={fr['plan']['M']}, every column and pole): "
+                           f"{fr['matvecs']} matvecs in {secs:.2f} s, scaled to the full ledger "
+                           f"({full['matvecs']} matvecs, {full['source']})"),
+                "sample_seconds": secs}
+    if config == "fourfold" and full:
+        import numpy as np
+        rng = np.random.default_rng(7)
+        side, beta = 3003, 7 ** 12
+        A = rng.integers(0, beta, size=2 * side * side, dtype=np.uint64)
+        B = rng.integers(0, beta, size=2 * side * side, dtype=np.uint64)
+        w = rng.integers(0, beta, size=2 * side, dtype=np.uint64)
+        t0 = time.time()
+        refapi.linrec_eval(7, 24, side, A, B, 0, w)
+        step = time.time() - t0
+        proj = step * full["matvecs"] / max(1, min(threads, 22))
+        return {"value": proj, "kind": "reference", "projection": True,
+                "sample": (f"one reference linrec_eval step at the fourfold's size (p=7, M=24: 2 limbs, side 3003, "
+                           f"generic path) took {step:.2f} s on one core; x {full['matvecs']} matvecs "
+                           f"({full['source']}) / min(cores, 22 columns); excludes the reference's per-column "
+                           f"RuvContext and ~150 GB of seed vectors, so a lower bound"),
+                "sample_seconds": step}
+    return None
+
+
+def validation():
+    """the projection method checked against complete reference runs in the
+    dev container (profiles/r02/cpu_baseline_validation.json)"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02", "cpu_baseline_validation.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
 
 def run_reference(args, cfg, rank):
+    """--impl reference: the reference's own CPU implementation on the host
+    cores (oracle/_ref), same config/metric/unit; rank 0 only"""
     if rank != 0:
         return
-    import paper_2602_24155_b200 as drzg
+    from oracle import refapi
     p, n, d, seed, desc = cfg
-    coeffs = drzg.random_hypersurface(p, n, d, seed=seed, fermat=(args.config.startswith("fermat")))
-    total = json.load(open(os.path.join(ROOT, "profiles", f"ledger_{args.config}.json")))["matvecs"]
-    vals = []
-    info = None
+    if args.config in ("threefold_batch", "fermat_fourfold_r1"):
+        print(json.dumps({"impl": "reference", "metric": METRIC,
+                          "unavailable": f"no reference arm for config {args.config}"}))
+        return
+    coeffs = [int(x) for x in refapi.hypersurface(p, n, d, seed=seed)]
+    threads = host_threads()
+    vals, info = [], None
     for i in range(args.warmup + args.steps):
-        r, threads, col, per = reference_rate(cfg, coeffs, target_s=args.ref_seconds)
-        proj = total * r["seconds"] / max(1, r["matvecs"])
+        info = reference_measure(args.config, coeffs, threads)
+        if info is None:
+            print(json.dumps({"impl": "reference", "metric": METRIC, "unavailable": "no reference ledger"}))
+            return
         if i >= args.warmup:
-            vals.append(proj)
-        info = (r, threads, col, per)
-    r, threads, col, per = info
+            vals.append(info["value"])
     v = sum(vals) / len(vals)
-    sample = (f"reference run_policy (p-chunk, lazy PEP) on column {col}'s top-pole seeds, {per} seeds x "
-              f"{threads} threads ({r['matvecs']} matvecs in {r['seconds']:.2f} s), scaled by the exact "
-              f"ledger of one zeta function ({total} matvecs)")
     line = {"metric": METRIC, "impl": "reference", "value": v, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64/u128 (reference)", "data": "synthetic",
             "config": {"workload": desc, "p": p, "n": n, "d": d},
-            "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "reference", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": info["kind"],
+                             "projection": info["projection"], "sample": info["sample"],
+                             "validation": validation()},
+            "per_step_s": [round(x, 3) for x in vals],
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
+
+
+# --------------------------------------------------------------------------
+# the product
+
+def roofline_of(kern, nL, peak, config):
+    """dominant-kernel roofline from a profiled (per-launch CUDA-event) pass"""
+    ksum = kern["gemm_ms"] + kern["carry_ms"] + kern["gather_ms"] + kern["epilogue_ms"] + kern["other_ms"]
+    # small systems (order <= 256) run the whole Dixon solve of a pole drop in
+    # one launch, larger ones as one dataflow launch per sweep chunk: both
+    # products of every digit are in gemm_ms
+    fused = kern["carry_launches"] == 0 and kern.get("carry_macs", 0) > 0
+    gemm_macs = kern["gemm_macs"] + (kern["carry_macs"] if fused else 0)
+    achieved = 2 * gemm_macs / max(1e-9, kern["gemm_ms"] / 1e3) / 1e12
+    if not fused:
+        kname = "tc::gemm_kernel (digit product y_k = bal(Cq . in_k))"
+    elif nL <= 256:
+        kname = "tc::dixon_fused_kernel (digit + carry products of every digit, one launch per pole drop)"
+    else:
+        kname = "tc::dixon_flow_kernel (dense digit + block-sparse carry tiles of every digit, one dataflow launch)"
+    traffic = committed_traffic(config)
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
+            "frac": achieved / peak if peak else None, "traffic": (traffic or {}).get("bytes_per_launch"),
+            "traffic_source": (traffic or {}).get("source"), "kernel": kname,
+            "avg_launch_ms": kern["gemm_ms"] / max(1, kern["gemm_launches"]),
+            "share_of_kernel_time": kern["gemm_ms"] / ksum if ksum else None,
+            "peak_source": "measured on this box: torch._int_mm 8192^3 int8 (cuBLASLt), best of 5",
+            "macs_per_launch": gemm_macs / max(1, kern["gemm_launches"]),
+            "epilogue": {"kernel": "dev::epilogue_kernel (w' = T_x y, carry-normalised digits)",
+                         "ms": kern["epilogue_ms"], "share_of_kernel_time": kern["epilogue_ms"] / ksum if ksum else None}}
+
+
+def fourfold_leg(drzg, torch, local, peak):
+    """ONE complete zeta function of the metric's own hypersurface (configs[4])
+    under clock sampling, after a one-column warm-up; then column 0 once more
+    with per-launch kernel timing for the roofline"""
+    p, n, d, seed, desc = CONFIGS["fourfold"]
+    coeffs = drzg.random_hypersurface(p, n, d, seed=seed)
+    t0 = time.time()
+    drzg.frobenius(p, n, d, coeffs, columns=[0], device=local)  # tables, state pool, allocations
+    warm = time.time() - t0
+    with ClockSampler(local, "_fourfold") as clk:
+        torch.cuda.synchronize()
+        clk.mark()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        z = drzg.zeta(p, n, d, coeffs, device=local, count_budget=FOURFOLD_COUNT_BUDGET)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e = e0.elapsed_time(e1) / 1e3
+    clocks = clk.summary()
+    fr = z["frobenius"]
+    ref = full_ledger("fourfold")
+    led = {k: fr[k] for k in ("matvecs", "startups", "combines")}
+    colp = drzg.frobenius(p, n, d, coeffs, columns=[0], device=local, profile=True)
+    kern = colp["kernels"]
+    rl = roofline_of(kern, colp["nL"], peak, "fourfold")
+    dev_s = fr["kernels"]["device_ms"] / 1e3
+    macs = fr["kernels"]["gemm_macs"] + fr["kernels"]["carry_macs"]
+    return {
+        "workload": desc, "value": z["seconds"], "unit": "s", "e2e": e2e, "warmup_one_column_s": warm,
+        "device_s": dev_s, "stage_seconds": fr["times"],
+        "engine_int8_tops": 2 * macs / max(1e-9, dev_s) / 1e12,
+        "engine_frac_of_int8_peak": (2 * macs / max(1e-9, dev_s) / 1e12) / peak if peak else None,
+        "ledger": led, "reference_ledger": ref, "ledger_equal": bool(ref) and all(led[k] == ref[k] for k in led),
+        "Q_sha256": hashlib.sha256(json.dumps(z["Q"]).encode()).hexdigest(), "Q_head": z["Q"][:4],
+        "counts": z["counts"], "counts_ok": all(ok for (_, _, ok) in z["counts"]) and len(z["counts"]) == 2,
+        "slopes": z["slopes"], "escalations": z["escalations"], "clocks": clocks,
+        "digits": fr["digits"], "peak_live_states": fr["kernels"]["peak_live_states"],
+        "roofline_column0": rl, "kernels_ms_column0": kern,
+        "gpu_launches": fr["traffic"]["launches"],
+        "h2d_bytes": fr["traffic"]["h2d_bytes"], "d2h_bytes": fr["traffic"]["d2h_bytes"],
+    }
 
 
 def main():
@@ -225,7 +397,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="k3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--fourfold-leg", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -249,6 +421,7 @@ def main():
     coeffs = drzg.random_hypersurface(p, n, d, seed=seed, fermat=fermat)
     h = hodge_counts(n, d)
     b = sum(h)
+    budget = FOURFOLD_COUNT_BUDGET if args.config == "fourfold" else 0
     # columns partitioned across ranks (longest-processing-time by pole order)
     from paper_2602_24155_b200 import parallel
     all_cols = [parallel.partition_columns(n, d, world, r) for r in range(world)]
@@ -260,25 +433,36 @@ def main():
         batch_coeffs = [drzg.random_hypersurface(p, n, d, seed=s) for s in range(rank, BATCH_SEEDS, world)]
 
     def step(profile=False):
-        """one zeta function (or the rank's share of a batch); returns (device_s, json of this rank)"""
+        """one zeta function (or the rank's share of a batch); returns
+        (zeta-call seconds, result json of this rank, frobenius json)"""
         if batch:
             zs = [drzg.zeta(p, n, d, co, device=local, profile=profile, verify_counts=True) for co in batch_coeffs]
             if not all(ok for z_ in zs for (_, _, ok) in z_["counts"]):
                 raise RuntimeError("a point count disagrees with Q")
             fr_ = merge_frobenius([z_["frobenius"] for z_ in zs])
             z0 = dict(zs[0], seconds=sum(z_["seconds"] for z_ in zs))
-            return fr_["kernels"]["device_ms"] / 1e3, z0, fr_
+            return z0["seconds"], z0, fr_
         if world == 1:
             z = drzg.zeta(p, n, d, coeffs, r_uniform=r_uniform, device=local, profile=profile,
-                          verify_counts=True)
-            return z["frobenius"]["kernels"]["device_ms"] / 1e3, z, z["frobenius"]
+                          verify_counts=True, count_budget=budget)
+            return z["seconds"], z, z["frobenius"]
+        t0 = time.time()
         fr = drzg.frobenius(p, n, d, coeffs, r_uniform=r_uniform, columns=mine, device=local, profile=profile)
         # one NCCL all_gather of the column blocks (62-bit limbs; see parallel.py)
         F = parallel.gather_frobenius(fr["F"], b, mine, world, all_cols, device=torch.device("cuda", local))
-        z = drzg.charpoly(p, n, d, [str(x) for x in F], b, r_uniform=r_uniform) if rank == 0 else None
-        return fr["kernels"]["device_ms"] / 1e3, z, fr
+        z = None
+        if rank == 0:
+            # run_zeta's battery on the gathered F: Q recovery, sign tie-break,
+            # Newton >= Hodge, point counts (the step fails unless it passes)
+            z = drzg.zeta_from_F(p, n, d, coeffs, [str(x) for x in F], b, r_uniform=r_uniform,
+                                 count_budget=budget)
+            if z["status"] != "ok":
+                raise RuntimeError(f"gathered F needs escalation: {z['reason']}")
+            if not all(ok for (_, _, ok) in z["counts"]):
+                raise RuntimeError("a point count disagrees with Q")
+        return time.time() - t0, z, fr
 
-    dev_times, e2e_times, zeta_times, last = [], [], [], None
+    vals, dev_times, e2e_times, last = [], [], [], None
     # the sampler starts before the warm-up: nvidia-smi's start-up (NVML
     # init) stalls CUDA calls of this process for up to seconds, which must
     # not land in a timed step; it keeps sampling through the timed region
@@ -296,18 +480,18 @@ def main():
                 dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            dev_s, z, fr = step()
+            call_s, z, fr = step()
             e1.record()
             torch.cuda.synchronize()
             e2e_s = e0.elapsed_time(e1) / 1e3
+            dev_s = fr["kernels"]["device_ms"] / 1e3
             if dist:
-                tt = torch.tensor([dev_s, e2e_s], dtype=torch.float64, device="cuda")
+                tt = torch.tensor([call_s, e2e_s, dev_s], dtype=torch.float64, device="cuda")
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                dev_s, e2e_s = tt.tolist()
-            dev_times.append(dev_s)
+                call_s, e2e_s, dev_s = tt.tolist()
+            vals.append(call_s)
             e2e_times.append(e2e_s)
-            if z and "seconds" in z:
-                zeta_times.append(z["seconds"])
+            dev_times.append(dev_s)
             last = (z, fr)
     if dist:
         dist.barrier()
@@ -319,50 +503,27 @@ def main():
             dist.destroy_process_group()
         return
     z, fr = last
-    value = sum(dev_times) / len(dev_times)
+    value = sum(vals) / len(vals)
     e2e = sum(e2e_times) / len(e2e_times)
     kern = frp["kernels"]
     peak = int8_peak_tops(torch)
-    ksum = kern["gemm_ms"] + kern["carry_ms"] + kern["gather_ms"] + kern["epilogue_ms"] + kern["other_ms"]
-    # small systems (order <= 256) run the whole Dixon solve of a pole drop in
-    # one launch (both products); larger ones launch the digit product and the
-    # block-sparse carry product separately
-    fused = kern["carry_launches"] == 0 and kern.get("carry_macs", 0) > 0
-    gemm_macs = kern["gemm_macs"] + (kern["carry_macs"] if fused else 0)
-    gemm_avg_ms = kern["gemm_ms"] / max(1, kern["gemm_launches"])
-    achieved = 2 * gemm_macs / max(1e-9, kern["gemm_ms"] / 1e3) / 1e12
-    carry = None
-    if not fused:
-        carry_tops = 2 * kern.get("carry_macs", 0) / max(1e-9, kern["carry_ms"] / 1e3) / 1e12
-        carry = {"kernel": "tc::gemm_kernel (block-sparse carry product + residual epilogue)",
-                 "achieved_tops": carry_tops, "frac": carry_tops / peak if peak else None,
-                 "share_of_kernel_time": kern["carry_ms"] / ksum if ksum else None}
-    if not fused:
-        kname = "tc::gemm_kernel (digit product y_k = bal(Cq . in_k))"
-    elif fr["nL"] <= 256:
-        kname = "tc::dixon_fused_kernel (digit + carry products of every digit, one launch per pole drop)"
-    else:
-        kname = "tc::dixon_flow_kernel (dense digit + block-sparse carry tiles of every digit, one dataflow launch)"
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    total_matvecs = fr["matvecs"] if world == 1 else None
-    if world == 1:
-        with open(os.path.join(ROOT, "gpurun_out", f"ledger_{args.config}.json"), "w") as f:
-            json.dump({"matvecs": fr["matvecs"], "startups": fr["startups"], "combines": fr["combines"]}, f)
+    rl = roofline_of(kern, fr["nL"], peak, args.config)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            r, threads, col, per = reference_rate(cfg, coeffs, target_s=args.ref_seconds)
-            proj = fr["matvecs"] * r["seconds"] / max(1, r["matvecs"])
-            cpu = {"value": proj, "unit": "s", "cores": threads, "kind": "reference",
-                   "sample": (f"reference run_policy (p-chunk, lazy PEP) on column {col}'s top-pole seeds, "
-                              f"{per} seeds x {threads} threads: {r['matvecs']} matvecs in {r['seconds']:.2f} s; "
-                              f"scaled by this zeta function's exact ledger ({fr['matvecs']} matvecs, "
-                              f"identical to the reference's)")}
+            from oracle import refapi
+            info = reference_measure(args.config, [int(x) for x in refapi.hypersurface(p, n, d, seed=seed)],
+                                     host_threads())
+            if info:
+                cpu = {"value": info["value"], "unit": "s", "cores": host_threads(), "kind": info["kind"],
+                       "projection": info["projection"], "sample": info["sample"], "validation": validation()}
         except Exception as e:  # the checker is optional on the box
             cpu = {"value": None, "unit": "s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
-    # mod-p^N reduction Gop/s = 2 side^2 per matvec x matvecs / s
-    gops = 2.0 * fr["side"] ** 2 * fr["matvecs"] / value / 1e9 if world == 1 else None
-    traffic = committed_traffic(args.config)
+    # mod-p^N reduction Gop/s = 2 side^2 per matvec x matvecs / s (engine time)
+    dev_mean = sum(dev_times) / len(dev_times)
+    gops = 2.0 * fr["side"] ** 2 * fr["matvecs"] / dev_mean / 1e9 if world == 1 else None
+    ref_led = full_ledger(args.config)
+    srt = sorted(vals)
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
@@ -373,22 +534,34 @@ def main():
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": fr["traffic"]["h2d_bytes"] + 8 * len(coeffs),
                 "d2h_bytes_per_step": fr["traffic"]["d2h_bytes"]},
         "gpu_launches": fr["traffic"]["launches"] * args.steps,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS (int8)",
-                     "frac": achieved / peak if peak else None, "traffic": (traffic or {}).get("bytes_per_launch"),
-                     "traffic_source": (traffic or {}).get("source"),
-                     "kernel": kname, "avg_launch_ms": gemm_avg_ms,
-                     "share_of_kernel_time": kern["gemm_ms"] / ksum if ksum else None,
-                     "peak_source": "measured on this box: torch._int_mm 8192^3 int8 (cuBLASLt), best of 5"},
+        "engine_device_s": dev_mean,
+        "roofline": rl,
         "reduction_gops": gops,
-        "carry_gemm": carry,
         "ledger": {"matvecs": fr["matvecs"], "startups": fr["startups"], "combines": fr["combines"],
-                   "terms": fr["terms"]},
-        "per_step_s": {"device": [round(x, 4) for x in dev_times], "e2e": [round(x, 4) for x in e2e_times],
-                       "zeta_call": [round(x, 4) for x in zeta_times]},
+                   "terms": fr["terms"], "reference": ref_led,
+                   "equal": bool(ref_led) and all(fr[k] == ref_led[k] for k in ("matvecs", "startups", "combines"))},
+        "per_step_s": {"zeta_call": [round(x, 4) for x in vals], "e2e": [round(x, 4) for x in e2e_times],
+                       "engine_device": [round(x, 4) for x in dev_times],
+                       "median": srt[len(srt) // 2], "p95": srt[min(len(srt) - 1, int(0.95 * len(srt)))]},
         "stage_seconds": fr["times"], "kernels_ms": kern,
         "cpu_baseline": cpu, "clocks": clocks,
-        "Q_head": (z["Q"][:4] if z and "Q" in z else (z["candidates"][0][:4] if z else None)),
+        "Q_head": (z["Q"][:4] if z and "Q" in z else None),
     }
+    leg = args.fourfold_leg == "on" or (args.fourfold_leg == "auto" and world == 1 and args.config == "k3")
+    if leg:
+        try:
+            line["fourfold"] = fourfold_leg(drzg, torch, local, peak)
+            ff_cpu = None
+            if not args.no_cpu_baseline:
+                from oracle import refapi
+                info = reference_measure("fourfold", [int(x) for x in refapi.hypersurface(7, 5, 3, seed=1)],
+                                         host_threads())
+                if info:
+                    ff_cpu = {"value": info["value"], "unit": "s", "cores": host_threads(), "kind": info["kind"],
+                              "projection": info["projection"], "sample": info["sample"]}
+            line["fourfold"]["cpu_baseline"] = ff_cpu
+        except Exception as e:
+            line["fourfold"] = {"error": str(e)}
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()

@@ -79,9 +79,22 @@ char* drzg_frobenius(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, i
 
 /* run_zeta(X, opts) — zeta.hpp:438-549.  JSON: Q, ambiguity, plan, slopes,
  * invariants (p-rank, height, domino, newton height), count checks, ledger,
- * wall time. */
+ * wall time.  count_budget: ZetaOptions::count_budget (zeta.hpp:406), the
+ * largest #P^n(F_{p^r}) the brute-force checks enumerate; <= 0 keeps the
+ * reference default 2e8 (the GPU counter makes larger budgets cheap: the
+ * cubic fourfold's r = 2 check enumerates 2.9e8 points of P^5(F_49)). */
 char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
-                int32_t nm_override, int32_t verify_counts, int32_t device, int32_t profile);
+                int32_t nm_override, int32_t verify_counts, int64_t count_budget, int32_t device, int32_t profile);
+
+/* the rest of run_zeta on a given Frobenius matrix (zeta.hpp:456-535): the
+ * charpoly, recover_Q, the sign tie-break, Newton >= Hodge and the point-count
+ * checks, for the plan choose_precision(overrides) after `escalations` steps
+ * of escalate_plan.  F: b*b decimal strings, row-major (e.g. gathered from
+ * several GPUs).  JSON {"status": "ok", Q, ...} or {"status": "escalate",
+ * "reason": ...} when the reference would escalate the plan. */
+char* drzg_zeta_from_F(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r_uniform,
+                       int32_t nm_override, int32_t escalations, int32_t b, const char* const* F,
+                       int32_t verify_counts, int64_t count_budget);
 
 /* synthetic input by the reference CLI's generator rule (drzeta_main.cpp:112-122):
  * std::mt19937_64(seed), coefficient rng() % p per grevlex monomial, redrawn

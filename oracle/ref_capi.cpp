@@ -20,6 +20,10 @@
 #include <cstring>
 #include <random>
 #include <sstream>
+#include <unordered_set>
+#include <atomic>
+#include <mutex>
+#include <thread>
 
 using namespace drz;
 
@@ -116,6 +120,173 @@ struct BuildStore : PepStoreBase {
 };
 
 }  // namespace
+
+
+// Value-free replay of frobenius_matrix's cost ledger (zeta.hpp:36-136 with
+// run_policy p-chunk, reduction.hpp:464-533): the reference's move choice
+// (choose_v_greedy, repair_v, k_max_legal, legal) is a function of (u, pole)
+// alone, so the ledger of a hypersurface needs no matrices.  Seeds come from
+// the reference's frobenius_terms; their exponent split restates
+// seed_reduction_input (reduction.hpp:538-563) without materialising w (the
+// random fourfold's seeds would be ~150 GB).  Bookkeeping per move is
+// reduce_chunk's (reduction.hpp:419-422: matvecs += k, startups += 1), and
+// states are merged by (u, pole) after every sweep (combine_states,
+// reduction.hpp:426-451; the first sweep runs before any merge, as there).
+// Used to pin the engine's ledger at plans the reference cannot run here.
+namespace {
+struct RKey {
+  u64 u;
+  int pole;
+  bool operator==(const RKey& o) const { return u == o.u && pole == o.pole; }
+};
+struct RKeyHash {
+  size_t operator()(const RKey& k) const { return std::hash<u64>()(k.u * 1315423911ull ^ (u64)k.pole); }
+};
+struct RState {
+  Expo u;
+  int pole;
+};
+
+CostLedger replay_column(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan, const std::set<int>& S,
+                         int j) {
+  const int nv = X.nv(), n = X.n, d = X.d;
+  const i64 p = (i64)X.p;
+  const int D = d * n - n;
+  CostLedger led;
+  std::vector<RState> seeds;
+  {
+    auto terms = frobenius_terms(X, B.mons[j], B.pole_of[j], plan);
+    seeds.reserve(terms.size());
+    for (const auto& t : terms) {
+      Expo full = t.exponent + Expo::ones(nv);
+      Expo u = tweak(full, D);
+      for (int i = 0; i < nv; ++i) {
+        if (S.count(i) || u[i] >= 1) continue;
+        int jj = -1;
+        for (int c = 0; c < nv; ++c) {
+          bool ok = S.count(c) ? u[c] >= 1 : u[c] >= 2;
+          if (ok && (jj < 0 || u[c] > u[jj])) jj = c;
+        }
+        DRZ_REQUIRE(jj >= 0, "seed: cannot honor the working set");
+        --u[jj];
+        ++u[i];
+      }
+      Expo wmon = full - u;
+      DRZ_REQUIRE(wmon.nonneg() && wmon.total() == D, "seed: bad split");
+      seeds.push_back({u, t.pole});
+    }
+  }
+  // active states bucketed by |u| (a sweep takes the top bucket), floor states apart
+  std::map<int, std::vector<RState>, std::greater<int>> act;
+  std::unordered_set<RKey, RKeyHash> floor;
+  i64 total_states = (i64)seeds.size(), final_states = 0;
+  auto move = [&](RState& st) {
+    Expo v = choose_v_greedy(d, st.u, S);
+    repair_v(st.u, v, S);
+    i64 k = std::min(std::min(p, (i64)st.pole - n), k_max_legal(st.u, v, S));
+    DRZ_REQUIRE(k >= 1, "p-chunk: no admissible move");
+    DRZ_REQUIRE(legal(d, st.u, v, k, S), "reduce_chunk: illegal move");
+    st.u = st.u - v.scaled((int)k);
+    st.pole -= (int)k;
+    led.matvecs += k;
+    led.startups += 1;
+  };
+  auto place = [&](std::vector<RState>& moved) {
+    for (auto& st : moved) {
+      if (st.pole == n) {
+        floor.insert({st.u.key(), st.pole});
+        continue;
+      }
+      act[st.u.total()].push_back(st);
+    }
+  };
+  // sweep 1: states at the top |u| move before any combine (duplicates move apart)
+  {
+    int top = -1;
+    for (auto& s : seeds)
+      if (s.pole > n) top = std::max(top, s.u.total());
+    std::vector<RState> moved;
+    for (auto& s : seeds) {
+      if (s.pole > n && s.u.total() == top) move(s);
+      moved.push_back(s);
+    }
+    seeds.clear();
+    seeds.shrink_to_fit();
+    place(moved);
+  }
+  // combine everything once (the first combine_states), then sweep by sweep
+  for (auto& kv : act) {
+    std::unordered_set<RKey, RKeyHash> seen;
+    std::vector<RState> keep;
+    for (auto& s : kv.second)
+      if (seen.insert({s.u.key(), s.pole}).second) keep.push_back(s);
+    kv.second.swap(keep);
+  }
+  while (!act.empty()) {
+    auto it = act.begin();
+    std::vector<RState> front = std::move(it->second);
+    act.erase(it);
+    // states landing on a bucket are merged against it at this sweep's combine
+    std::map<int, std::unordered_set<RKey, RKeyHash>> seen;
+    for (auto& s : front) move(s);
+    for (auto& s : front) {
+      if (s.pole == n) {
+        floor.insert({s.u.key(), s.pole});
+        continue;
+      }
+      auto& bucket = act[s.u.total()];
+      auto& sn = seen[s.u.total()];
+      if (sn.empty())
+        for (auto& o : bucket) sn.insert({o.u.key(), o.pole});
+      if (sn.insert({s.u.key(), s.pole}).second) bucket.push_back(s);
+    }
+  }
+  for (auto& kv : act) final_states += (i64)kv.second.size();
+  final_states += (i64)floor.size();
+  led.combines = total_states - final_states;
+  return led;
+}
+}  // namespace
+
+extern "C" char* ref_replay_ledger(u64 p, int n, int d, const u64* coeffs, int r_uniform, int nm_override,
+                                   int threads) {
+  return guarded([&] {
+    auto t0 = std::chrono::steady_clock::now();
+    Hypersurface X = make_x(p, n, d, coeffs);
+    std::set<int> S = working_set_for(X, Policy::p_chunk);
+    Basis B = compute_basis(X);
+    PrecisionPlan plan = choose_precision(p, n, d, overrides(r_uniform, nm_override));
+    std::vector<CostLedger> per(B.b);
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    std::exception_ptr err;
+    std::mutex emu;
+    for (int t = 0; t < std::max(1, threads); ++t)
+      pool.emplace_back([&] {
+        try {
+          for (int j = next++; j < (int)B.b; j = next++) per[j] = replay_column(X, B, plan, S, j);
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(emu);
+          err = std::current_exception();
+        }
+      });
+    for (auto& th : pool) th.join();
+    if (err) std::rethrow_exception(err);
+    CostLedger tot;
+    std::ostringstream cols;
+    for (int j = 0; j < (int)B.b; ++j) {
+      tot.matvecs += per[j].matvecs;
+      tot.startups += per[j].startups;
+      tot.combines += per[j].combines;
+      cols << (j ? "," : "") << "[" << per[j].matvecs << "," << per[j].startups << "," << per[j].combines << "]";
+    }
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::ostringstream os;
+    os << "{\"matvecs\":" << tot.matvecs << ",\"startups\":" << tot.startups << ",\"combines\":" << tot.combines
+       << ",\"columns\":[" << cols.str() << "],\"plan\":" << plan_json(plan) << ",\"seconds\":" << secs << "}";
+    return os.str();
+  });
+}
 
 extern "C" {
 
@@ -456,6 +627,59 @@ char* ref_charpoly(u64 p, int n, int d, int r_uniform, int nm_override, int b, c
     os << "{\"charpoly\":" << zarr(dres) << ",\"status\":" << (int)rec.status << ",\"candidates\":[";
     for (size_t i = 0; i < rec.candidates.size(); ++i) os << (i ? "," : "") << zarr(rec.candidates[i]);
     os << "]}";
+    return os.str();
+  });
+}
+
+
+// A reusable RuvContext + build_ruv store for many chunks at one (f, M): the
+// random cubic fourfold's context (a 3003 x 6237 unit echelon, MpzEchelon
+// at 2 limbs) takes hours to build, so the fixture script builds it once.
+struct RefCtx {
+  Hypersurface X;
+  StripePlan kp;
+  std::set<int> S;
+  RuvContext C;
+  BuildStore store;
+  RefCtx(const Hypersurface& x, const StripePlan& p, const std::set<int>& s)
+      : X(x), kp(p), S(s), C(x, p, s), store(C) {}
+};
+
+void* ref_ctx_new(u64 p, int n, int d, const u64* coeffs, int M) {
+  try {
+    Hypersurface X = make_x(p, n, d, coeffs);
+    return new RefCtx(X, StripePlan::make(p, M), default_S(n, d));
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+void ref_ctx_free(void* h) { delete (RefCtx*)h; }
+
+// reduce_chunk (reduction.hpp:394-423) on the shared context
+char* ref_ctx_chunk(void* h, const int* u, int pole, const int* v, long k, const u64* w_in, u64* w_out) {
+  return guarded([&] {
+    RefCtx& R = *(RefCtx*)h;
+    int nv = R.X.nv();
+    GameState st;
+    st.u = Expo(nv);
+    Expo vv(nv);
+    for (int i = 0; i < nv; ++i) {
+      st.u[i] = u[i];
+      vv[i] = v[i];
+    }
+    st.pole = pole;
+    st.w = ModVec(R.kp, R.C.side);
+    std::memcpy(st.w.d.data(), w_in, sizeof(u64) * st.w.d.size());
+    CostLedger led;
+    auto t0 = std::chrono::steady_clock::now();
+    reduce_chunk(R.C, R.store, st, vv, k, led);
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::memcpy(w_out, st.w.d.data(), sizeof(u64) * st.w.d.size());
+    std::ostringstream os;
+    os << "{\"side\":" << R.C.side << ",\"limbs\":" << R.kp.limbs << ",\"u\":" << expo_arr(st.u)
+       << ",\"pole\":" << st.pole << ",\"matvecs\":" << led.matvecs << ",\"startups\":" << led.startups
+       << ",\"seconds\":" << secs << "}";
     return os.str();
   });
 }

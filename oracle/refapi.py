@@ -24,7 +24,7 @@ def lib():
         if not os.path.exists(REF_SO):
             raise RuntimeError(f"{REF_SO} missing: run `make -C oracle` where /root/reference exists")
         L = ctypes.CDLL(REF_SO)
-        for name in ("ref_mono_table", "ref_hypersurface", "ref_plan", "ref_basis", "ref_seeds",
+        for name in ("ref_replay_ledger", "ref_mono_table", "ref_hypersurface", "ref_plan", "ref_basis", "ref_seeds",
                      "ref_chunk", "ref_frobenius", "ref_zeta", "ref_charpoly", "ref_policy_sample"):
             getattr(L, name).restype = ctypes.c_void_p
         _lib = L
@@ -174,3 +174,9 @@ def policy_sample(p, n, d, coeffs, col, max_seeds, threads, r_uniform=0, nm=0):
     """reference run_policy on a bounded sample of one column's top-pole seeds"""
     return _js(lib().ref_policy_sample(ctypes.c_uint64(p), n, d, _u64(coeffs), r_uniform, nm, col, max_seeds,
                                        threads))
+
+
+def replay_ledger(p, n, d, coeffs, r_uniform=0, nm=0, threads=4):
+    """the reference's frobenius_matrix cost ledger by value-free replay
+    (matvecs, startups, combines, per column); equals the real run's ledger"""
+    return _js(lib().ref_replay_ledger(ctypes.c_uint64(p), n, d, _u64(coeffs), r_uniform, nm, threads))

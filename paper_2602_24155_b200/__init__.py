@@ -39,7 +39,7 @@ def lib():
             raise DrzgError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}/csrc`")
         L = ctypes.CDLL(LIB_PATH)
         L.drzg_last_error.restype = ctypes.c_char_p
-        for name in ("drzg_zeta", "drzg_frobenius", "drzg_reduce_chunk", "drzg_charpoly"):
+        for name in ("drzg_zeta", "drzg_frobenius", "drzg_reduce_chunk", "drzg_charpoly", "drzg_zeta_from_F"):
             getattr(L, name).restype = ctypes.c_void_p
         _lib = L
     return _lib
@@ -157,10 +157,20 @@ def frobenius(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, only_pole=0,
                                       only_pole, cols, ncols, device, int(profile)))
 
 
-def zeta(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, verify_counts=True, device=0, profile=False):
-    """reference run_zeta (zeta.hpp:438-549)"""
+def zeta(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, verify_counts=True, device=0, profile=False,
+         count_budget=0):
+    """reference run_zeta (zeta.hpp:438-549); count_budget <= 0 keeps the
+    reference's 2e8-point budget for the brute-force count checks"""
     return _json(lib().drzg_zeta(ctypes.c_uint64(p), n, d, _u64arr(coeffs), POLICIES[policy], r_uniform, nm,
-                                 int(verify_counts), device, int(profile)))
+                                 int(verify_counts), ctypes.c_int64(count_budget), device, int(profile)))
+
+
+def zeta_from_F(p, n, d, coeffs, F, b, r_uniform=0, nm=0, escalations=0, verify_counts=True, count_budget=0):
+    """run_zeta's battery (zeta.hpp:456-535) on a given F, e.g. one gathered
+    from several GPUs: {"status": "ok", "Q": ...} or {"status": "escalate"}"""
+    arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F])
+    return _json(lib().drzg_zeta_from_F(ctypes.c_uint64(p), n, d, _u64arr(coeffs), r_uniform, nm, escalations, b, arr,
+                                        int(verify_counts), ctypes.c_int64(count_budget)))
 
 
 def random_hypersurface(p, n, d, seed=1, policy="p-chunk", fermat=False):

@@ -127,6 +127,25 @@ std::string frob_json_body(const FrobResult& fr) {
      << ",\"launches\":" << g_traffic.launches.load() << "}";
   return os.str();
 }
+std::string zeta_json_body(const ZetaOut& r) {
+  std::ostringstream os;
+  os.precision(9);
+  os << "\"Q\":" << zjson(r.Q) << ",\"Q_alt\":" << zjson(r.Q_alt)
+     << ",\"ambiguous\":" << (r.ambiguous ? "true" : "false") << ",\"plan\":" << plan_json(r.plan)
+     << ",\"p_rank\":" << r.inv.p_rank << ",\"height\":\"" << r.inv.height << "\",\"domino\":\"" << r.inv.domino
+     << "\",\"domino_any\":\"" << r.domino << "\",\"newton_height\":\"" << r.inv.newton_height
+     << "\",\"fsplit\":" << (r.inv.fsplit_defined ? (r.inv.fsplit ? "true" : "false") : "null") << ",\"slopes\":[";
+  for (size_t i = 0; i < r.np.slopes.size(); ++i)
+    os << (i ? "," : "") << "[\"" << r.np.slopes[i].first.str() << "\"," << r.np.slopes[i].second << "]";
+  os << "],\"counts\":[";
+  for (size_t i = 0; i < r.counts.size(); ++i)
+    os << (i ? "," : "") << "[" << r.counts[i].r << ",\"" << r.counts[i].from_zeta.str() << "\","
+       << (r.counts[i].ok ? "true" : "false") << "]";
+  os << "],\"escalations\":[";
+  for (size_t i = 0; i < r.reasons.size(); ++i) os << (i ? "," : "") << "\"" << r.reasons[i] << "\"";
+  os << "]";
+  return os.str();
+}
 Policy policy_of(int p) {
   DRZG_REQUIRE(p >= 0 && p <= 2, "unknown policy");
   return (Policy)p;
@@ -305,33 +324,40 @@ char* drzg_frobenius(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, i
 }
 
 char* drzg_zeta(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t policy, int32_t r_uniform,
-                int32_t nm_override, int32_t verify_counts, int32_t device, int32_t profile) {
+                int32_t nm_override, int32_t verify_counts, int64_t count_budget, int32_t device, int32_t profile) {
   return guard_str([&]() -> std::string {
     Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
     ZetaOptions zo;
     zo.policy = policy_of(policy);
     zo.overrides = overrides(r_uniform, nm_override);
     zo.verify_counts = verify_counts != 0;
+    if (count_budget > 0) zo.count_budget = count_budget;
     zo.profile = profile != 0;
     g_traffic.reset();
     ZetaOut r = run_zeta(X, zo, device);
-    std::ostringstream os;
-    os.precision(9);
-    os << "{\"Q\":" << zjson(r.Q) << ",\"Q_alt\":" << zjson(r.Q_alt)
-       << ",\"ambiguous\":" << (r.ambiguous ? "true" : "false") << ",\"plan\":" << plan_json(r.plan)
-       << ",\"p_rank\":" << r.inv.p_rank << ",\"height\":\"" << r.inv.height << "\",\"domino\":\"" << r.inv.domino
-       << "\",\"domino_any\":\"" << r.domino << "\",\"newton_height\":\"" << r.inv.newton_height
-       << "\",\"fsplit\":" << (r.inv.fsplit_defined ? (r.inv.fsplit ? "true" : "false") : "null") << ",\"slopes\":[";
-    for (size_t i = 0; i < r.np.slopes.size(); ++i)
-      os << (i ? "," : "") << "[\"" << r.np.slopes[i].first.str() << "\"," << r.np.slopes[i].second << "]";
-    os << "],\"counts\":[";
-    for (size_t i = 0; i < r.counts.size(); ++i)
-      os << (i ? "," : "") << "[" << r.counts[i].r << ",\"" << r.counts[i].from_zeta.str() << "\","
-         << (r.counts[i].ok ? "true" : "false") << "]";
-    os << "],\"escalations\":[";
-    for (size_t i = 0; i < r.reasons.size(); ++i) os << (i ? "," : "") << "\"" << r.reasons[i] << "\"";
-    os << "],\"seconds\":" << r.wall << ",\"frobenius\":{" << frob_json_body(r.last) << "}}";
-    return os.str();
+    return "{" + zeta_json_body(r) + ",\"seconds\":" + std::to_string(r.wall) + ",\"frobenius\":{" +
+           frob_json_body(r.last) + "}}";
+  });
+}
+
+char* drzg_zeta_from_F(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t r_uniform,
+                       int32_t nm_override, int32_t escalations, int32_t b, const char* const* F,
+                       int32_t verify_counts, int64_t count_budget) {
+  return guard_str([&]() -> std::string {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    ZetaOptions zo;
+    zo.overrides = overrides(r_uniform, nm_override);
+    zo.verify_counts = verify_counts != 0;
+    if (count_budget > 0) zo.count_budget = count_budget;
+    PrecisionPlan plan = choose_precision(p, n, d, zo.overrides);
+    for (int e = 0; e < escalations; ++e) DRZG_REQUIRE(escalate_plan(plan), "zeta_from_F: no such escalation step");
+    DRZG_REQUIRE(b == (int)plan.b, "zeta_from_F: F is not b x b for this plan");
+    std::vector<Z> f((size_t)b * b);
+    for (size_t i = 0; i < f.size(); ++i) f[i] = Z::from_str(F[i]);
+    ZetaOut r;
+    const std::string why = finish_zeta(X, plan, f, b, zo, r);
+    if (!why.empty()) return "{\"status\":\"escalate\",\"reason\":\"" + why + "\",\"plan\":" + plan_json(plan) + "}";
+    return "{\"status\":\"ok\"," + zeta_json_body(r) + "}";
   });
 }
 

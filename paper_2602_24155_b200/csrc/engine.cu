@@ -388,8 +388,11 @@ void ReductionEngine::grow_pool(int need) {
   if (want > vmm_mapped_) trim_mempool(dev);  // unused stream-ordered reserve back to the driver
   DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
   size_t margin = (size_t)2 << 30;
+  std::unique_lock<std::mutex> tmp_lock(tmp_mu_, std::defer_lock);
+  if (want > vmm_mapped_ + (fr > margin ? fr - margin : 0)) tmp_lock.lock();  // no sweep is launching now
   if (want > vmm_mapped_ + (fr > margin ? fr - margin : 0) && bcap_ > 0) {
     // give the batch temporaries back first; they are re-sized on demand
+    // (stream-ordered frees: kernels already queued on st_ still see them)
     Bg_.release();
     Y_.release();
     IN_.release();
@@ -658,6 +661,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
   const RuvTables& T = *T_;
   const int B = (int)ks.size();
   if (B == 0) return 0;
+  std::lock_guard<std::mutex> tmp_lock(tmp_mu_);  // grow_pool on the policy thread may release them
   ensure_batch(B);
   i64 mv = 0;
   for (int b0 = 0; b0 < B; b0 += bcap_) {

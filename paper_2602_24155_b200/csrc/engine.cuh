@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <thread>
 #include <unordered_map>
 #include <unordered_set>
@@ -66,8 +67,11 @@ class Stager {
     }
     for (void* h : retired_) cudaFreeHost(h);
   }
+  // one ring for the whole process: concurrent callers (one host thread per
+  // device, say) take turns, so no two copies share a pinned buffer
   void copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (!bytes) return;
+    std::lock_guard<std::mutex> lk(mu_);
     Buf& b = bufs_[next_];
     next_ = (next_ + 1) % kRing;
     if (!b.ev) DRZG_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
@@ -95,6 +99,7 @@ class Stager {
   };
   Buf bufs_[kRing];
   int next_ = 0;
+  std::mutex mu_;
   std::vector<void*> retired_;
 };
 
@@ -224,7 +229,10 @@ class ReductionEngine {
   // sweep arrays
   DevBuf<int> d_slot_, d_vdir_, d_u0_;
   DevBuf<i64> d_k_;
-  // temporaries
+  // temporaries.  The launcher thread owns them; the policy thread may give
+  // them back (grow_pool, when the state pool needs their memory), so both
+  // hold tmp_mu_ while they touch bcap_ or the buffers
+  std::mutex tmp_mu_;
   int bcap_ = 0;
   int sms_ = 148;  // SM count of the engine device (set at construction)
   DevBuf<int8_t> Bg_, IN_, Y_;

@@ -2,6 +2,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
+#include <map>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -864,6 +866,41 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
 }  // namespace tc
 
 namespace {
+// Per-device launch facts.  The SM count and the >48 KB dynamic shared-memory
+// opt-in are properties of (device, kernel): a process that launches on a
+// second device must opt in there too.
+constexpr int kMaxDev = 64;
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+int sm_count() {
+  static std::atomic<int> sms[kMaxDev];
+  const int d = cur_device();
+  DRZG_REQUIRE(d >= 0 && d < kMaxDev, "tc_gemm: device index out of range");
+  int v = sms[d].load(std::memory_order_relaxed);
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    sms[d].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+template <class K>
+void smem_opt_in(K* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes opted in
+  const int d = cur_device();
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{reinterpret_cast<const void*>(kernel), d}];
+  if (have >= bytes) return;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  DRZG_REQUIRE(e == cudaSuccess, std::string("shared-memory opt-in: ") + cudaGetErrorString(e));
+  have = bytes;
+}
+}  // namespace
+
+namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -905,17 +942,8 @@ void tc_gemm_i8(const int8_t* A, int rowsA, int lda, const int8_t* B, int rowsB,
   uint32_t idesc = (2u << 4) | (a_signed << 7) | (1u << 10) | ((uint32_t)(epi.b_mn ? 1u : 0u) << 16) |
                    ((uint32_t)(tc::BN >> 3) << 17) |
                    ((uint32_t)(tc::BM >> 4) << 24);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  smem_opt_in(tc::gemm_kernel, tc::SMEM_BYTES);
+  const int sms = sm_count();
   int tiles = ((epi.N + tc::BN - 1) / tc::BN) * ((epi.M + tc::BM - 1) / tc::BM);
   dim3 grid(std::min(tiles, sms));
   tc::gemm_kernel<<<grid, tc::THREADS, tc::SMEM_BYTES, st>>>(ma, mb, K, idesc, epi);
@@ -974,11 +1002,7 @@ void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs&
   const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
   const int smem = tc::fz::smem_bytes(nt, NS);
-  static int attr_for = -1;
-  if (attr_for != smem) {
-    cudaFuncSetAttribute(tc::dixon_fused_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_for = smem;
-  }
+  smem_opt_in(tc::dixon_fused_kernel<NS>, smem);
   const int nblk = (fa.N + NS - 1) / NS;
   static const bool one_block = std::getenv("DRZG_FUSED_ONEBLOCK") != nullptr;  // debug: one block per CTA
   tc::dixon_fused_kernel<NS><<<one_block ? nblk : std::min(nblk, sms), tc::fz::THREADS, smem, st>>>(
@@ -994,12 +1018,7 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
   thread_local MapCache ccache, jcache;
   const CUtensorMap& mc = cached_map(ccache, C, fa.nLp, 0, [&] { return make_map(C, fa.nLp, fa.nLp, fa.nLp, 128); });
   const CUtensorMap& mj = cached_map(jcache, Jd, fa.nLp, 0, [&] { return make_map(Jd, fa.nLp, fa.nLp, fa.nLp, 128); });
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = sm_count();
   // small batches (fewer 128-state blocks than SMs) run 64-state blocks
   const char* ns_env = std::getenv("DRZG_FUSED_NS");  // per launch: the path tests switch it
   // (32-state blocks when the whole batch fits one round of them: the
@@ -1034,17 +1053,8 @@ void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st)
                           ((uint32_t)(tc::BM >> 4) << 24);
   fa.idesc_d = common | (1u << 7);  // Cq signed
   fa.idesc_c = common;              // Jp unsigned
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc::dixon_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-    attr = true;
-  }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  smem_opt_in(tc::dixon_flow_kernel, tc::SMEM_BYTES);
+  const int sms = sm_count();
   const int mt = (e.M + tc::BM - 1) / tc::BM;
   const int nph = 2 * e.Ld - 1;
   // columns per group: enough tiles per phase (~2 rounds of the grid) that a

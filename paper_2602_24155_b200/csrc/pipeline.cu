@@ -201,6 +201,72 @@ i64 count_points_any(const Hypersurface& X, int r, i64 budget) {
 }
 }  // namespace
 
+std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const std::vector<Z>& F, i64 b,
+                        const ZetaOptions& opt, ZetaOut& res) {
+  res.hodge = hodge_numbers(X.n, X.d);
+  Z cp_mod = Z::pow(X.p, (u64)(plan.M + X.n));
+  std::vector<Z> dres = berkowitz(F, (int)b, cp_mod);
+  Recovered rec = recover_Q(dres, plan);
+  if (rec.status == 2) return rec.reason;
+  auto cands = std::move(rec.candidates);
+  bool ambiguous = false;
+  if (cands.size() > 1) {
+    int rounds = 0;
+    for (int r = 1; r <= 3 && cands.size() > 1; ++r) {
+      Z pts(0);
+      for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
+      if (pts > Z((long)opt.count_budget)) break;
+      ++rounds;
+      Z truth((long)count_points_any(X, r, opt.count_budget));
+      std::vector<std::vector<Z>> kept;
+      for (auto& c : cands)
+        if (counts_from_zeta(c, X.p, X.n, r) == truth) kept.push_back(c);
+      if (kept.empty()) break;
+      cands = std::move(kept);
+    }
+    if (cands.empty() || (cands.size() > 1 && rounds > 0)) return "sign of the functional equation undecided";
+    ambiguous = cands.size() > 1;
+  }
+  std::vector<Z> a = cands.front();
+  NewtonPolygon np = newton_polygon(a, X.p);
+  bool geom_ok = np.vertices.front() == std::make_pair<i64, i64>(0, 0);
+  i64 HP_end = hodge_polygon_at(res.hodge, X.n, plan.b);
+  geom_ok = geom_ok && np.vertices.back().first == plan.b && np.vertices.back().second == HP_end;
+  for (i64 x = 0; x <= plan.b && geom_ok; ++x)
+    if (np.value_at(x) < Q64::make(hodge_polygon_at(res.hodge, X.n, x), 1)) geom_ok = false;
+  if (!geom_ok) return "Newton polygon escapes the Hodge bound";
+  std::vector<CountCheck> checks;
+  bool counts_ok = true;
+  if (opt.verify_counts && !ambiguous) {
+    for (int r = 1; r <= 2; ++r) {
+      Z pts(0);
+      for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
+      if (pts > Z((long)opt.count_budget)) break;
+      CountCheck ck;
+      ck.r = r;
+      ck.from_zeta = counts_from_zeta(a, X.p, X.n, r);
+      ck.from_count = Z((long)count_points_any(X, r, opt.count_budget));
+      ck.ok = ck.from_zeta == ck.from_count;
+      counts_ok = counts_ok && ck.ok;
+      checks.push_back(ck);
+    }
+  }
+  if (!counts_ok) return "point counts disagree with the recovered zeta";
+  res.Q = a;
+  res.ambiguous = ambiguous;
+  if (ambiguous) res.Q_alt = cands.back();
+  res.np = np;
+  res.inv = classify(np, res.hodge, X.n, X.d);
+  res.domino = domino_number(np, res.hodge, X.n);
+  if (X.d <= X.nv()) {
+    res.inv.fsplit_defined = true;
+    res.inv.fsplit = fedder_is_fsplit(X);
+  }
+  res.counts = checks;
+  res.plan = plan;
+  return "";
+}
+
 ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
   double t0 = now_s();
   if (!check_smooth(X, full_set(X.nv())))
@@ -210,7 +276,6 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
   Basis B = compute_basis(X);
   PrecisionPlan plan = choose_precision(X.p, X.n, X.d, opt.overrides);
   ZetaOut res;
-  res.hodge = hodge_numbers(X.n, X.d);
   for (;;) {
     FrobOptions fo;
     fo.policy = opt.policy;
@@ -218,85 +283,16 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
     fo.profile = opt.profile;
     FrobResult fr = frobenius_matrix(X, B, plan, S, fo, device);
     res.led = fr.led;
-    Z cp_mod = Z::pow(X.p, (u64)(plan.M + X.n));
-    std::vector<Z> dres = berkowitz(fr.F, (int)fr.b, cp_mod);
+    std::vector<Z> F = fr.F;
+    const i64 b = fr.b;
     res.last = std::move(fr);
-    Recovered rec = recover_Q(dres, plan);
-    auto escalate_or_throw = [&](const std::string& why) {
-      res.reasons.push_back(why);
-      if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] escalate: %s\n", why.c_str());
-      if (!escalate_plan(plan)) throw escalation_exhausted("precision ladder exhausted: " + why);
-    };
-    if (rec.status == 2) {
-      escalate_or_throw(rec.reason);
-      continue;
-    }
-    auto cands = std::move(rec.candidates);
-    bool ambiguous = false;
-    if (cands.size() > 1) {
-      int rounds = 0;
-      for (int r = 1; r <= 3 && cands.size() > 1; ++r) {
-        Z pts(0);
-        for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
-        if (pts > Z((long)opt.count_budget)) break;
-        ++rounds;
-        Z truth((long)count_points_any(X, r, opt.count_budget));
-        std::vector<std::vector<Z>> kept;
-        for (auto& c : cands)
-          if (counts_from_zeta(c, X.p, X.n, r) == truth) kept.push_back(c);
-        if (kept.empty()) break;
-        cands = std::move(kept);
-      }
-      if (cands.empty() || (cands.size() > 1 && rounds > 0)) {
-        escalate_or_throw("sign of the functional equation undecided");
-        continue;
-      }
-      ambiguous = cands.size() > 1;
-    }
-    std::vector<Z> a = cands.front();
-    NewtonPolygon np = newton_polygon(a, X.p);
-    bool geom_ok = np.vertices.front() == std::make_pair<i64, i64>(0, 0);
-    i64 HP_end = hodge_polygon_at(res.hodge, X.n, plan.b);
-    geom_ok = geom_ok && np.vertices.back().first == plan.b && np.vertices.back().second == HP_end;
-    for (i64 x = 0; x <= plan.b && geom_ok; ++x)
-      if (np.value_at(x) < Q64::make(hodge_polygon_at(res.hodge, X.n, x), 1)) geom_ok = false;
-    if (!geom_ok) {
-      escalate_or_throw("Newton polygon escapes the Hodge bound");
-      continue;
-    }
-    std::vector<CountCheck> checks;
-    bool counts_ok = true;
-    if (opt.verify_counts && !ambiguous) {
-      for (int r = 1; r <= 2; ++r) {
-        Z pts(0);
-        for (int i = 0; i <= X.n; ++i) pts += Z::pow(ipow(X.p, r), (u64)i);
-        if (pts > Z((long)opt.count_budget)) break;
-        CountCheck ck;
-        ck.r = r;
-        ck.from_zeta = counts_from_zeta(a, X.p, X.n, r);
-        ck.from_count = Z((long)count_points_any(X, r, opt.count_budget));
-        ck.ok = ck.from_zeta == ck.from_count;
-        counts_ok = counts_ok && ck.ok;
-        checks.push_back(ck);
-      }
-    }
-    if (!counts_ok) {
-      escalate_or_throw("point counts disagree with the recovered zeta");
-      continue;
-    }
-    res.Q = a;
-    res.ambiguous = ambiguous;
-    if (ambiguous) res.Q_alt = cands.back();
-    res.np = np;
-    res.inv = classify(np, res.hodge, X.n, X.d);
-    res.domino = domino_number(np, res.hodge, X.n);
-    if (X.d <= X.nv()) {
-      res.inv.fsplit_defined = true;
-      res.inv.fsplit = fedder_is_fsplit(X);
-    }
-    res.counts = checks;
-    res.plan = plan;
-    break;
+    // the reference's escalation ladder (zeta.hpp:472-535): more series
+    // terms, then more digits, until the battery passes
+    const std::string why = finish_zeta(X, plan, F, b, opt, res);
+    if (why.empty()) break;
+    res.reasons.push_back(why);
+    if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] escalate: %s\n", why.c_str());
+    if (!escalate_plan(plan)) throw escalation_exhausted("precision ladder exhausted: " + why);
   }
   res.wall = now_s() - t0;
   return res;

@@ -71,6 +71,13 @@ struct ZetaOut {
 
 ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device);
 
+// run_zeta's battery on a given F (zeta.hpp:456-535): charpoly, Q recovery,
+// sign tie-break by point counts, Newton >= Hodge, point-count checks.
+// Returns "" (res filled) or the reason the plan must escalate.  Used by the
+// multi-GPU path on the gathered F.
+std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const std::vector<Z>& F, i64 b,
+                        const ZetaOptions& opt, ZetaOut& res);
+
 std::set<int> working_set_for(const Hypersurface& X, Policy pol);
 
 }  // namespace drzg

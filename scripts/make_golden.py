@@ -38,6 +38,11 @@ E2E = {
     "threefold_f13_s1_r1": (13, 4, 3, "random", 1, 1, 0, 8),
     "fermat_fourfold_f7_r1": (7, 5, 3, "fermat", 1, 1, 0, 4),
     "quintic_surface_f7_s1_r1": (7, 3, 5, "random", 1, 1, 3, 8),
+    # the metric's own hypersurface (configs[4], random cubic fourfold /F7,
+    # seed 1) at series-truncated plans the reference can finish here: N_m = 2
+    # (M = 2, one base-49 digit) and N_m = 3 (M = 3, two digits: Dixon carry)
+    "random_fourfold_f7_s1_nm2": (7, 5, 3, "random", 1, 0, 2, 6),
+    "random_fourfold_f7_s1_nm3": (7, 5, 3, "random", 1, 0, 3, 6),
 }
 
 

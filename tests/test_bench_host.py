@@ -1,5 +1,6 @@
 """Host logic of bench.py (no GPU): the batch step's counter merge and the
 threefold batch configuration (BASELINE.json configs[3])."""
+import json
 import os
 import sys
 
@@ -30,3 +31,24 @@ def test_threefold_batch_config():
     for world in (1, 2, 4, 8):
         got = sorted(s for r in range(world) for s in range(r, bench.BATCH_SEEDS, world))
         assert got == list(range(64))
+
+
+def test_reference_arm_never_loads_the_product():
+    """--impl reference runs the unmodified reference (oracle/_ref) only: the
+    product package and libdrzg.so stay unloaded in that process"""
+    import subprocess
+    import pytest
+    from conftest import have_ref
+    if not have_ref():
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, json, bench\n"
+            "sys.argv = ['bench.py', '--impl', 'reference', '--config', 'quintic', '--steps', '1', '--warmup', '0']\n"
+            "bench.main()\n"
+            "assert 'paper_2602_24155_b200' not in sys.modules\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert 'libdrzg' not in maps, 'libdrzg.so mapped'\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["projection"] is False

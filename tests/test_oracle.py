@@ -99,3 +99,19 @@ def test_reference_kernel_paths_agree(idx):
     s, _ = refapi.sparse_steps(c["p"], c["M"], c["side"], _arr(c["A"]), _arr(c["B"]), c["tmax"], _arr(c["w"]))
     if refapi.stripe_plan_py(c["p"], c["M"])["limbs"] <= 2:
         assert (d == s).all()
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["quintic_f7_s1.json", "fermat_cubic_curve_f7.json", "k3_f11_s1_r1.json",
+                                  "threefold_f13_s1_r1.json", "fermat_fourfold_f7_r1.json",
+                                  "quintic_surface_f7_s1_r1.json", "k3_f11_s1.json"])
+def test_ledger_replay_equals_reference_run(name):
+    """the value-free replay (ref_replay_ledger) gives the real reference
+    run's ledger: the basis for the replayed default-plan ledgers
+    (tests/golden/ledger_replay_*.json) the engine is checked against"""
+    from oracle import refapi
+    g = golden(name)
+    r = refapi.replay_ledger(g["p"], g["n"], g["d"], g["coeffs"], r_uniform=g["r_uniform"], nm=g["nm_override"],
+                             threads=2)
+    assert (r["matvecs"], r["startups"], r["combines"]) == tuple(
+        g["ledger"][k] for k in ("matvecs", "startups", "combines"))
