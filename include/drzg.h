@@ -116,6 +116,53 @@ int drzg_count_points_device(uint64_t p, int32_t n, int32_t d, const uint64_t* c
 char* drzg_charpoly(uint64_t p, int32_t n, int32_t d, int32_t r_uniform, int32_t nm_override, int32_t b,
                     const char* const* F);
 
+/* ---- reduction-policy interface on device-resident GameStates ----------
+ *
+ * drzg_ctx stands in for the reference's (RuvContext, PepStoreBase) pair of
+ * one (f, S, p^M) run (reduction.hpp:150-242, 143-147): the shared Dixon
+ * tables (Jp, Jp^-1 mod q, the gather/scatter tables) and the HBM slot pool
+ * the states live in.  A state id names one GameState{u, pole, w}
+ * (reduction.hpp:113-117); w crosses the boundary in ModVec layout (limbs
+ * planes of base-beta digits over Homog_{dn-n}, linalg.hpp:94-117).  The
+ * working set is default_S(n, d), or {n} for policy 2 (var-by-var),
+ * zeta.hpp:433-436.  A context serves one call at a time (internal lock). */
+typedef struct drzg_ctx drzg_ctx;
+
+/* RuvContext(X, StripePlan::make(p, M), S) — reduction.hpp:150-195; NULL on error */
+drzg_ctx* drzg_ctx_create(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int32_t policy,
+                          int32_t device);
+void drzg_ctx_free(drzg_ctx* ctx);
+/* side = |Homog_{dn-n}| (RuvContext::side), floor_len = |Homog_{dn-n-1}|,
+ * the StripePlan of the ModVec layout, and the device digit plan q^Ld */
+int drzg_ctx_info(drzg_ctx* ctx, int32_t* side, int32_t* floor_len, drzg_stripe_plan* plan, int32_t* digit_base,
+                  int32_t* digit_planes);
+/* upload GameStates (e.g. seed_reduction_input's, reduction.hpp:538-563):
+ * u: count x (n+1), pole: count, w: count x (limbs x side) */
+int drzg_states_seed(drzg_ctx* ctx, int32_t count, const int32_t* u, const int32_t* pole, const uint64_t* w,
+                     int32_t* ids_out);
+/* download states; any output pointer may be NULL */
+int drzg_states_read(drzg_ctx* ctx, int32_t count, const int32_t* ids, int32_t* u_out, int32_t* pole_out,
+                     uint64_t* w_out);
+int drzg_states_free(drzg_ctx* ctx, int32_t count, const int32_t* ids);
+/* reduce_chunk(C, store, st, v, k, ledger) for every listed state at once —
+ * reduction.hpp:394-423: k pole drops along v (count x (n+1)); u <- u - k v,
+ * pole <- pole - k.  ledger (matvecs, startups, combines) is added to. */
+int drzg_step_batch(drzg_ctx* ctx, int32_t count, const int32_t* ids, const int32_t* v, const int64_t* k,
+                    int64_t* ledger);
+/* combine_states(states, ledger) — reduction.hpp:426-451: states with equal
+ * (u, pole) are summed into the first; ids_out receives the survivors in
+ * order (the others are freed) */
+int drzg_states_combine(drzg_ctx* ctx, int32_t count, const int32_t* ids, int32_t* ids_out, int32_t* count_out,
+                        int64_t* ledger);
+/* run_policy(C, store, states, policy, ledger) — reduction.hpp:464-533:
+ * drives every state to pole n (0 p-chunk, 1 depth-first, 2 var-by-var);
+ * ids_out receives the floor states the reference returns */
+int drzg_run_policy(drzg_ctx* ctx, int32_t count, const int32_t* ids, int32_t policy, int32_t* ids_out,
+                    int32_t* count_out, int64_t* ledger);
+/* floor_to_numerator(C, st, g) for every listed floor state — reduction.hpp:
+ * 566-581: g (ModVec layout over Homog_{dn-n-1}, floor_len entries) += x^{u-1} w */
+int drzg_floor_accumulate(drzg_ctx* ctx, int32_t count, const int32_t* ids, uint64_t* g);
+
 #ifdef __cplusplus
 }
 #endif

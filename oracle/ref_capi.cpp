@@ -684,4 +684,44 @@ char* ref_ctx_chunk(void* h, const int* u, int pole, const int* v, long k, const
   });
 }
 
+
+// reference run_policy (reduction.hpp:464-533) on caller-given GameStates
+// (u, pole, w in ModVec layout), then floor_to_numerator (reduction.hpp:
+// 566-581) of every floor state: the oracle of the device states API
+char* ref_run_policy_states(u64 p, int n, int d, const u64* coeffs, int M, const char* policy, int count,
+                            const int* u, const int* pole, const u64* w) {
+  return guarded([&] {
+    Hypersurface X = make_x(p, n, d, coeffs);
+    Policy pol = policy_from_name(policy);
+    StripePlan kp = StripePlan::make(p, M);
+    RuvContext C(X, kp, working_set_for(X, pol));
+    auto store = make_pep_store("lazy", C);
+    const int nv = n + 1;
+    std::vector<GameState> sts;
+    for (int i = 0; i < count; ++i) {
+      GameState st;
+      st.u = Expo(nv);
+      for (int j = 0; j < nv; ++j) st.u[j] = u[(size_t)i * nv + j];
+      st.pole = pole[i];
+      st.w = ModVec(kp, C.side);
+      std::memcpy(st.w.d.data(), w + (size_t)i * st.w.d.size(), sizeof(u64) * st.w.d.size());
+      sts.push_back(std::move(st));
+    }
+    CostLedger led;
+    std::vector<GameState> fl = run_policy(C, *store, std::move(sts), pol, led);
+    std::vector<mpz_class> g;
+    for (const auto& st : fl) floor_to_numerator(C, st, g);
+    std::ostringstream os;
+    os << "{\"matvecs\":" << led.matvecs << ",\"startups\":" << led.startups << ",\"combines\":" << led.combines
+       << ",\"g\":" << zarr(g) << ",\"states\":[";
+    for (size_t i = 0; i < fl.size(); ++i) {
+      os << (i ? "," : "") << "{\"u\":" << expo_arr(fl[i].u) << ",\"pole\":" << fl[i].pole << ",\"w\":[";
+      for (size_t j = 0; j < fl[i].w.d.size(); ++j) os << (j ? "," : "") << "\"" << fl[i].w.d[j] << "\"";
+      os << "]}";
+    }
+    os << "]}";
+    return os.str();
+  });
+}
+
 }  // extern "C"

@@ -24,7 +24,7 @@ def lib():
         if not os.path.exists(REF_SO):
             raise RuntimeError(f"{REF_SO} missing: run `make -C oracle` where /root/reference exists")
         L = ctypes.CDLL(REF_SO)
-        for name in ("ref_replay_ledger", "ref_mono_table", "ref_hypersurface", "ref_plan", "ref_basis", "ref_seeds",
+        for name in ("ref_run_policy_states", "ref_replay_ledger", "ref_mono_table", "ref_hypersurface", "ref_plan", "ref_basis", "ref_seeds",
                      "ref_chunk", "ref_frobenius", "ref_zeta", "ref_charpoly", "ref_policy_sample"):
             getattr(L, name).restype = ctypes.c_void_p
         _lib = L
@@ -180,3 +180,15 @@ def replay_ledger(p, n, d, coeffs, r_uniform=0, nm=0, threads=4):
     """the reference's frobenius_matrix cost ledger by value-free replay
     (matvecs, startups, combines, per column); equals the real run's ledger"""
     return _js(lib().ref_replay_ledger(ctypes.c_uint64(p), n, d, _u64(coeffs), r_uniform, nm, threads))
+
+
+def run_policy_states(p, n, d, coeffs, M, policy, u, pole, w):
+    """reference run_policy on given GameStates (u: count x nv, pole: count, w:
+    count x limbs*side ModVec digits) + floor_to_numerator of the floor states"""
+    import numpy as np
+    count = len(pole)
+    ua = _i32([x for row in u for x in row])
+    pa = _i32(pole)
+    w = np.ascontiguousarray(w, dtype=np.uint64)
+    return _js(lib().ref_run_policy_states(ctypes.c_uint64(p), n, d, _u64(coeffs), M, policy.encode(), count, ua, pa,
+                                           w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))

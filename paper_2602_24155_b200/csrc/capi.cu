@@ -163,6 +163,10 @@ std::vector<u64> coeff_vec(int n, int d, const uint64_t* coeffs) {
 
 }  // namespace
 
+namespace drzg {
+void set_last_error(const std::string& s) { g_err = s; }
+}  // namespace drzg
+
 extern "C" {
 
 const char* drzg_last_error(void) { return g_err.c_str(); }

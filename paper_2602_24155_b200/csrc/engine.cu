@@ -1382,4 +1382,323 @@ void ReductionEngine::chunk_batch(const std::vector<Expo>& u, const std::vector<
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// State-level primitives and the round-based policies.
+
+std::vector<int> ReductionEngine::seed_states(const std::vector<int>& eptr, const std::vector<int>& eg,
+                                              const std::vector<i8>& edig) {
+  const int ns = (int)eptr.size() - 1;
+  std::vector<int> slots(ns);
+  if (ns <= 0) return slots;
+  while ((int)free_.size() < ns) grow_pool(cap_ + ns);
+  for (int i = 0; i < ns; ++i) slots[i] = alloc_slot();
+  DevBuf<int> da, db, dc;
+  DevBuf<int8_t> dd;
+  da.upload(slots, st_);
+  db.upload(eptr, st_);
+  dc.upload(eg, st_);
+  dd.upload(std::vector<int8_t>(edig.begin(), edig.end()), st_);
+  timed(&clock.other_ms, [&] {
+    dev::seed_kernel<<<ns, 128, 0, st_>>>(pool_, slot_stride_, sidep_, T_->dp.Ld, da.p, db.p, dc.p, dd.p, ns);
+  });
+  DRZG_CUDA(cudaGetLastError());
+  DRZG_CUDA(cudaStreamSynchronize(st_));
+  return slots;
+}
+
+void ReductionEngine::step_states(const std::vector<Live*>& sts, const std::vector<int>& vdir,
+                                  const std::vector<i64>& k, Ledger& led) {
+  const RuvTables& T = *T_;
+  const int B = (int)sts.size();
+  if (!B) return;
+  std::vector<int> order(B);
+  for (int i = 0; i < B; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return k[a] != k[b] ? k[a] > k[b] : vdir[a] < vdir[b]; });
+  std::vector<int> hslot, hvdir, hu0;
+  std::vector<i64> ks;
+  i64 maxpole = 0;
+  for (int i : order) {
+    const Live& s = *sts[i];
+    const Expo& v = dirs_host_.at(vdir[i]);
+    DRZG_REQUIRE(k[i] >= 1, "reduce_chunk: empty chunk");
+    DRZG_REQUIRE(legal(T.d, s.u, v, k[i], T.S), "reduce_chunk: illegal move");
+    DRZG_REQUIRE(s.pole - k[i] >= n_, "reduce_chunk: chunk passes the floor");
+    maxpole = std::max<i64>(maxpole, s.pole);
+    ks.push_back(k[i]);
+    hslot.push_back(s.slot);
+    hvdir.push_back(vdir[i]);
+    for (int j = 0; j < T.nv; ++j) hu0.push_back(s.u[j]);
+  }
+  // the multiply-high T_x epilogue assumes exponents below 4096 (x = u - y v < d * pole)
+  const bool fast_saved = fast_;
+  if ((i64)T.d * maxpole >= 4096) fast_ = false;
+  d_slot_.stage(hslot, stager_, st_);
+  d_vdir_.stage(hvdir, stager_, st_);
+  d_u0_.stage(hu0, stager_, st_);
+  d_k_.stage(ks, stager_, st_);
+  led.matvecs += run_sweep(ks);
+  led.startups += B;
+  fast_ = fast_saved;
+  for (int i = 0; i < B; ++i) {
+    Live& s = *sts[i];
+    const Expo& v = dirs_host_[vdir[i]];
+    for (int j = 0; j < T.nv; ++j) s.u[j] -= (int)(k[i] * v[j]);
+    s.pole -= (int)k[i];
+  }
+}
+
+void ReductionEngine::combine_live(std::vector<Live>& sts, Ledger& led) {
+  const RuvTables& T = *T_;
+  std::unordered_map<std::string, int> first;  // key -> position in out
+  std::vector<Live> out;
+  std::vector<std::vector<int>> groups;        // per out position: merged slots (first = keeper)
+  out.reserve(sts.size());
+  for (auto& s : sts) {
+    std::string key((const char*)s.u.e, sizeof(int) * s.u.nv);
+    key.append((const char*)&s.pole, sizeof(int));
+    key.append((const char*)&s.col, sizeof(int));
+    auto it = first.find(key);
+    if (it == first.end()) {
+      first.emplace(std::move(key), (int)out.size());
+      groups.push_back({s.slot});
+      out.push_back(s);
+    } else {
+      groups[it->second].push_back(s.slot);
+      led.combines += 1;
+    }
+  }
+  std::vector<int> gptr{0}, mem, freed;
+  for (auto& g : groups) {
+    if (g.size() < 2) continue;
+    mem.insert(mem.end(), g.begin(), g.end());
+    gptr.push_back((int)mem.size());
+    freed.insert(freed.end(), g.begin() + 1, g.end());
+  }
+  if (gptr.size() > 1) {
+    DevBuf<int> dp, dm;
+    dp.upload(gptr, st_);
+    dm.upload(mem, st_);
+    const size_t ng = gptr.size() - 1;
+    dim3 gm((unsigned)((T.side + 127) / 128) * ng);
+    timed(&clock.other_ms, [&] {
+      dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, T.dp.Ld, T.dp.q, dp.p, dm.p);
+    });
+    DRZG_CUDA(cudaGetLastError());
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+  }
+  for (int f : freed) free_slot(f);
+  sts.swap(out);
+}
+
+void ReductionEngine::run_policy_live(std::vector<Live>& sts, Policy pol, Ledger& led) {
+  const RuvTables& T = *T_;
+  const int n = n_, d = T.d;
+  auto active = [&](const Live& s) { return s.pole > n; };
+  std::vector<Live*> batch;
+  std::vector<int> vd;
+  std::vector<i64> kk;
+  auto flush = [&] {
+    step_states(batch, vd, kk, led);
+    batch.clear();
+    vd.clear();
+    kk.clear();
+  };
+  if (pol == Policy::depth_first) {
+    // every state chunk after chunk to the floor, never combined
+    // (reduction.hpp:472-483); states move in lockstep rounds, which changes
+    // no state's trajectory
+    for (;;) {
+      for (auto& s : sts) {
+        if (!active(s)) continue;
+        Expo v = choose_v_greedy(d, s.u, T.S);
+        repair_v(s.u, v, T.S);
+        const i64 k = std::min<i64>(k_max_legal(s.u, v, T.S), (i64)s.pole - n);
+        DRZG_REQUIRE(k >= 1, "depth-first: no admissible move");
+        batch.push_back(&s);
+        vd.push_back((int)rank_of(v));
+        kk.push_back(k);
+      }
+      if (batch.empty()) break;
+      flush();
+    }
+    return;
+  }
+  if (pol == Policy::p_chunk) {
+    // reduction.hpp:486-503: per sweep the states at the top |u| take
+    // k = min(p, pole - n, k_max) along the greedy v, then combine_states
+    for (;;) {
+      int top = -1;
+      for (auto& s : sts)
+        if (active(s)) top = std::max(top, s.u.total());
+      if (top < 0) break;
+      for (auto& s : sts) {
+        if (!active(s) || s.u.total() != top) continue;
+        Expo v;
+        i64 k;
+        pchunk_move(d, n, (i64)p_, s.u, s.pole, T.S, &v, &k);
+        DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
+        batch.push_back(&s);
+        vd.push_back((int)rank_of(v));
+        kk.push_back(k);
+      }
+      flush();
+      combine_live(sts, led);
+    }
+    return;
+  }
+  // var-by-var (reduction.hpp:507-532): stages t = n..0 over S = {n}; u_t is
+  // driven to 0 (t in S) or 1, with a combine between stages
+  DRZG_REQUIRE(T.S == (1u << n), "var-by-var: working set must be {n}");
+  for (int t = n; t >= 0; --t) {
+    const int target = ((T.S >> t) & 1u) ? 0 : 1;
+    const unsigned stage = 1u << t;
+    for (;;) {
+      for (auto& s : sts) {
+        if (!active(s) || s.u[t] <= target) continue;
+        Expo v = choose_v_greedy(d, s.u, stage);
+        repair_v(s.u, v, T.S);
+        i64 k = std::min<i64>(k_max_legal(s.u, v, T.S), (i64)s.pole - n);
+        if (v[t] > 0) k = std::min<i64>(k, ((i64)s.u[t] - target) / v[t]);
+        DRZG_REQUIRE(k >= 1, "var-by-var: no admissible move");
+        batch.push_back(&s);
+        vd.push_back((int)rank_of(v));
+        kk.push_back(k);
+      }
+      if (batch.empty()) break;
+      flush();
+    }
+    combine_live(sts, led);
+  }
+  for (auto& s : sts) DRZG_REQUIRE(!active(s), "var-by-var: states left above the floor");
+}
+
+void ReductionEngine::floor_accumulate(const std::vector<Live>& sts, long long* dG, int ncols) {
+  const RuvTables& T = *T_;
+  if (sts.empty()) return;
+  std::vector<int> fs, fc, fu;
+  for (auto& s : sts) {
+    DRZG_REQUIRE(s.pole == n_, "floor_to_numerator: not at the floor");
+    DRZG_REQUIRE(s.col >= 0 && s.col < ncols, "floor_accumulate: column out of range");
+    fs.push_back(s.slot);
+    fc.push_back(s.col);
+    for (int j = 0; j < T.nv; ++j) fu.push_back(s.u[j]);
+  }
+  DevBuf<int> da, db, dc, derr;
+  da.upload(fs, st_);
+  db.upload(fc, st_);
+  dc.upload(fu, st_);
+  derr.alloc(1, st_);
+  DRZG_CUDA(cudaMemsetAsync(derr.p, 0, sizeof(int), st_));
+  dim3 gf((unsigned)((T.side + 127) / 128) * fs.size());
+  timed(&clock.other_ms, [&] {
+    dev::floor_kernel<<<gf, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, T.dp.Ld, T.nv, da.p, db.p, dc.p,
+                                           mon_.p, btab_.p, dG, gsize_, derr.p);
+  });
+  DRZG_CUDA(cudaGetLastError());
+  DRZG_CUDA(cudaStreamSynchronize(st_));
+}
+
+std::vector<i8> ReductionEngine::read_states(const std::vector<int>& slots) {
+  const RuvTables& T = *T_;
+  const int Ld = T.dp.Ld;
+  std::vector<i8> out((size_t)slots.size() * Ld * T.side);
+  std::vector<int8_t> stage((size_t)slot_stride_);
+  for (size_t i = 0; i < slots.size(); ++i) {
+    DRZG_CUDA(cudaMemcpyAsync(stage.data(), pool_ + (size_t)slots[i] * slot_stride_, stage.size(),
+                              cudaMemcpyDeviceToHost, st_));
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    for (int t = 0; t < Ld; ++t)
+      for (int g = 0; g < T.side; ++g) out[(i * Ld + t) * T.side + g] = stage[(size_t)t * sidep_ + g];
+  }
+  g_traffic.d2h += (long long)(slots.size() * slot_stride_);
+  return out;
+}
+
+void ReductionEngine::write_state(int slot, const std::vector<i8>& digits) {
+  const RuvTables& T = *T_;
+  const int Ld = T.dp.Ld;
+  DRZG_REQUIRE(digits.size() == (size_t)Ld * T.side, "write_state: digit array size");
+  std::vector<int8_t> stage((size_t)slot_stride_, 0);
+  for (int t = 0; t < Ld; ++t)
+    for (int g = 0; g < T.side; ++g) stage[(size_t)t * sidep_ + g] = digits[(size_t)t * T.side + g];
+  DRZG_CUDA(cudaMemcpyAsync(pool_ + (size_t)slot * slot_stride_, stage.data(), stage.size(), cudaMemcpyHostToDevice,
+                            st_));
+  DRZG_CUDA(cudaStreamSynchronize(st_));
+  g_traffic.h2d += (long long)stage.size();
+}
+
+void ReductionEngine::release_slots(const std::vector<int>& slots) {
+  for (int s : slots) free_slot(s);
+}
+
+void ReductionEngine::run_rounds(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led,
+                                 Policy pol) {
+  const RuvTables& T = *T_;
+  const int nv = T.nv, Ld = T.dp.Ld, ncol = (int)cols.size();
+  cudaEvent_t run0, run1;
+  DRZG_CUDA(cudaEventCreate(&run0));
+  DRZG_CUDA(cudaEventCreate(&run1));
+  DRZG_CUDA(cudaEventRecord(run0, st_));
+  DevBuf<long long> dG;
+  dG.alloc((size_t)ncol * Ld * gsize_, st_);
+  DRZG_CUDA(cudaMemsetAsync(dG.p, 0, dG.n * sizeof(long long), st_));
+  // every seed is its own state (the reference seeds one GameState per term,
+  // zeta.hpp:66-69); depth-first never combines, so its states may run in
+  // waves that fit the pool; var-by-var combines across all of a column's
+  // states, so a column runs whole
+  size_t fr = 0, tot = 0;
+  DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t wave = std::max<size_t>(1024, (size_t)(fr * 0.4) / (size_t)slot_stride_);
+  for (int c = 0; c < ncol; ++c) {
+    std::vector<Live> sts;
+    std::vector<int> eptr{0}, eg;
+    std::vector<i8> ed;
+    auto run_wave = [&] {
+      if (sts.empty()) return;
+      std::vector<int> slots = seed_states(eptr, eg, ed);
+      for (size_t i = 0; i < sts.size(); ++i) sts[i].slot = slots[i];
+      run_policy_live(sts, pol, led);
+      floor_accumulate(sts, dG.p, ncol);
+      std::vector<int> fsl;
+      for (auto& s : sts) fsl.push_back(s.slot);
+      release_slots(fsl);
+      sts.clear();
+      eptr.assign(1, 0);
+      eg.clear();
+      ed.clear();
+    };
+    for (auto& kv : cols[c].by_pole) {
+      const SeedBucket& bk = kv.second;
+      for (size_t i = 0; i < bk.size(); ++i) {
+        Live s;
+        s.col = c;
+        s.u = Expo(nv);
+        for (int j = 0; j < nv; ++j) s.u[j] = bk.u[i * nv + j];
+        s.pole = kv.first;
+        sts.push_back(s);
+        eg.push_back(bk.g[i]);
+        ed.insert(ed.end(), bk.dig.begin() + i * Ld, bk.dig.begin() + (i + 1) * Ld);
+        eptr.push_back((int)eg.size());
+        if (pol == Policy::depth_first && sts.size() >= wave) run_wave();
+      }
+    }
+    run_wave();
+  }
+  std::vector<long long> hG(dG.n);
+  DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
+  g_traffic.d2h += (long long)(dG.n * sizeof(long long));
+  DRZG_CUDA(cudaEventRecord(run1, st_));
+  DRZG_CUDA(cudaStreamSynchronize(st_));
+  float ms = 0;
+  DRZG_CUDA(cudaEventElapsedTime(&ms, run0, run1));
+  clock.device_ms += ms;
+  cudaEventDestroy(run0);
+  cudaEventDestroy(run1);
+  G.assign(ncol, {});
+  for (int c = 0; c < ncol; ++c)
+    G[c].assign(hG.begin() + (size_t)c * Ld * gsize_, hG.begin() + (size_t)(c + 1) * Ld * gsize_);
+}
+
 }  // namespace drzg

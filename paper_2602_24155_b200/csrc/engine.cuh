@@ -167,6 +167,40 @@ class ReductionEngine {
   void chunk_batch(const std::vector<Expo>& u, const std::vector<int>& vdir, const std::vector<i64>& k,
                    std::vector<i8>& w_digits, Ledger& led);
 
+  // ---- state-level primitives: the C ABI's states API (drzg_states_*,
+  // drzg_step_batch, drzg_run_policy) and the round-based policies ----
+  struct Live {
+    int col = 0;   // column (frobenius) or 0 (states API)
+    Expo u;
+    int pole = 0;
+    int slot = -1;
+  };
+  // new states, one per entry list (CSR over (side row g, Ld balanced digits))
+  std::vector<int> seed_states(const std::vector<int>& eptr, const std::vector<int>& eg, const std::vector<i8>& edig);
+  // reduce_chunk (reduction.hpp:394-423) for every listed state at once: k
+  // pole drops along its v (rank in Homog_d); u, pole updated
+  void step_states(const std::vector<Live*>& sts, const std::vector<int>& vdir, const std::vector<i64>& k,
+                   Ledger& led);
+  // combine_states (reduction.hpp:426-451) over the listed states, keyed by
+  // (col, u, pole): the first of each key keeps its slot and receives the
+  // sum, the others are freed and dropped from the list
+  void combine_live(std::vector<Live>& sts, Ledger& led);
+  // run_policy (reduction.hpp:464-533) on device-resident states: every state
+  // is driven to pole n with the policy's moves and combines; the floor states
+  // are left in `sts`
+  void run_policy_live(std::vector<Live>& sts, Policy pol, Ledger& led);
+  // floor_to_numerator (reduction.hpp:566-581) of floor states into per-column
+  // digit-sum accumulators (ncols x Ld x |Homog_{dn-n-1}|, int64)
+  void floor_accumulate(const std::vector<Live>& sts, long long* dG, int ncols);
+  // residues of states as Ld x side balanced digits (host)
+  std::vector<i8> read_states(const std::vector<int>& slots);
+  void write_state(int slot, const std::vector<i8>& digits);  // Ld x side
+  void release_slots(const std::vector<int>& slots);
+  // frobenius_matrix's per-column loop for the depth-first and var-by-var
+  // policies (p-chunk has its own pipelined path, run_pchunk)
+  void run_rounds(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led, Policy pol);
+  const std::vector<Expo>& dirs() const { return dirs_host_; }
+
   KernelClock clock;
   bool tensor_cores() const { return use_tc_; }
   int floor_size() const { return gsize_; }

@@ -24,7 +24,6 @@ std::set<int> working_set_for(const Hypersurface& X, Policy pol) {
 
 FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan, const std::set<int>& S,
                             const FrobOptions& opt, int device) {
-  DRZG_REQUIRE(opt.policy == Policy::p_chunk, "device engine: only the p-chunk policy is implemented");
   double t0 = now_s();
   DRZG_CUDA(cudaSetDevice(device));
   cudaStream_t st;
@@ -109,7 +108,10 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       std::vector<std::vector<i64>> Gg;
       const double tg = now_s();
       const i64 mv0 = out.led.matvecs;
-      eng.run_pchunk(grp, Gg, out.led);
+      if (opt.policy == Policy::p_chunk)
+        eng.run_pchunk(grp, Gg, out.led);  // pipelined: policy thread + launcher
+      else
+        eng.run_rounds(grp, Gg, out.led, opt.policy);  // depth-first, var-by-var
       if (std::getenv("DRZG_VERBOSE"))
         std::fprintf(stderr, "[drzg] group %d: columns %zu-%zu, %lld matvecs, %.2f s, peak live %lld\n", out.groups,
                      c0, c1 - 1, (long long)(out.led.matvecs - mv0), now_s() - tg, (long long)eng.peak_live());

@@ -25,7 +25,7 @@ from oracle import refapi  # noqa: E402
 
 GOLD = os.path.join(ROOT, "tests", "golden")
 
-# name -> (p, n, d, mode, seed, r_uniform, nm_override, threads)
+# name -> (p, n, d, mode, seed, r_uniform, nm_override, threads[, policy])
 E2E = {
     "fermat_cubic_curve_f7": (7, 2, 3, "fermat", 1, 0, 0, 1),
     "random_cubic_curve_f11_s3": (11, 2, 3, "random", 3, 0, 0, 1),
@@ -43,16 +43,23 @@ E2E = {
     # (M = 2, one base-49 digit) and N_m = 3 (M = 3, two digits: Dixon carry)
     "random_fourfold_f7_s1_nm2": (7, 5, 3, "random", 1, 0, 2, 6),
     "random_fourfold_f7_s1_nm3": (7, 5, 3, "random", 1, 0, 3, 6),
+    # the other two reduction policies (reduction.hpp:464-533): same F, own ledgers
+    "quintic_f7_s1_depth": (7, 2, 5, "random", 1, 0, 0, 4, "depth-first"),
+    "quintic_f7_s1_vbv": (7, 2, 5, "random", 1, 0, 0, 4, "var-by-var"),
+    "k3_f11_s1_r1_depth": (11, 3, 4, "random", 1, 1, 0, 8, "depth-first"),
+    "k3_f11_s1_r1_vbv": (11, 3, 4, "random", 1, 1, 0, 8, "var-by-var"),
+    "threefold_f13_s1_r1_vbv": (13, 4, 3, "random", 1, 1, 0, 8, "var-by-var"),
 }
 
 
 def e2e(name):
-    p, n, d, mode, seed, ru, nm, threads = E2E[name]
-    coeffs = refapi.hypersurface(p, n, d, seed=seed, mode=mode)
+    p, n, d, mode, seed, ru, nm, threads = E2E[name][:8]
+    policy = E2E[name][8] if len(E2E[name]) > 8 else "p-chunk"
+    coeffs = refapi.hypersurface(p, n, d, seed=seed, mode=mode, policy=policy)
     t0 = time.time()
-    fr = refapi.frobenius(p, n, d, coeffs, threads=threads, r_uniform=ru, nm=nm)
+    fr = refapi.frobenius(p, n, d, coeffs, policy=policy, threads=threads, r_uniform=ru, nm=nm)
     out = {
-        "name": name, "p": p, "n": n, "d": d, "mode": mode, "seed": seed,
+        "name": name, "p": p, "n": n, "d": d, "mode": mode, "seed": seed, "policy": policy,
         "r_uniform": ru, "nm_override": nm, "coeffs": coeffs,
         "plan": fr["plan"], "b": fr["b"], "F": fr["F"], "charpoly": fr["charpoly"],
         "ledger": {k: fr[k] for k in ("matvecs", "startups", "combines", "pep_misses")},
