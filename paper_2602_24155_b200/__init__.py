@@ -228,3 +228,96 @@ def test_tc_gemm_mn(A, B, a_unsigned=False):
     _check(lib().drzg_test_tc_gemm_mn(M, N, K, A.ctypes.data_as(ctypes.c_void_p), B.ctypes.data_as(ctypes.c_void_p),
                                       D.ctypes.data_as(ctypes.c_void_p), int(a_unsigned)))
     return D
+
+
+class Context:
+    """the reduction-policy interface on device-resident GameStates (drzg_ctx:
+    the reference's RuvContext + PepStoreBase of one (f, S, p^M) run,
+    reduction.hpp:143-242).  States are ids; w crosses in ModVec layout."""
+
+    def __init__(self, p, n, d, coeffs, M, policy="p-chunk", device=0):
+        L = lib()
+        L.drzg_ctx_create.restype = ctypes.c_void_p
+        self.n, self.nv = n, n + 1
+        self.h = L.drzg_ctx_create(ctypes.c_uint64(p), n, d, _u64arr(coeffs), M, POLICIES[policy], device)
+        if not self.h:
+            raise DrzgError(_err())
+        side, fl, q, Ld = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        sp = StripePlan()
+        _check(L.drzg_ctx_info(ctypes.c_void_p(self.h), ctypes.byref(side), ctypes.byref(fl), ctypes.byref(sp),
+                               ctypes.byref(q), ctypes.byref(Ld)))
+        self.side, self.floor_len, self.plan, self.q, self.Ld = side.value, fl.value, sp, q.value, Ld.value
+        self.ledger = [0, 0, 0]
+
+    def close(self):
+        if self.h:
+            lib().drzg_ctx_free(ctypes.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ids(self, ids):
+        return (ctypes.c_int32 * len(ids))(*ids)
+
+    def _led(self, arr):
+        for i in range(3):
+            self.ledger[i] += arr[i]
+
+    def seed(self, u, pole, w):
+        """GameStates in: u (count x nv), pole (count), w (count x limbs*side)"""
+        count = len(pole)
+        w = np.ascontiguousarray(w, dtype=np.uint64).reshape(count, -1)
+        out = (ctypes.c_int32 * count)()
+        _check(lib().drzg_states_seed(ctypes.c_void_p(self.h), count, (ctypes.c_int32 * (count * self.nv))(
+            *[int(x) for row in u for x in row]), (ctypes.c_int32 * count)(*pole), w.ctypes.data_as(_P64), out))
+        return list(out)
+
+    def read(self, ids):
+        count = len(ids)
+        u = (ctypes.c_int32 * (count * self.nv))()
+        pole = (ctypes.c_int32 * count)()
+        w = np.zeros((count, self.plan.limbs * self.side), dtype=np.uint64)
+        _check(lib().drzg_states_read(ctypes.c_void_p(self.h), count, self._ids(ids), u, pole,
+                                      w.ctypes.data_as(_P64)))
+        return [list(u[i * self.nv:(i + 1) * self.nv]) for i in range(count)], list(pole), w
+
+    def free(self, ids):
+        _check(lib().drzg_states_free(ctypes.c_void_p(self.h), len(ids), self._ids(ids)))
+
+    def step(self, ids, v, k):
+        """reduce_chunk for each state: v (count x nv), k (count)"""
+        count = len(ids)
+        led = (ctypes.c_int64 * 3)()
+        _check(lib().drzg_step_batch(ctypes.c_void_p(self.h), count, self._ids(ids),
+                                     (ctypes.c_int32 * (count * self.nv))(*[int(x) for row in v for x in row]),
+                                     (ctypes.c_int64 * count)(*k), led))
+        self._led(led)
+
+    def combine(self, ids):
+        out = (ctypes.c_int32 * max(1, len(ids)))()
+        cnt = ctypes.c_int32()
+        led = (ctypes.c_int64 * 3)()
+        _check(lib().drzg_states_combine(ctypes.c_void_p(self.h), len(ids), self._ids(ids), out, ctypes.byref(cnt),
+                                         led))
+        self._led(led)
+        return list(out[:cnt.value])
+
+    def run_policy(self, ids, policy="p-chunk"):
+        out = (ctypes.c_int32 * max(1, len(ids)))()
+        cnt = ctypes.c_int32()
+        led = (ctypes.c_int64 * 3)()
+        _check(lib().drzg_run_policy(ctypes.c_void_p(self.h), len(ids), self._ids(ids), POLICIES[policy], out,
+                                     ctypes.byref(cnt), led))
+        self._led(led)
+        return list(out[:cnt.value])
+
+    def floor_numerator(self, ids, g=None):
+        if g is None:
+            g = np.zeros(self.plan.limbs * self.floor_len, dtype=np.uint64)
+        g = np.ascontiguousarray(g, dtype=np.uint64).copy()
+        _check(lib().drzg_floor_accumulate(ctypes.c_void_p(self.h), len(ids), self._ids(ids), g.ctypes.data_as(_P64)))
+        return g
