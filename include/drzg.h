@@ -163,6 +163,29 @@ int drzg_run_policy(drzg_ctx* ctx, int32_t count, const int32_t* ids, int32_t po
  * 566-581: g (ModVec layout over Homog_{dn-n-1}, floor_len entries) += x^{u-1} w */
 int drzg_floor_accumulate(drzg_ctx* ctx, int32_t count, const int32_t* ids, uint64_t* g);
 
+/* ---- the linear-recurrence data structure (PEP) ------------------------
+ *
+ * PepStoreBase::get(v) / stats() (reduction.hpp:143-147) over a context, with
+ * make_pep_store's backings "eager", "lazy", "lru:N", "lfuda:N" (pep.hpp:
+ * 15-209): exactly-once builds under concurrency, shared entries (an eviction
+ * never invalidates a held one).  An entry is build_ruv(C, v) (reduction.hpp:
+ * 253-297): the n+2 matrices A_0..A_n, A_{n+1}, computed from the device's
+ * unit-vector solves Jp^-1 e_j.  NULL on error (drzg_last_error). */
+typedef struct drzg_pep_store drzg_pep_store;
+drzg_pep_store* drzg_pep_store_create(drzg_ctx* ctx, const char* spec);
+void drzg_pep_store_free(drzg_pep_store* store);
+/* entry for move vector v (n+1 exponents, |v| = d): planes_out (may be NULL)
+ * receives (n+2) x limbs x side x side u64 (ModMatrix plane layout per
+ * matrix, linalg.hpp:119-141), nnz_out the PepEntry::nnz count */
+int drzg_pep_get(drzg_pep_store* store, const int32_t* v, uint64_t* planes_out, int64_t* nnz_out);
+/* PepStats: hits, misses, evictions */
+int drzg_pep_stats(drzg_pep_store* store, int64_t* hits, int64_t* misses, int64_t* evictions);
+/* eval_to_linear(E, x, v, plan) — reduction.hpp:300-339: A = sum_i v_i A_i,
+ * B = sum_i x_i A_i + A_{n+1} (ModMatrix layout), the operands drzg_linrec_eval takes */
+int drzg_pep_eval_to_linear(drzg_pep_store* store, const int32_t* v, const int32_t* x, uint64_t* A, uint64_t* B);
+/* test hook: a store over stub entries (no device), for the backings' bookkeeping */
+drzg_pep_store* drzg_pep_store_create_stub(int32_t nv, int32_t d, const char* spec);
+
 #ifdef __cplusplus
 }
 #endif

@@ -724,4 +724,28 @@ char* ref_run_policy_states(u64 p, int n, int d, const u64* coeffs, int M, const
   });
 }
 
+
+// build_ruv(C, v) (reduction.hpp:253-297): the n+2 matrices in ModMatrix plane
+// layout, (n+2) x limbs x side x side, plus PepEntry::nnz
+int ref_build_ruv(u64 p, int n, int d, const u64* coeffs, int M, const char* policy, const int* v, u64* out,
+                  long* nnz) {
+  try {
+    Hypersurface X = make_x(p, n, d, coeffs);
+    StripePlan kp = StripePlan::make(p, M);
+    RuvContext C(X, kp, working_set_for(X, policy_from_name(policy)));
+    Expo vv(n + 1);
+    for (int i = 0; i <= n; ++i) vv[i] = v[i];
+    PepEntry E = build_ruv(C, vv);
+    size_t off = 0;
+    for (const auto& m : E.mats) {
+      std::memcpy(out + off, m.d.data(), sizeof(u64) * m.d.size());
+      off += m.d.size();
+    }
+    *nnz = E.nnz;
+    return 0;
+  } catch (...) {
+    return 1;
+  }
+}
+
 }  // extern "C"

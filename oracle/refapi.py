@@ -192,3 +192,18 @@ def run_policy_states(p, n, d, coeffs, M, policy, u, pole, w):
     w = np.ascontiguousarray(w, dtype=np.uint64)
     return _js(lib().ref_run_policy_states(ctypes.c_uint64(p), n, d, _u64(coeffs), M, policy.encode(), count, ua, pa,
                                            w.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+
+
+def build_ruv(p, n, d, coeffs, M, v, policy="p-chunk"):
+    """reference build_ruv(C, v): (n+2) x limbs x side x side u64 planes, nnz"""
+    import numpy as np
+    from math import comb
+    sp = stripe_plan_py(p, M)
+    side = comb(d * n - n + n, n)
+    out = np.zeros((n + 2) * sp["limbs"] * side * side, dtype=np.uint64)
+    nnz = ctypes.c_long()
+    rc = lib().ref_build_ruv(ctypes.c_uint64(p), n, d, _u64(coeffs), M, policy.encode(), _i32(v),
+                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(nnz))
+    if rc:
+        raise RuntimeError("reference build_ruv raised")
+    return out, nnz.value

@@ -321,3 +321,67 @@ class Context:
         g = np.ascontiguousarray(g, dtype=np.uint64).copy()
         _check(lib().drzg_floor_accumulate(ctypes.c_void_p(self.h), len(ids), self._ids(ids), g.ctypes.data_as(_P64)))
         return g
+
+
+class PepStore:
+    """PepStoreBase over a Context (reference reduction.hpp:143-147, pep.hpp:
+    15-209): spec "eager", "lazy", "lru:N" or "lfuda:N".  get(v) returns the
+    n+2 matrices of build_ruv(C, v) as ((n+2), limbs, side, side) u64 planes."""
+
+    def __init__(self, ctx, spec, _stub=None):
+        L = lib()
+        L.drzg_pep_store_create.restype = ctypes.c_void_p
+        L.drzg_pep_store_create_stub.restype = ctypes.c_void_p
+        self.ctx = ctx
+        if _stub is not None:
+            nv, d = _stub
+            self.h = L.drzg_pep_store_create_stub(nv, d, spec.encode())
+            self.nv = nv
+        else:
+            self.h = L.drzg_pep_store_create(ctypes.c_void_p(ctx.h), spec.encode())
+            self.nv = ctx.nv
+        if not self.h:
+            raise DrzgError(_err())
+
+    @classmethod
+    def stub(cls, nv, d, spec):
+        """bookkeeping-only store (no device): entries are placeholders"""
+        return cls(None, spec, _stub=(nv, d))
+
+    def close(self):
+        if self.h:
+            lib().drzg_pep_store_free(ctypes.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def get(self, v, planes=True):
+        va = (ctypes.c_int32 * self.nv)(*v)
+        nnz = ctypes.c_int64()
+        out = None
+        if planes and self.ctx is not None:
+            c = self.ctx
+            out = np.zeros((self.nv + 1, c.plan.limbs, c.side, c.side), dtype=np.uint64)
+            _check(lib().drzg_pep_get(ctypes.c_void_p(self.h), va, out.ctypes.data_as(_P64), ctypes.byref(nnz)))
+        else:
+            _check(lib().drzg_pep_get(ctypes.c_void_p(self.h), va, None, ctypes.byref(nnz)))
+        return out, nnz.value
+
+    def stats(self):
+        h, m, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().drzg_pep_stats(ctypes.c_void_p(self.h), ctypes.byref(h), ctypes.byref(m), ctypes.byref(e)))
+        return {"hits": h.value, "misses": m.value, "evictions": e.value}
+
+    def eval_to_linear(self, v, x):
+        """reference eval_to_linear(E, x, v, plan): (A, B) in ModMatrix layout"""
+        c = self.ctx
+        A = np.zeros(c.plan.limbs * c.side * c.side, dtype=np.uint64)
+        B = np.zeros_like(A)
+        _check(lib().drzg_pep_eval_to_linear(ctypes.c_void_p(self.h), (ctypes.c_int32 * self.nv)(*v),
+                                             (ctypes.c_int32 * self.nv)(*x), A.ctypes.data_as(_P64),
+                                             B.ctypes.data_as(_P64)))
+        return A, B

@@ -146,6 +146,8 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     std::fprintf(stderr, "[drzg] system order: %lld of %lld Jp blocks nonzero (%.3f s)\n", ord.blocks,
                  (long long)((T.nL + 127) / 128) * ((T.nL + 127) / 128),
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - to0).count());
+  pos_m_ = ord.pos_m;
+  pos_r_ = ord.pos_r;
   const std::vector<int>& pm = ord.pos_m;
   const std::vector<int>& pr = ord.pos_r;
   kblocks_ = ord.blocks;
@@ -214,9 +216,28 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
   const char* fl = std::getenv("DRZG_FLOW");
   flow_ = use_tc_ && sparse_carry_ && !fused_ && nLp_ % 128 == 0 && !(fl && std::string(fl) == "0");
+  const char* f2e = std::getenv("DRZG_FLOW2");
+  flow2_ = flow_ && !(f2e && std::string(f2e) == "0");
   if (sparse_carry_) {
     kb_ptr_.upload(ord.kb_ptr, st_);
     kb_idx_.upload(ord.kb_idx, st_);
+    // pair tiles (rows 256 i .. 256 i + 255): the union of the two K-block lists
+    const int nt = (int)ord.kb_ptr.size() - 1;
+    std::vector<int> p2{0}, i2;
+    for (int i = 0; 2 * i < nt; ++i) {
+      std::vector<int> u(ord.kb_idx.begin() + ord.kb_ptr[2 * i], ord.kb_idx.begin() + ord.kb_ptr[2 * i + 1]);
+      if (2 * i + 1 < nt) u.insert(u.end(), ord.kb_idx.begin() + ord.kb_ptr[2 * i + 1], ord.kb_idx.begin() + ord.kb_ptr[2 * i + 2]);
+      std::sort(u.begin(), u.end());
+      u.erase(std::unique(u.begin(), u.end()), u.end());
+      i2.insert(i2.end(), u.begin(), u.end());
+      p2.push_back((int)i2.size());
+    }
+    kblocks2_ = (long long)i2.size();
+    kb2_ptr_.upload(p2, st_);
+    kb2_idx_.upload(i2, st_);
+    if (std::getenv("DRZG_VERBOSE"))
+      std::fprintf(stderr, "[drzg] carry K blocks: %lld (128-row tiles), %lld (256-row pairs, x2 rows)\n", kblocks_,
+                   kblocks2_);
   }
   jp_ptr_.upload(jptr, st_);
   jp_col_.upload(jcol, st_);
@@ -603,9 +624,16 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     const size_t nctr = (size_t)(2 * T.dp.Ld - 1) * ((nb + 255) / 256);
     flow_ctr_.alloc(std::max<size_t>(nctr, (size_t)(2 * T.dp.Ld - 1) * ((bcap_ + 255) / 256)), st_);
     f.counters = flow_ctr_.p;
-    timed(&clock.gemm_ms, [&] { dixon_flow(C_.p, Jd_.p, f, st_); });
+    f.kb2_ptr = kb2_ptr_.p;
+    f.kb2_idx = kb2_idx_.p;
+    if (flow2_)
+      timed(&clock.gemm_ms, [&] { dixon_flow2(C_.p, Jd_.p, f, st_); });
+    else
+      timed(&clock.gemm_ms, [&] { dixon_flow(C_.p, Jd_.p, f, st_); });
     ++clock.gemm_launches;
     clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * nb;
+    // useful carry work: Jp's nonzero 128 x 128 blocks (the pair kernel
+    // also multiplies the zero blocks its union lists bring in)
     clock.carry_macs += (double)(T.dp.Ld - 1) * kblocks_ * 128 * 128 * nb;
     return;
   }
@@ -1699,6 +1727,42 @@ void ReductionEngine::run_rounds(std::vector<ColumnSeeds>& cols, std::vector<std
   G.assign(ncol, {});
   for (int c = 0; c < ncol; ++c)
     G[c].assign(hG.begin() + (size_t)c * Ld * gsize_, hG.begin() + (size_t)(c + 1) * Ld * gsize_);
+}
+
+
+std::vector<i8> ReductionEngine::solve_units(const std::vector<int>& rows) {
+  const RuvTables& T = *T_;
+  const int Ld = T.dp.Ld, B = (int)rows.size();
+  std::vector<i8> out((size_t)B * Ld * T.nL, 0);
+  if (!B) return out;
+  std::lock_guard<std::mutex> tmp_lock(tmp_mu_);
+  ensure_batch(std::min(B, 1 << 14));
+  std::vector<int8_t> hY;
+  for (int b0 = 0; b0 < B; b0 += bcap_) {
+    const int nb = std::min(bcap_, B - b0);
+    // b = e_j: digit 0 is 1 at the system-order position of row j
+    DRZG_CUDA(cudaMemsetAsync(Bg_.p, 0, Bg_.n, st_));
+    std::vector<int> pos(nb);
+    for (int s = 0; s < nb; ++s) {
+      DRZG_REQUIRE(rows[b0 + s] >= 0 && rows[b0 + s] < T.nL, "solve_units: row out of range");
+      pos[s] = pos_m_[rows[b0 + s]];
+    }
+    std::vector<int8_t> one(1, 1);
+    for (int s = 0; s < nb; ++s)
+      DRZG_CUDA(cudaMemcpyAsync(Bg_.p + (size_t)pos[s] * bcap_ + s, one.data(), 1, cudaMemcpyHostToDevice, st_));
+    dev::StepArgs a = make_args(0, nb, 0);
+    a.B = nb;
+    dixon(a);
+    DRZG_CUDA(cudaGetLastError());
+    hY.resize((size_t)Ld * nLp_ * bcap_);
+    DRZG_CUDA(cudaMemcpyAsync(hY.data(), Y_.p, hY.size(), cudaMemcpyDeviceToHost, st_));
+    DRZG_CUDA(cudaStreamSynchronize(st_));
+    for (int s = 0; s < nb; ++s)
+      for (int k = 0; k < Ld; ++k)
+        for (int r = 0; r < T.nL; ++r)
+          out[((size_t)(b0 + s) * Ld + k) * T.nL + r] = hY[((size_t)k * nLp_ + pos_r_[r]) * bcap_ + s];
+  }
+  return out;
 }
 
 }  // namespace drzg

@@ -200,6 +200,10 @@ class ReductionEngine {
   // policies (p-chunk has its own pipelined path, run_pchunk)
   void run_rounds(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led, Policy pol);
   const std::vector<Expo>& dirs() const { return dirs_host_; }
+  // y = Jp^{-1} e_j mod q^Ld for every listed Homog_L row j (the unit-echelon
+  // solves RuvContext::solve_column hands build_ruv, reduction.hpp:200-215):
+  // Ld balanced digits per solution index, [state][digit][r] (r in RuvTables order)
+  std::vector<i8> solve_units(const std::vector<int>& rows);
 
   KernelClock clock;
   bool tensor_cores() const { return use_tc_; }
@@ -240,6 +244,9 @@ class ReductionEngine {
   bool sparse_carry_ = false;  // carry GEMM over the nonzero K blocks of Jp only
   bool fused_ = false;         // whole solve in one launch (nLp <= 256; DRZG_FUSED=0 disables)
   bool flow_ = false;          // whole solve as one dataflow launch (larger systems; DRZG_FLOW=0 disables)
+  bool flow2_ = false;         // ... on CTA pairs, M = 256 tiles (DRZG_FLOW2=0 keeps single-CTA tiles)
+  DevBuf<int> kb2_ptr_, kb2_idx_;  // per 256-row tile: union of its 128-row tiles' nonzero K blocks
+  long long kblocks2_ = 0;
   DevBuf<int> flow_ctr_;       // its per-column phase counters
   long long kblocks_ = 0;      // nonzero 128 x 128 blocks of Jp (system order)
   DevBuf<int> kb_ptr_, kb_idx_;
@@ -284,6 +291,7 @@ class ReductionEngine {
   double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
   unsigned host_threads_ = std::max(1u, std::thread::hardware_concurrency());
   std::vector<Expo> dirs_host_;
+  std::vector<int> pos_m_, pos_r_;  // system order of Homog_L rows / solution indices
 };
 
 }  // namespace drzg

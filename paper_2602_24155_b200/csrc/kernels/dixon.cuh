@@ -219,19 +219,7 @@ __device__ __forceinline__ void epi_row(const EpiCtx& c, const long long (&roff)
   int tqb[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) tqb[j] = c.tq0;
-  uint32_t nxt[NT > 0 ? NT : 1];
-#pragma unroll
-  for (int e = 0; e < NT; ++e) nxt[e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + roff[e]));
-#pragma unroll
-  for (int t = 0; t < LD; ++t) {
-    uint32_t cur[NT > 0 ? NT : 1];
-#pragma unroll
-    for (int e = 0; e < NT; ++e) cur[e] = nxt[e];
-    if (t + 1 < LD) {
-#pragma unroll
-      for (int e = 0; e < NT; ++e)
-        nxt[e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + (size_t)(t + 1) * c.plane + roff[e]));
-    }
+  auto digit = [&](int t, const uint32_t* cur) {
     int dg[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -244,6 +232,33 @@ __device__ __forceinline__ void epi_row(const EpiCtx& c, const long long (&roff)
     }
     out[t] = __byte_perm(__byte_perm((uint32_t)dg[0], (uint32_t)dg[1], 0x0040),
                          __byte_perm((uint32_t)dg[2], (uint32_t)dg[3], 0x0040), 0x5410);
+  };
+  if constexpr (NT * LD <= 48) {
+    // every plane's words in flight at once: the row is latency-bound, and
+    // LD x NT independent 128-byte warp loads keep enough bytes in flight
+    uint32_t w[LD][NT > 0 ? NT : 1];
+#pragma unroll
+    for (int t = 0; t < LD; ++t)
+#pragma unroll
+      for (int e = 0; e < NT; ++e) w[t][e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + (size_t)t * c.plane + roff[e]));
+#pragma unroll
+    for (int t = 0; t < LD; ++t) digit(t, w[t]);
+  } else {
+    uint32_t nxt[NT > 0 ? NT : 1];
+#pragma unroll
+    for (int e = 0; e < NT; ++e) nxt[e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + roff[e]));
+#pragma unroll
+    for (int t = 0; t < LD; ++t) {
+      uint32_t cur[NT > 0 ? NT : 1];
+#pragma unroll
+      for (int e = 0; e < NT; ++e) cur[e] = nxt[e];
+      if (t + 1 < LD) {
+#pragma unroll
+        for (int e = 0; e < NT; ++e)
+          nxt[e] = __ldg(reinterpret_cast<const uint32_t*>(c.Y + (size_t)(t + 1) * c.plane + roff[e]));
+      }
+      digit(t, cur);
+    }
   }
 }
 

@@ -577,6 +577,209 @@ __device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
   return d;
 }
 
+
+// ---------------------------------------------------------------------------
+// The dataflow solve on CTA PAIRS (cta_group::2).  Same tiles, phases and
+// counters as dixon_flow_kernel, but a tile is 256 rows of Cq / Jp x 256
+// states, computed by the two CTAs of a cluster as one M = 256, N = 256
+// tcgen05.mma.cta_group::2: each CTA stages its own 128 rows of A and HALF of
+// B (128 states), so a K block costs each SM 32 KB of L2 -> SMEM traffic for
+// 128 x 256 x 128 MACs instead of 48 KB (the single-CTA kernel was L2-bound).
+// The leader CTA (rank 0) issues the MMAs; both CTAs' TMA loads complete on
+// the leader's full barrier; the MMA commits multicast to both CTAs' empty /
+// tfull barriers; both CTAs' epilogue warps release the accumulator on the
+// leader's tempty barrier.  Each CTA drains its own TMEM lanes (its 128 rows,
+// all 256 states).  Carry tiles run over the union of the two 128-row tiles'
+// nonzero K blocks.
+namespace f2 {
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK;        // 16 KB: this CTA's 128 rows
+constexpr int B_BYTES = (BN / 2) * BK;  // 16 KB: this CTA's 128 states
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
+}  // namespace f2
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's shared memory, completing on an mbarrier of either CTA of the pair
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive (once) on the barrier at this shared offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    dixon_flow2_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
+                       const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmIn,
+                       const __grid_constant__ CUtensorMap tmY, FlowArgs fa) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = base;
+  uint8_t* sB = base + f2::STAGES * f2::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + f2::STAGES * f2::B_BYTES);
+  uint64_t* full = bars;                           // leader's is used
+  uint64_t* empty = bars + f2::STAGES;             // each CTA's own
+  uint64_t* tfull = bars + 2 * f2::STAGES;         // [2], each CTA's own
+  uint64_t* tempty = bars + 2 * f2::STAGES + 2;    // [2], leader's is used
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * f2::STAGES + 4);
+  const TcEpiArgs& epi = fa.epi;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int nk = epi.nLp / BK;
+  const int mt = (epi.M + BM - 1) / BM;  // 128-row tiles (counter targets)
+  const int mt2 = (mt + 1) / 2;          // 256-row pair tiles
+  const int nph = 2 * epi.Ld - 1;
+  const int tiles = nph * fa.ncol * mt2;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < f2::STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmJ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB0) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmIn) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmY) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote use
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int t = cid; t < tiles; t += ncl) {
+        const FlowTile f = flow_tile(t, mt2, fa.ncol, fa.G, nph);
+        const int k = f.p >> 1;
+        const bool digit = !(f.p & 1);
+        const int m0 = f.mi * (2 * BM) + (int)rank * BM, n0 = f.col * BN + (int)rank * (BN / 2);
+        // every CTA of every pair tile of the previous phase publishes (also
+        // the half of a last pair that lies beyond the system when mt is odd)
+        if (f.p) flow_wait(fa.counters + (size_t)(f.p - 1) * fa.ncol + f.col, 2 * mt2 * EPI_WARPS);
+        const int kb0 = digit ? 0 : __ldg(fa.kb2_ptr + f.mi);
+        const int nkt = digit ? nk : __ldg(fa.kb2_ptr + f.mi + 1) - kb0;
+        const CUtensorMap* ma = digit ? &tmC : &tmJ;
+        const CUtensorMap* mb = digit ? (k ? &tmIn : &tmB0) : &tmY;
+        const int rowoff = digit ? 0 : k * epi.nLp;
+        for (int kb = 0; kb < nkt; ++kb, ++it) {
+          const int kc = (digit ? kb : __ldg(fa.kb2_idx + kb0 + kb)) * BK;
+          const int s = it % f2::STAGES;
+          mbar_wait(smem_u32(&empty[s]), ((it / f2::STAGES) & 1) ^ 1);
+          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+          if (rank == 0) mbar_expect_tx(smem_u32(&full[s]), 2 * (f2::A_BYTES + f2::B_BYTES));
+          tma_load_2d_pair(smem_u32(sA + s * f2::A_BYTES), ma, fb, kc, m0);
+          tma_load_2d_pair(smem_u32(sB + s * f2::B_BYTES), mb, fb, n0, rowoff + kc);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      int it = 0, i = 0;
+      for (int t = cid; t < tiles; t += ncl, ++i) {
+        const FlowTile f = flow_tile(t, mt2, fa.ncol, fa.G, nph);
+        const bool digit = !(f.p & 1);
+        const int acc = i & 1;
+        mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        const int nkt = digit ? nk : __ldg(fa.kb2_ptr + f.mi + 1) - __ldg(fa.kb2_ptr + f.mi);
+        const uint32_t idesc = digit ? fa.idesc_d : fa.idesc_c;
+        for (int kb = 0; kb < nkt; ++kb, ++it) {
+          const int s = it % f2::STAGES;
+          mbar_wait(smem_u32(&full[s]), (it / f2::STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t a0 = smem_u32(sA + s * f2::A_BYTES), b0 = smem_u32(sB + s * f2::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 32; ++kk)
+            mma_i8_pair(d, sw128_desc(a0 + kk * 32), sw128_mn_desc_1atom(b0 + kk * 4096), idesc, (kb | kk) != 0);
+          mma_commit_pair(smem_u32(&empty[s]));
+        }
+        mma_commit_pair(smem_u32(&tfull[acc]));
+      }
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    const int quarter = e & 3, half = e >> 2;
+    const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    int i = 0;
+    for (int t = cid; t < tiles; t += ncl, ++i) {
+      const FlowTile f = flow_tile(t, mt2, fa.ncol, fa.G, nph);
+      const int k = f.p >> 1;
+      const bool digit = !(f.p & 1);
+      const int m0 = f.mi * (2 * BM) + (int)rank * BM, n0 = f.col * BN;
+      const int acc = i & 1;
+      const int m = m0 + quarter * 32 + lane;
+      const bool mok = m < epi.M;
+      if (!digit) epi_carry_prefetch(epi, k, m, mok, n0 + half * (BN / 2));
+      mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
+      if (digit)
+        epi_digit_tile(epi, k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      else
+        epi_carry_tile<true>(epi, k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      __syncwarp();
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      if (lane == 0) mbar_arrive_cluster(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
+      // publish: this warp's rows of the tile are in global memory
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(fa.counters + (size_t)f.p * fa.ncol + f.col, 1);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();  // the peer's MMAs and remote arrivals are over before the TMEM goes
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+}
+
 // ---------------------------------------------------------------------------
 // Whole Dixon solve of a 128-state block in one CTA, for systems with
 // nLp <= 256 (the K3 surface: nL = 220).  Cq and Jp stay in shared memory
@@ -901,6 +1104,16 @@ void smem_opt_in(K* kernel, int bytes) {
 }  // namespace
 
 namespace {
+// grid rounds of tiles per phase of a column group: a tile's dependencies
+// (the previous phase of its column) were issued this many rounds earlier
+int flow_rounds() {
+  static const int r = [] {
+    const char* e = std::getenv("DRZG_FLOW_ROUNDS");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 1 && v <= 64 ? v : 2;
+  }();
+  return r;
+}
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -1059,7 +1272,7 @@ void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st)
   const int nph = 2 * e.Ld - 1;
   // columns per group: enough tiles per phase (~2 rounds of the grid) that a
   // tile's dependencies were issued a round earlier
-  fa.G = std::max(1, std::min(fa.ncol, (2 * sms + mt - 1) / mt));
+  fa.G = std::max(1, std::min(fa.ncol, (flow_rounds() * sms + mt - 1) / mt));
   {
     cudaError_t me = cudaMemsetAsync(fa.counters, 0, sizeof(int) * (size_t)nph * fa.ncol, st);
     DRZG_REQUIRE(me == cudaSuccess, std::string("dixon_flow counters: ") + cudaGetErrorString(me));
@@ -1068,6 +1281,61 @@ void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st)
   tc::dixon_flow_kernel<<<std::min(tiles, sms), tc::THREADS, tc::SMEM_BYTES, st>>>(mc, mj, mb0, min_, my, fa);
   cudaError_t err = cudaGetLastError();
   DRZG_REQUIRE(err == cudaSuccess, std::string("dixon_flow launch: ") + cudaGetErrorString(err));
+}
+
+
+void dixon_flow2(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st) {
+  TcEpiArgs& e = fa.epi;
+  DRZG_REQUIRE(fa.kb2_ptr && fa.kb2_idx, "dixon_flow2: the carry needs its pair K-block lists");
+  DRZG_REQUIRE(e.nLp % tc::BK == 0 && e.P % 64 == 0, "dixon_flow2: system order / pitch alignment");
+  e.b_mn = 1;
+  fa.ncol = (e.N + tc::BN - 1) / tc::BN;
+  CUtensorMap mc = make_map(C, e.nLp, e.nLp, e.nLp, tc::BM);
+  CUtensorMap mj = make_map(Jd, e.nLp, e.nLp, e.nLp, tc::BM);
+  CUtensorMap mb0 = make_map(e.Bg, e.nLp, e.P, e.P, tc::BK);
+  CUtensorMap min_ = make_map(e.IN, e.nLp, e.P, e.P, tc::BK);
+  CUtensorMap my = make_map(e.Y, e.Ld * e.nLp, e.P, e.P, tc::BK);
+  // kind::i8, D s32, B signed MN-major, N = 256, M = 256 (the pair)
+  const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(tc::BN >> 3) << 17) |
+                          ((uint32_t)((2 * tc::BM) >> 4) << 24);
+  fa.idesc_d = common | (1u << 7);  // Cq signed
+  fa.idesc_c = common;              // Jp unsigned
+  smem_opt_in(tc::dixon_flow2_kernel, tc::f2::SMEM_BYTES);
+  const int mt = (e.M + tc::BM - 1) / tc::BM, mt2 = (mt + 1) / 2;
+  const int nph = 2 * e.Ld - 1;
+  // every cluster must be resident at once (tiles wait on other clusters'
+  // counters): the grid is the number of co-resident pairs
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(tc::THREADS);
+  cfg.dynamicSmemBytes = tc::f2::SMEM_BYTES;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static thread_local int max_clusters[64] = {0};
+  const int dev = cur_device();
+  if (!max_clusters[dev]) {
+    cfg.gridDim = dim3(2 * (sm_count() / 2));
+    int nc = 0;
+    cudaError_t oe = cudaOccupancyMaxActiveClusters(&nc, tc::dixon_flow2_kernel, &cfg);
+    DRZG_REQUIRE(oe == cudaSuccess && nc > 0, std::string("dixon_flow2 occupancy: ") + cudaGetErrorString(oe));
+    max_clusters[dev] = nc;
+  }
+  fa.G = std::max(1, std::min(fa.ncol, (flow_rounds() * max_clusters[dev] + mt2 - 1) / mt2));
+  {
+    cudaError_t me = cudaMemsetAsync(fa.counters, 0, sizeof(int) * (size_t)nph * fa.ncol, st);
+    DRZG_REQUIRE(me == cudaSuccess, std::string("dixon_flow2 counters: ") + cudaGetErrorString(me));
+  }
+  const int tiles = nph * fa.ncol * mt2;
+  cfg.gridDim = dim3(2 * std::min(tiles, max_clusters[dev]));
+  cudaError_t err = cudaLaunchKernelEx(&cfg, tc::dixon_flow2_kernel, mc, mj, mb0, min_, my, fa);
+  DRZG_REQUIRE(err == cudaSuccess, std::string("dixon_flow2 launch: ") + cudaGetErrorString(err));
+  err = cudaGetLastError();
+  DRZG_REQUIRE(err == cudaSuccess, std::string("dixon_flow2 launch: ") + cudaGetErrorString(err));
 }
 
 }  // namespace drzg

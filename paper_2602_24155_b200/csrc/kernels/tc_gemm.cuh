@@ -78,7 +78,13 @@ struct FlowArgs {
   int ncol = 0, G = 0;       // 256-state columns, columns per group (set by dixon_flow)
   int* counters = nullptr;   // (2 Ld - 1) x ncol ints of device scratch
   uint32_t idesc_d = 0, idesc_c = 0;
+  // CTA-pair variant: per 256-row tile, the union of its two 128-row tiles'
+  // nonzero K blocks
+  const int* kb2_ptr = nullptr;
+  const int* kb2_idx = nullptr;
 };
 void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st);
+// the same dataflow solve on CTA pairs (cta_group::2, M = 256 tiles)
+void dixon_flow2(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st);
 
 }  // namespace drzg

@@ -147,3 +147,44 @@ def test_step_batch_and_combine_match_reference():
             c = sum(int(cw[i][t * side + r]) * int(sp.beta) ** t for t in range(sp.limbs))
             assert c == (2 * a) % mod
     ctx.close()
+
+
+PEP_CASES = [("quintic_f7_s1.json", 16, [[2, 1, 2], [1, 1, 3], [0, 2, 3]]),
+             ("k3_f11_s1_r1.json", 9, [[1, 1, 1, 1], [0, 1, 2, 1]]),
+             ("quintic_f7_s1.json", 24, [[2, 1, 2]])]  # two limbs
+
+
+@needs_ref
+@pytest.mark.parametrize("case", PEP_CASES, ids=lambda c: f"{c[0]}-M{c[1]}")
+def test_pep_entries_match_reference_build_ruv(case):
+    """PepStoreBase::get(v) == build_ruv(C, v) bit for bit (reduction.hpp:253-297),
+    through every backing, and the PEP route of a chunk (eval_to_linear +
+    linrec_eval on the device) == the reference's reduce_chunk"""
+    from oracle import refapi
+    name, M, moves = case
+    g = golden(name)
+    p, n, d = g["p"], g["n"], g["d"]
+    ctx = drzg.Context(p, n, d, g["coeffs"], M)
+    stores = {spec: drzg.PepStore(ctx, spec) for spec in ("lazy", "lru:1", "lfuda:1")}
+    for v in moves:
+        ref, ref_nnz = refapi.build_ruv(p, n, d, g["coeffs"], M, v)
+        for spec, st in stores.items():
+            got, nnz = st.get(v)
+            assert nnz == ref_nnz, spec
+            assert (got.reshape(-1) == ref).all(), spec
+    assert stores["lazy"].stats()["misses"] == len(moves)
+    # the reference chunk path through the store: k = 2 steps along v0 from u
+    v = moves[0]
+    u = [30 if i != n else 25 for i in range(n + 1)] if n == 3 else [20, 20, 23]
+    pole, k = 27 if n == 3 else 21, 2
+    x = [u[i] - k * v[i] for i in range(n + 1)]
+    A, B = stores["lazy"].eval_to_linear(v, x)
+    rng = np.random.default_rng(5)
+    sp = refapi.stripe_plan_py(p, M)
+    side = ctx.side
+    vals = [int(rng.integers(0, 2**62)) % (p ** M) for _ in range(side)]
+    w = np.array([(val // sp["beta"] ** t) % sp["beta"] for t in range(sp["limbs"]) for val in vals], dtype=np.uint64)
+    got_w, ctr = drzg.linrec_eval(p, M, side, A, B, k - 1, w)
+    ref_w, info = refapi.chunk(p, n, d, g["coeffs"], M, u, pole, v, k, w)
+    assert (got_w == ref_w).all() and ctr == k
+    ctx.close()
