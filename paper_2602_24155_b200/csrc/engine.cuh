@@ -289,7 +289,7 @@ class ReductionEngine {
   }
   Stager& stager_ = shared_stager();
   double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
-  unsigned host_threads_ = std::max(1u, std::thread::hardware_concurrency());
+  unsigned host_threads_ = usable_cores();
   std::vector<Expo> dirs_host_;
   std::vector<int> pos_m_, pos_r_;  // system order of Homog_L rows / solution indices
 };

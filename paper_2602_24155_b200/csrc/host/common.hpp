@@ -5,6 +5,9 @@
 // code plus a thread-local message.
 #pragma once
 
+#include <sched.h>
+#include <thread>
+
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -89,6 +92,23 @@ inline u128 mulm128(u128 a, u128 b, u128 m) {
   u128 r = (a * hi) % m;
   r = ((r << 40) + a * lo) % m;
   return r;
+}
+
+// host threads this process may run on: the affinity mask (a container's
+// cpuset), not every CPU of the node (std::thread::hardware_concurrency);
+// oversubscribed host threads stall the launcher and leave the GPU idle
+inline unsigned usable_cores() {
+  static const unsigned n = [] {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) {
+      const int c = CPU_COUNT(&set);
+      if (c > 0) return (unsigned)c;
+    }
+    const unsigned h = std::thread::hardware_concurrency();
+    return h ? h : 1u;
+  }();
+  return n;
 }
 
 }  // namespace drzg

@@ -45,6 +45,42 @@ inline void to_digits_u128(u128 v, const DigitPlan& dp, i8* out) {
     v = (v - (u128)(i128)r) / (u128)dp.q;  // exact; r may be negative
   }
 }
+// the same for v < q^Ld when q^Ld <= 2^127: one 128-bit division splits v
+// into base-q^c halves that fit 64 bits, then 64-bit digit extraction
+// (the seed expansion converts millions of residues per column)
+struct DigitSplitter {
+  int q = 0, Ld = 0, c = 0;  // q^c < 2^63
+  u64 qc = 1;
+  static DigitSplitter make(const DigitPlan& dp) {
+    DigitSplitter d;
+    d.q = dp.q;
+    d.Ld = dp.Ld;
+    while (d.c < dp.Ld && d.qc <= (u64(1) << 62) / (u64)dp.q) d.qc *= (u64)dp.q, ++d.c;
+    return d;
+  }
+  void digits(u128 v, i8* out) const {
+    u64 lo, hi;
+    if (c >= Ld) {
+      lo = (u64)v;
+      hi = 0;
+    } else {
+      lo = (u64)(v % qc);
+      hi = (u64)(v / qc);  // < q^(Ld - c) < 2^64 when Ld - c <= c
+    }
+    int carry = 0;
+    const int h = q / 2;
+    for (int t = 0; t < Ld; ++t) {
+      u64& src = t < c ? lo : hi;
+      const int r0 = (int)(src % (u64)q);
+      src /= (u64)q;
+      int r = r0 + carry;
+      carry = 0;
+      if (r > h) r -= q, carry = 1;
+      out[t] = (i8)r;
+    }
+  }
+};
+
 inline void to_digits_z(const Z& v0, const DigitPlan& dp, i8* out) {
   Z v = v0, q((long)dp.q);
   for (int t = 0; t < dp.Ld; ++t) {
@@ -133,6 +169,10 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
   const Expo one = Expo::ones(nv);
   const Expo& beta = B.mons[col];
   const DigitPlan& dp = T.dp;
+  const DigitSplitter split = DigitSplitter::make(dp);
+  const bool small_s = (smod >> 63) == 0;  // D_j, C_{j,alpha} < p^s: their product fits 128 bits
+  // v < p^M <= q^Ld; the 64-bit split covers q^Ld < 2^126 (Ld - c <= c)
+  const bool fast_digits = !hm.wide && 2 * split.c >= dp.Ld;
   for (int j = 0; j < N; ++j) {
     if (Dj[j] == 0) continue;
     int P = (int)p * (m + j);
@@ -143,7 +183,7 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
     const auto& tab = fj.table();
     for (int a = 0; a < fj.size(); ++a) {
       if (!fj.c[a]) continue;
-      u128 dc = mulm128(Dj[j], fj.c[a], smod);
+      u128 dc = small_s ? (Dj[j] * fj.c[a]) % smod : mulm128(Dj[j], fj.c[a], smod);
       if (dc == 0) continue;
       ++out.nterms;
       Expo full = beta + tab.mons[a] + one;
@@ -156,7 +196,12 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
       bk.g.push_back((i32)rank_of(wm));
       size_t off = bk.dig.size();
       bk.dig.resize(off + dp.Ld);
-      if (!hm.wide) {
+      if (fast_digits) {
+        // dc < p^s and kappa < p^M < 2^80: the product fits 128 bits when
+        // s bits + 80 < 128, one reduction
+        const u128 v = (dc >> 47) == 0 ? (dc * kap128) % hm.m128 : mulm128(dc, kap128, hm.m128);
+        split.digits(v, bk.dig.data() + off);
+      } else if (!hm.wide) {
         to_digits_u128(mulm128(dc, kap128, hm.m128), dp, bk.dig.data() + off);
       } else {
         to_digits_z((Z::from_u128(dc) * kap).mod(hm.mz), dp, bk.dig.data() + off);

@@ -173,16 +173,16 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
 // weights (x_i + mu_i per state) live in registers across the digit loop, so
 // the work per digit and state is NT byte-extract + multiply-adds and one
 // balanced division by q (multiply-high, bias folded into the running carry).
-constexpr int kEpiRows = 64, kEpiTermCap = 512, kEpiMaxNT = 6;
+constexpr int kEpiRows = 64, kEpiRowsMax = 512, kEpiTermCap = 1024, kEpiMaxNT = 6;
 static_assert(kEpiRows == StepArgs{}.epi_rows, "StepArgs::epi_rows defaults to kEpiRows");
 // rows per block for a batch of B states: kEpiRows when the batch fills the
 // GPU, else halved (down to one row per warp) until there are >= 8 blocks per
 // SM -- small batches are latency-bound, one warp per row in flight at once
 inline int epi_rows_for(int B, int side, int sms) {
   static const int fixed = [] {
-    const char* e = std::getenv("DRZG_EPI_ROWS");  // A/B override: 8, 16, 32 or 64
+    const char* e = std::getenv("DRZG_EPI_ROWS");  // A/B override: 8 ... 512
     const int r = e ? std::atoi(e) : 0;
-    return (r == 8 || r == 16 || r == 32 || r == 64) ? r : 0;
+    return (r == 8 || r == 16 || r == 32 || r == 64 || r == 128 || r == 256 || r == 512) ? r : 0;
   }();
   if (fixed) return fixed;
   const int bx = (B + 127) / 128;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
   __shared__ int xs_s[6][128];
   __shared__ int vd_s[128];
   __shared__ int ct_s[128];  // bit 0 valid, bit 1 continues
-  __shared__ int tp_s[kEpiRows + 1];
+  __shared__ int tp_s[kEpiRowsMax + 1];
   __shared__ int2 tm_s[kEpiTermCap];  // {r, i | mu << 8}
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int sb = blockIdx.x * 128;

@@ -144,6 +144,26 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// 32-byte (256-bit) per-lane global accesses: an epilogue lane owns one row
+// and 32 consecutive states, so every access of a warp touches 32 different
+// lines; one 256-bit instruction per line instead of two 128-bit ones halves
+// the L1 wavefronts, which bound the epilogues
+__device__ __forceinline__ void ld256_cg(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void ld256_nc(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void st256(void* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
+               "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 // Dixon carry epilogue of one tile row segment: c = (r_k - Jp y_k) / q
 // (exact), r_{k+1} = b_{k+1} + c, stored as in_{k+1} = bal(r_{k+1}) (the
 // next digit product's operand, in place over in_k) and its quotient h_{k+1}
@@ -163,15 +183,18 @@ __device__ __forceinline__ void epi_carry_prefetch(const TcEpiArgs& epi, int k, 
 
 template <bool COHERENT>
 __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
-                                               int cend, uint32_t tb) {
+                                               int cend, uint32_t tb, int cstep = 32) {
   // 32 states per step: every global access is a whole 32-byte sector
   const size_t P = (size_t)epi.P;
   const int8_t* rlo = (k ? epi.IN : epi.Bg) + (size_t)m * P;  // in_k, or b_0
   const int8_t* rhi = epi.H + (size_t)m * P;                    // h_k (k > 0)
   const int8_t* bk1p = epi.Bg + ((size_t)(k + 1) * epi.nLp + m) * P;
   const bool wh = k + 2 < epi.Ld;  // a later carry reads h_{k+1}
-  auto ld = [&](const int8_t* p) {
-    return COHERENT ? __ldcg(reinterpret_cast<const uint4*>(p)) : __ldg(reinterpret_cast<const uint4*>(p));
+  auto ld = [&](const int8_t* p, uint4 (&v)[2]) {
+    if (COHERENT)
+      ld256_cg(p, v[0], v[1]);
+    else
+      ld256_nc(p, v[0], v[1]);
   };
   uint4 nlo[2], nhi[2], nb1[2];
 #pragma unroll
@@ -179,19 +202,16 @@ __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int 
   auto fetch = [&](int c) {
     const int nb = n0 + c;
     if (!mok || nb >= epi.N) return;
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-      nlo[x] = ld(rlo + nb + 16 * x);
-      nb1[x] = __ldg(reinterpret_cast<const uint4*>(bk1p + nb + 16 * x));
-      if (k) nhi[x] = ld(rhi + nb + 16 * x);
-    }
+    ld(rlo + nb, nlo);
+    ld256_nc(bk1p + nb, nb1[0], nb1[1]);
+    if (k) ld(rhi + nb, nhi);
   };
   fetch(cbeg);
-  for (int c = cbeg; c < cend; c += 32) {
+  for (int c = cbeg; c < cend; c += cstep) {
     uint4 lo[2], hi[2], b1[2];
 #pragma unroll
     for (int x = 0; x < 2; ++x) lo[x] = nlo[x], hi[x] = nhi[x], b1[x] = nb1[x];
-    if (c + 32 < cend) fetch(c + 32);
+    if (c + cstep < cend) fetch(c + cstep);
     int v[32];
     tmem_ld32(tb + (uint32_t)c, v);
     const int nb = n0 + c;
@@ -225,21 +245,15 @@ __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int 
       o_in[x] = make_uint4(in4[0], in4[1], in4[2], in4[3]);
       o_h[x] = make_uint4(h4[0], h4[1], h4[2], h4[3]);
     }
-    uint4* di = reinterpret_cast<uint4*>(epi.IN + (size_t)m * P + nb);
-    di[0] = o_in[0];
-    di[1] = o_in[1];
-    if (wh) {
-      uint4* dh = reinterpret_cast<uint4*>(epi.H + (size_t)m * P + nb);
-      dh[0] = o_h[0];
-      dh[1] = o_h[1];
-    }
+    st256(epi.IN + (size_t)m * P + nb, o_in[0], o_in[1]);
+    if (wh) st256(epi.H + (size_t)m * P + nb, o_h[0], o_h[1]);
   }
 }
 
 // Dixon digit epilogue: Y[k][m][n0 + c ..] = bal(D), 32 states (one sector) per step
 __device__ __forceinline__ void epi_digit_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
-                                               int cend, uint32_t tb) {
-  for (int c = cbeg; c < cend; c += 32) {
+                                               int cend, uint32_t tb, int cstep = 32) {
+  for (int c = cbeg; c < cend; c += cstep) {
     int v[32];
     tmem_ld32(tb + (uint32_t)c, v);
     const int nb = n0 + c;
@@ -255,9 +269,8 @@ __device__ __forceinline__ void epi_digit_tile(const TcEpiArgs& epi, int k, int 
                 << (8 * b);
       w8[q4] = word;
     }
-    uint4* dy = reinterpret_cast<uint4*>(epi.Y + ((size_t)k * epi.nLp + m) * epi.P + nb);
-    dy[0] = make_uint4(w8[0], w8[1], w8[2], w8[3]);
-    dy[1] = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+    st256(epi.Y + ((size_t)k * epi.nLp + m) * epi.P + nb, make_uint4(w8[0], w8[1], w8[2], w8[3]),
+          make_uint4(w8[4], w8[5], w8[6], w8[7]));
   }
 }
 
@@ -592,6 +605,11 @@ __device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
 // all 256 states).  Carry tiles run over the union of the two 128-row tiles'
 // nonzero K blocks.
 namespace f2 {
+// 12 epilogue warps (3 per TMEM lane quarter, each a third of the 256 state
+// columns): the epilogues, not the MMAs, bound the dataflow solve, and 2
+// epilogue warps per scheduler could not hide their latencies
+constexpr int EPI_WARPS = 12;
+constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr int STAGES = 6;
 constexpr int A_BYTES = BM * BK;        // 16 KB: this CTA's 128 rows
 constexpr int B_BYTES = (BN / 2) * BK;  // 16 KB: this CTA's 128 states
@@ -637,11 +655,57 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
           bar)
       : "memory");
 }
+// The pair kernel's schedule: rounds of exactly one tile per cluster (the
+// grid is G * mt2 clusters, a round is one phase of one G-column group).
+// Three streams of column groups run one phase apart, round-robin, so every
+// cluster alternates digit and carry tiles: the long carry epilogue of one
+// tile overlaps the long digit MMA of the next (two carry tiles in a row left
+// the tensor pipe waiting on TMEM).  A tile's dependency (the previous phase
+// of its columns) is two rounds old.
+__device__ __forceinline__ bool flow2_slot(int r, int j, const FlowArgs& fa, int mt2, int nph, FlowTile& f) {
+  const int S = fa.streams;
+  const int st = r % S, q = r / S;
+  const int item = q - st;
+  if (item < 0) return false;
+  const int ph = item % nph, gs = item / nph;
+  const int group = st + S * gs;
+  if (group >= fa.ngroups) return false;
+  const int cg = j / mt2;
+  const int col = group * fa.G + cg;
+  if (cg >= fa.G || col >= fa.ncol) return false;
+  f.p = ph;
+  f.col = col;
+  f.mi = (j % mt2 + cg + ph) % mt2;
+  return true;
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+// the whole warp waits for a phase counter: lane 0 polls with relaxed loads
+// (an acquire per poll would invalidate L1 every time), then one acquire fence
+__device__ __forceinline__ void flow_wait_warp(const int* ctr, int target, int lane) {
+  if (lane == 0) {
+    for (uint32_t spin = 0;; ++spin) {
+      int v;
+      asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      __nanosleep(32);
+      if (spin > (1u << 27)) __trap();
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+  }
+  __syncwarp();
+}
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(f2::THREADS, 1)
     dixon_flow2_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
                        const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmIn,
                        const __grid_constant__ CUtensorMap tmY, FlowArgs fa) {
@@ -662,8 +726,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int mt = (epi.M + BM - 1) / BM;  // 128-row tiles (counter targets)
   const int mt2 = (mt + 1) / 2;          // 256-row pair tiles
   const int nph = 2 * epi.Ld - 1;
-  const int tiles = nph * fa.ncol * mt2;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int cid = blockIdx.x >> 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < f2::STAGES; ++s) {
@@ -672,7 +735,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&tfull[b]), 1);
-      mbar_init(smem_u32(&tempty[b]), 2 * EPI_WARPS);
+      mbar_init(smem_u32(&tempty[b]), 2 * f2::EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
@@ -692,38 +755,49 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
+  // producer and MMA roles run warp-uniformly (every lane walks the loop, one
+  // elected lane issues): the stage / phase / descriptor arithmetic then lives
+  // in uniform registers instead of being re-broadcast for every instruction
   if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;
-      for (int t = cid; t < tiles; t += ncl) {
-        const FlowTile f = flow_tile(t, mt2, fa.ncol, fa.G, nph);
-        const int k = f.p >> 1;
-        const bool digit = !(f.p & 1);
-        const int m0 = f.mi * (2 * BM) + (int)rank * BM, n0 = f.col * BN + (int)rank * (BN / 2);
-        // every CTA of every pair tile of the previous phase publishes (also
-        // the half of a last pair that lies beyond the system when mt is odd)
-        if (f.p) flow_wait(fa.counters + (size_t)(f.p - 1) * fa.ncol + f.col, 2 * mt2 * EPI_WARPS);
-        const int kb0 = digit ? 0 : __ldg(fa.kb2_ptr + f.mi);
-        const int nkt = digit ? nk : __ldg(fa.kb2_ptr + f.mi + 1) - kb0;
-        const CUtensorMap* ma = digit ? &tmC : &tmJ;
-        const CUtensorMap* mb = digit ? (k ? &tmIn : &tmB0) : &tmY;
-        const int rowoff = digit ? 0 : k * epi.nLp;
-        for (int kb = 0; kb < nkt; ++kb, ++it) {
-          const int kc = (digit ? kb : __ldg(fa.kb2_idx + kb0 + kb)) * BK;
-          const int s = it % f2::STAGES;
-          mbar_wait(smem_u32(&empty[s]), ((it / f2::STAGES) & 1) ^ 1);
-          const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t full0 = mapa_shared(smem_u32(&full[0]), 0);
+    for (int r = 0; r < fa.rounds; ++r) {
+      FlowTile f;
+      if (!flow2_slot(r, cid, fa, mt2, nph, f)) continue;
+      const int k = f.p >> 1;
+      const bool digit = !(f.p & 1);
+      const int m0 = f.mi * (2 * BM) + (int)rank * BM, n0 = f.col * BN + (int)rank * (BN / 2);
+      // every CTA of every pair tile of the previous phase publishes (also
+      // the half of a last pair that lies beyond the system when mt is odd)
+      if (f.p) flow_wait_warp(fa.counters + (size_t)(f.p - 1) * fa.ncol + f.col, 2 * mt2 * f2::EPI_WARPS, lane);
+      const int kb0 = digit ? 0 : __ldg(fa.kb2_ptr + f.mi);
+      const int nkt = digit ? nk : __ldg(fa.kb2_ptr + f.mi + 1) - kb0;
+      const CUtensorMap* ma = digit ? &tmC : &tmJ;
+      const CUtensorMap* mb = digit ? (k ? &tmIn : &tmB0) : &tmY;
+      const int rowoff = digit ? 0 : k * epi.nLp;
+      for (int kb = 0; kb < nkt; ++kb) {
+        const int kc = (digit ? kb : __ldg(fa.kb2_idx + kb0 + kb)) * BK;
+        mbar_wait(smem_u32(&empty[s]), ph ^ 1);
+        if (elect_one()) {
           if (rank == 0) mbar_expect_tx(smem_u32(&full[s]), 2 * (f2::A_BYTES + f2::B_BYTES));
-          tma_load_2d_pair(smem_u32(sA + s * f2::A_BYTES), ma, fb, kc, m0);
-          tma_load_2d_pair(smem_u32(sB + s * f2::B_BYTES), mb, fb, n0, rowoff + kc);
+          tma_load_2d_pair(smem_u32(sA + s * f2::A_BYTES), ma, full0 + 8 * s, kc, m0);
+          tma_load_2d_pair(smem_u32(sB + s * f2::B_BYTES), mb, full0 + 8 * s, n0, rowoff + kc);
         }
+        __syncwarp();
+        if (++s == f2::STAGES) s = 0, ph ^= 1;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      int it = 0, i = 0;
-      for (int t = cid; t < tiles; t += ncl, ++i) {
-        const FlowTile f = flow_tile(t, mt2, fa.ncol, fa.G, nph);
+    if (rank == 0) {
+      int s = 0, i = 0;
+      uint32_t ph = 0;
+      // descriptors: start address (>> 4) in bits 0-13; one MMA (K = 32)
+      // advances A by 32 bytes and B by 32 rows of 128 bytes
+      const uint64_t adesc0 = sw128_desc(smem_u32(sA)), bdesc0 = sw128_mn_desc_1atom(smem_u32(sB));
+      for (int r = 0; r < fa.rounds; ++r) {
+        FlowTile f;
+        if (!flow2_slot(r, cid, fa, mt2, nph, f)) continue;
         const bool digit = !(f.p & 1);
         const int acc = i & 1;
         mbar_wait(smem_u32(&tempty[acc]), ((i >> 1) & 1) ^ 1);
@@ -731,47 +805,67 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t d = tmem + (uint32_t)(acc * BN);
         const int nkt = digit ? nk : __ldg(fa.kb2_ptr + f.mi + 1) - __ldg(fa.kb2_ptr + f.mi);
         const uint32_t idesc = digit ? fa.idesc_d : fa.idesc_c;
-        for (int kb = 0; kb < nkt; ++kb, ++it) {
-          const int s = it % f2::STAGES;
-          mbar_wait(smem_u32(&full[s]), (it / f2::STAGES) & 1);
+        for (int kb = 0; kb < nkt; ++kb) {
+          mbar_wait(smem_u32(&full[s]), ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t a0 = smem_u32(sA + s * f2::A_BYTES), b0 = smem_u32(sB + s * f2::B_BYTES);
+          const uint64_t ad = adesc0 + (uint64_t)((s * f2::A_BYTES) >> 4);
+          const uint64_t bd = bdesc0 + (uint64_t)((s * f2::B_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 32; ++kk)
-            mma_i8_pair(d, sw128_desc(a0 + kk * 32), sw128_mn_desc_1atom(b0 + kk * 4096), idesc, (kb | kk) != 0);
-          mma_commit_pair(smem_u32(&empty[s]));
+            for (int kk = 0; kk < BK / 32; ++kk)
+              mma_i8_pair(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 256), idesc, (kb | kk) != 0);
+            mma_commit_pair(smem_u32(&empty[s]));
+          }
+          __syncwarp();
+          if (++s == f2::STAGES) s = 0, ph ^= 1;
         }
-        mma_commit_pair(smem_u32(&tfull[acc]));
+        if (elect_one()) mma_commit_pair(smem_u32(&tfull[acc]));
+        __syncwarp();
+        ++i;
       }
     }
   } else if (warp >= 4) {
     const int e = warp - 4;
-    const int quarter = e & 3, half = e >> 2;
+    // TMEM lane quarter (warp % 4) and which third of the 32-column chunks
+    const int quarter = e & 3, part = e >> 2;
+    const int cbeg = part * 32, cstep = 32 * (f2::EPI_WARPS / 4);
     const uint32_t tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
     int i = 0;
-    for (int t = cid; t < tiles; t += ncl, ++i) {
-      const FlowTile f = flow_tile(t, mt2, fa.ncol, fa.G, nph);
+    for (int r = 0; r < fa.rounds; ++r) {
+      FlowTile f;
+      if (!flow2_slot(r, cid, fa, mt2, nph, f)) continue;
       const int k = f.p >> 1;
       const bool digit = !(f.p & 1);
       const int m0 = f.mi * (2 * BM) + (int)rank * BM, n0 = f.col * BN;
       const int acc = i & 1;
       const int m = m0 + quarter * 32 + lane;
       const bool mok = m < epi.M;
-      if (!digit) epi_carry_prefetch(epi, k, m, mok, n0 + half * (BN / 2));
+      if (!digit) epi_carry_prefetch(epi, k, m, mok, n0 + cbeg);
       mbar_wait(smem_u32(&tfull[acc]), (i >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t tb = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN);
-      if (digit)
-        epi_digit_tile(epi, k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+      if (fa.debug == 1) {
+        for (int c = cbeg; c < BN; c += cstep) {
+          int v[32];
+          tmem_ld32(tb + (uint32_t)c, v);
+          if (v[0] == 0x7fffffff) fa.counters[0] = v[1];  // keep the loads
+        }
+      } else if (fa.debug == 2) {
+      } else if (digit)
+        epi_digit_tile(epi, k, m, mok, n0, cbeg, BN, tb, cstep);
       else
-        epi_carry_tile<true>(epi, k, m, mok, n0, half * (BN / 2), (half + 1) * (BN / 2), tb);
+        epi_carry_tile<true>(epi, k, m, mok, n0, cbeg, BN, tb, cstep);
       __syncwarp();
       asm volatile("tcgen05.fence::before_thread_sync;");
       if (lane == 0) mbar_arrive_cluster(tempty0 + (uint32_t)(acc * sizeof(uint64_t)));
-      // publish: this warp's rows of the tile are in global memory
-      __threadfence();
+      // publish: the warp barrier orders every lane's stores of the tile
+      // before lane 0's gpu-scope release (cumulative), which the consumer's
+      // acquire fence pairs with
       __syncwarp();
-      if (lane == 0) atomicAdd(fa.counters + (size_t)f.p * fa.ncol + f.col, 1);
+      if (lane == 0)
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(fa.counters + (size_t)f.p * fa.ncol + f.col)
+                     : "memory");
+      ++i;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -1301,6 +1395,11 @@ void dixon_flow2(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st
   fa.idesc_d = common | (1u << 7);  // Cq signed
   fa.idesc_c = common;              // Jp unsigned
   smem_opt_in(tc::dixon_flow2_kernel, tc::f2::SMEM_BYTES);
+  static const int dbg = [] {
+    const char* e = std::getenv("DRZG_FLOW_DEBUG");
+    return e ? std::atoi(e) : 0;
+  }();
+  fa.debug = dbg;
   const int mt = (e.M + tc::BM - 1) / tc::BM, mt2 = (mt + 1) / 2;
   const int nph = 2 * e.Ld - 1;
   // every cluster must be resident at once (tiles wait on other clusters'
@@ -1311,7 +1410,7 @@ void dixon_flow2(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.blockDim = dim3(tc::THREADS);
+  cfg.blockDim = dim3(tc::f2::THREADS);
   cfg.dynamicSmemBytes = tc::f2::SMEM_BYTES;
   cfg.stream = st;
   cfg.attrs = attr;
@@ -1325,13 +1424,23 @@ void dixon_flow2(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st
     DRZG_REQUIRE(oe == cudaSuccess && nc > 0, std::string("dixon_flow2 occupancy: ") + cudaGetErrorString(oe));
     max_clusters[dev] = nc;
   }
-  fa.G = std::max(1, std::min(fa.ncol, (flow_rounds() * max_clusters[dev] + mt2 - 1) / mt2));
+  // one round = one phase of a G-column group = one tile per cluster
+  fa.G = std::max(1, max_clusters[dev] / mt2);
+  fa.ngroups = (fa.ncol + fa.G - 1) / fa.G;
+  fa.streams = std::min(3, fa.ngroups);
+  {
+    int rounds = 0;
+    for (int st = 0; st < fa.streams; ++st) {
+      const int groups = (fa.ngroups - st + fa.streams - 1) / fa.streams;
+      rounds = std::max(rounds, fa.streams * (groups * nph + st));
+    }
+    fa.rounds = rounds;
+  }
   {
     cudaError_t me = cudaMemsetAsync(fa.counters, 0, sizeof(int) * (size_t)nph * fa.ncol, st);
     DRZG_REQUIRE(me == cudaSuccess, std::string("dixon_flow2 counters: ") + cudaGetErrorString(me));
   }
-  const int tiles = nph * fa.ncol * mt2;
-  cfg.gridDim = dim3(2 * std::min(tiles, max_clusters[dev]));
+  cfg.gridDim = dim3(2 * std::min(fa.G, fa.ncol) * mt2);
   cudaError_t err = cudaLaunchKernelEx(&cfg, tc::dixon_flow2_kernel, mc, mj, mb0, min_, my, fa);
   DRZG_REQUIRE(err == cudaSuccess, std::string("dixon_flow2 launch: ") + cudaGetErrorString(err));
   err = cudaGetLastError();

@@ -82,6 +82,9 @@ struct FlowArgs {
   // nonzero K blocks
   const int* kb2_ptr = nullptr;
   const int* kb2_idx = nullptr;
+  int ngroups = 0, streams = 1, rounds = 0;  // the pair kernel's round schedule (set by dixon_flow2)
+  int debug = 0;  // DRZG_FLOW_DEBUG (timing experiments only; results are wrong): 1 skip the
+                  // epilogue arithmetic and memory, 2 also the TMEM loads
 };
 void dixon_flow(const int8_t* C, const int8_t* Jd, FlowArgs fa, cudaStream_t st);
 // the same dataflow solve on CTA pairs (cta_group::2, M = 256 tiles)

@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <exception>
 #include <thread>
+#include <condition_variable>
+#include <mutex>
 
 #include "pipeline.cuh"
 #include "kernels/count.cuh"
@@ -51,40 +53,67 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     cols.push_back(j);
   }
   out.computed = cols;
-  // column expansions in parallel host threads (the reference threads over
-  // columns too, zeta.hpp:109-133); the final reducer's levels are built
-  // meanwhile on this thread
+  // column expansions on background host threads (the reference threads over
+  // columns too, zeta.hpp:109-133), overlapped with the device: a group of
+  // columns starts as soon as its own seeds exist, while later columns are
+  // still being expanded.  The final reducer's levels are built meanwhile.
   PowerCache pc;
   std::vector<ColumnSeeds> seeds(cols.size());
+  std::vector<char> ready(cols.size(), 0);
+  std::mutex smu;
+  std::condition_variable scv;
+  std::exception_ptr serr;
   FinalReducer fin(X, B, T.dp, hm);
-  {
-    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)std::thread::hardware_concurrency()));
-    std::atomic<size_t> next{0};
-    std::vector<std::exception_ptr> errs(nth);
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nth; ++t)
-      pool.emplace_back([&, t] {
+  // while the device runs, the engine's policy, launcher and seed-preparer
+  // threads need cores too: expansion takes half of them
+  const int nexp = std::max(1, std::min<int>((int)cols.size(), (int)std::max(1u, usable_cores() / 2)));
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> pool;
+  auto join_pool = [&] {
+    for (auto& th : pool)
+      if (th.joinable()) th.join();
+  };
+  for (int t = 0; t < nexp; ++t)
+    pool.emplace_back([&] {
+      for (size_t i = next++; i < cols.size(); i = next++) {
         try {
-          for (size_t i = next++; i < cols.size(); i = next++) seeds[i] = expand_column(X, B, plan, T, hm, pc, cols[i]);
+          ColumnSeeds cs = expand_column(X, B, plan, T, hm, pc, cols[i]);
+          std::lock_guard<std::mutex> lk(smu);
+          seeds[i] = std::move(cs);
+          ready[i] = 1;
         } catch (...) {
-          errs[t] = std::current_exception();
+          std::lock_guard<std::mutex> lk(smu);
+          if (!serr) serr = std::current_exception();
+          ready[i] = 1;
         }
-      });
+        scv.notify_all();
+      }
+    });
+  auto wait_column = [&](size_t i) -> ColumnSeeds& {
+    std::unique_lock<std::mutex> lk(smu);
+    scv.wait(lk, [&] { return ready[i] || serr; });
+    if (serr) {
+      lk.unlock();
+      join_pool();
+      std::rethrow_exception(serr);
+    }
+    return seeds[i];
+  };
+  try {
     fin.prepare();
-    for (auto& th : pool) th.join();
-    for (auto& e : errs)
-      if (e) std::rethrow_exception(e);
+  } catch (...) {
+    next = cols.size();
+    join_pool();
+    throw;
   }
-  for (auto& s : seeds) out.terms += s.nterms;
   double t2 = now_s();
-  out.t.seeds = t2 - t1;
 
   // columns run through the device engine in groups whose states fit HBM:
   // live states stay below ~60% of a group's seeds (SURVEY 8a peaks), and a
   // group may use half of the free memory
   std::vector<std::vector<i64>> G(cols.size());
-  double td0 = 0;
-  {
+  double td0 = 0, seed_wait = 0;
+  try {
     const double te0 = now_s();
     ReductionEngine eng(T, n, p, st);
     if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] engine setup %.3f s\n", now_s() - te0);
@@ -97,14 +126,22 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     while (c0 < cols.size()) {
       size_t c1 = c0;
       double need = 0;
+      const double w0 = now_s();
       while (c1 < cols.size()) {
-        double add = 0.6 * (double)seeds[c1].nterms * slot_bytes;
+        double add = 0.6 * (double)wait_column(c1).nterms * slot_bytes;
         if (c1 > c0 && need + add > budget) break;
         need += add;
         ++c1;
       }
-      std::vector<ColumnSeeds> grp(std::make_move_iterator(seeds.begin() + c0),
-                                   std::make_move_iterator(seeds.begin() + c1));
+      seed_wait += now_s() - w0;
+      std::vector<ColumnSeeds> grp;
+      {
+        std::lock_guard<std::mutex> lk(smu);
+        for (size_t i = c0; i < c1; ++i) {
+          out.terms += seeds[i].nterms;
+          grp.push_back(std::move(seeds[i]));
+        }
+      }
       std::vector<std::vector<i64>> Gg;
       const double tg = now_s();
       const i64 mv0 = out.led.matvecs;
@@ -122,15 +159,22 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     eng.clock.peak_live = eng.peak_live();
     out.clk = eng.clock;
     td0 = now_s();
+  } catch (...) {
+    next = cols.size();
+    join_pool();
+    throw;
   }
+  join_pool();
   double t3 = now_s();
   if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] engine teardown %.3f s\n", t3 - td0);
-  out.t.device = t3 - t2;
+  // seeds: the host time the device waited for expansions (the rest overlapped)
+  out.t.seeds = (t2 - t1) + seed_wait;
+  out.t.device = t3 - t2 - seed_wait;
 
   const int gsize = (int)mono_count(X.nv(), T.D - 1);
   std::vector<std::vector<Z>> colres(cols.size());
   {
-    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)std::thread::hardware_concurrency()));
+    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)usable_cores()));
     std::atomic<size_t> next{0};
     std::vector<std::exception_ptr> errs(nth);
     std::vector<std::thread> pool;
