@@ -31,6 +31,7 @@ __device__ __forceinline__ int balmod(int x, int q) {
   return r;
 }
 
+#ifndef DRZG_EPILOGUE_ONLY
 // b = P_v w at the first step of a chunk, from the slot pool into the
 // state-contiguous operand Bg.  A block owns 32 states: for each digit plane
 // it stages the 32 states' plane (32 x sidep bytes, coalesced 16-byte loads
@@ -161,6 +162,8 @@ __global__ void dixon_carry_kernel(StepArgs a, int k) {
   a.IN[off] = (int8_t)rem;
   a.H[off] = (int8_t)hq;
 }
+
+#endif  // DRZG_EPILOGUE_ONLY
 
 // w' = T_x y into W (Ld x sidep x P) or the next step's gathered operand Bg,
 // carry-normalised digits.  A block owns 128 states (each lane 4 consecutive
@@ -401,23 +404,28 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
     }
   }
 }
-// host dispatch over the digit-plane count
+// host dispatch over the digit-plane count; the instantiations live in four
+// translation units (kernels/epilogue_*.cu) so they compile in parallel
+void launch_epilogue_1_8(const StepArgs& a, dim3 grid, cudaStream_t st);
+void launch_epilogue_9_16(const StepArgs& a, dim3 grid, cudaStream_t st);
+void launch_epilogue_17_24(const StepArgs& a, dim3 grid, cudaStream_t st);
+void launch_epilogue_25_32(const StepArgs& a, dim3 grid, cudaStream_t st);
 inline void launch_epilogue(const StepArgs& a, dim3 grid, cudaStream_t st) {
-  switch (a.Ld) {
-#define DRZG_EPI(L) \
-  case L:           \
-    epilogue_kernel<L><<<grid, 256, 0, st>>>(a); \
-    break;
-    DRZG_EPI(1) DRZG_EPI(2) DRZG_EPI(3) DRZG_EPI(4) DRZG_EPI(5) DRZG_EPI(6) DRZG_EPI(7) DRZG_EPI(8)
-    DRZG_EPI(9) DRZG_EPI(10) DRZG_EPI(11) DRZG_EPI(12) DRZG_EPI(13) DRZG_EPI(14) DRZG_EPI(15) DRZG_EPI(16)
-    DRZG_EPI(17) DRZG_EPI(18) DRZG_EPI(19) DRZG_EPI(20) DRZG_EPI(21) DRZG_EPI(22) DRZG_EPI(23) DRZG_EPI(24)
-    DRZG_EPI(25) DRZG_EPI(26) DRZG_EPI(27) DRZG_EPI(28) DRZG_EPI(29) DRZG_EPI(30) DRZG_EPI(31) DRZG_EPI(32)
-#undef DRZG_EPI
-    default:
-      break;
-  }
+  if (a.Ld <= 8)
+    launch_epilogue_1_8(a, grid, st);
+  else if (a.Ld <= 16)
+    launch_epilogue_9_16(a, grid, st);
+  else if (a.Ld <= 24)
+    launch_epilogue_17_24(a, grid, st);
+  else
+    launch_epilogue_25_32(a, grid, st);
 }
+#define DRZG_EPI_CASE(L)                           \
+  case L:                                          \
+    epilogue_kernel<L><<<grid, 256, 0, st>>>(a);   \
+    break;
 
+#ifndef DRZG_EPILOGUE_ONLY
 // W -> slot pool for the batch columns [s_lo, s_hi) whose chunk ends here:
 // 32 states x 64 side rows per block, transposed through shared memory
 __global__ void __launch_bounds__(256) flush_kernel(StepArgs a, int s_lo, int s_hi) {
@@ -544,6 +552,8 @@ __global__ void floor_kernel(const int8_t* pool, long long slot_stride, int side
     if (dv) atomicAdd(reinterpret_cast<unsigned long long*>(Gc + (size_t)t * gsize + rank), (unsigned long long)(long long)dv);
   }
 }
+
+#endif  // DRZG_EPILOGUE_ONLY
 
 }  // namespace dev
 }  // namespace drzg
