@@ -186,6 +186,31 @@ int drzg_pep_eval_to_linear(drzg_pep_store* store, const int32_t* v, const int32
 /* test hook: a store over stub entries (no device), for the backings' bookkeeping */
 drzg_pep_store* drzg_pep_store_create_stub(int32_t nv, int32_t d, const char* spec);
 
+/* ---- multi-GPU: the Frobenius gather over NCCL -------------
+ *
+ * One process per GPU reduces a subset of the columns (drzg_frobenius with
+ * `columns`); the columns are independent (zeta.hpp:109-133).  drzg_gather_F
+ * assembles F on every rank with one ncclAllGather of 62-bit limbs plus each
+ * rank's column-ownership mask (no reduction: every entry has one owner, and
+ * NCCL's integer Sum would wrap mod 2^64).  The communicator is NCCL's:
+ * rank 0 makes the id, the caller ships it to the other ranks (e.g. over
+ * torch.distributed), every rank calls drzg_comm_init.  NCCL is resolved at
+ * run time (the process's libnccl.so.2, else the system one). */
+#define DRZG_NCCL_ID_BYTES 128
+typedef struct drzg_comm drzg_comm;
+int drzg_nccl_unique_id(uint8_t* id_out);
+drzg_comm* drzg_comm_init(int32_t nranks, const uint8_t* id, int32_t rank, int32_t device);
+void drzg_comm_free(drzg_comm* comm);
+/* F_local: b*b decimal strings (this rank's columns filled); cols: the ncols
+ * columns this rank owns; width: 62-bit limbs per entry.  JSON {"F": [...]}
+ * (the full matrix, on every rank); NULL on error */
+char* drzg_gather_F(drzg_comm* comm, int32_t b, const char* const* F_local, const int32_t* cols, int32_t ncols,
+                    int32_t width);
+/* test hook: the same encode/decode without NCCL for nranks blocks at once
+ * (F_blocks: nranks x b*b strings; rank r owns cols[col_ptr[r] .. col_ptr[r+1])) */
+char* drzg_gather_F_host(int32_t nranks, int32_t b, const char* const* F_blocks, const int32_t* cols,
+                         const int32_t* col_ptr, int32_t width);
+
 #ifdef __cplusplus
 }
 #endif

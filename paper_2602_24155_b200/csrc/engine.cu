@@ -214,6 +214,8 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
                                  T.dp.Ld * dev::kFlushRows * dev::kFlushStates));
   const char* fz = std::getenv("DRZG_FUSED");
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
+  const char* ck = std::getenv("DRZG_CHUNK");
+  chunk_ = fused_ && dixon_chunk_ok(nLp_, T.dp.Ld) && !(ck && std::string(ck) == "0");
   const char* fl = std::getenv("DRZG_FLOW");
   flow_ = use_tc_ && sparse_carry_ && !fused_ && nLp_ % 128 == 0 && !(fl && std::string(fl) == "0");
   const char* f2e = std::getenv("DRZG_FLOW2");
@@ -576,6 +578,23 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     f.fast = fast_ ? 1 : 0;
     f.Bg = Bg_.p;
     f.Y = Y_.p;
+    if (chunk_now_) {
+      // every step of the sub-batch's chunks in this launch (T_x in-kernel)
+      f.chunk = 1;
+      f.ks = a.ks;
+      f.vdir = a.vdir;
+      f.u0 = a.u0;
+      f.dirs = a.dirs;
+      f.t_ptr = a.t_ptr;
+      f.t_src = a.t_src;
+      f.sol_i = a.sol_i;
+      f.sol_mu = a.sol_mu;
+      f.ginv = a.ginv;
+      f.W = a.W;
+      f.side = a.side;
+      f.sidep = a.sidep;
+      f.nv = a.nv;
+    }
     static int traces = std::getenv("DRZG_FUSED_TRACE") ? 6 : 0;
     DevBuf<long long> tb;
     if (traces > 0 && nb <= 2048) {
@@ -597,8 +616,8 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
       std::fprintf(stderr, "\n");
     }
     ++clock.gemm_launches;
-    clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * nb;
-    clock.carry_macs += (double)(T.dp.Ld - 1) * T.nL * T.nL * nb;
+    clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * chunk_steps_;
+    clock.carry_macs += (double)(T.dp.Ld - 1) * T.nL * T.nL * chunk_steps_;
     return;
   }
   if (flow_) {
@@ -685,6 +704,14 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
   }
 }
 
+int ReductionEngine::chunk_max_states() const {
+  static const int mult = [] {
+    const char* e = std::getenv("DRZG_CHUNK_MAX");  // states per SM (A/B experiments)
+    return e ? std::atoi(e) : 64;
+  }();
+  return mult * sms_;
+}
+
 i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
   const RuvTables& T = *T_;
   const int B = (int)ks.size();
@@ -694,6 +721,30 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
   i64 mv = 0;
   for (int b0 = 0; b0 < B; b0 += bcap_) {
     const int nb = std::min(bcap_, B - b0);
+    // (only batches that fit one round of 32-state blocks: larger ones run
+    // 64-state blocks step by step, which a whole-chunk launch cannot hold in
+    // shared memory together with the block's y planes)
+    if (fused_ && chunk_ && nb <= chunk_max_states()) {
+      // small systems: gather, every step of every chunk in one launch (the
+      // fused Dixon solve with T_x in-kernel), then W -> pool for all
+      dev::StepArgs a = make_args(b0, nb, 1);
+      const int gb = (nb + dev::kGatherStates - 1) / dev::kGatherStates;
+      const size_t gsm = (size_t)dev::kGatherStates * sidep_;
+      timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gb, dev::kGatherThreads, gsm, st_>>>(a); });
+      i64 steps = 0;
+      for (int i = 0; i < nb; ++i) steps += ks[b0 + i];
+      chunk_now_ = true;
+      chunk_steps_ = (double)steps;
+      dixon(a);
+      chunk_now_ = false;
+      chunk_steps_ = 0;
+      dim3 gF((nb + dev::kFlushStates - 1) / dev::kFlushStates, (T.side + dev::kFlushRows - 1) / dev::kFlushRows);
+      size_t fsm = (size_t)T.dp.Ld * dev::kFlushRows * dev::kFlushStates;
+      timed(&clock.epi_ms, [&] { dev::flush_kernel<<<gF, 256, fsm, st_>>>(a, 0, nb); });
+      DRZG_CUDA(cudaGetLastError());
+      mv += steps;
+      continue;
+    }
     // prefix sizes: states of this sub-batch still stepping at y
     auto count_ge = [&](i64 y) {
       int c = 0;
@@ -709,6 +760,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
         const size_t gsm = (size_t)dev::kGatherStates * sidep_;
         timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gb, dev::kGatherThreads, gsm, st_>>>(a); });
       }  // later steps: the previous epilogue already wrote this step's operand
+      chunk_steps_ = (double)By;
       dixon(a);
       a.epi_rows = dev::epi_rows_for(By, T.side, sms_);
       dim3 gE((By + 127) / 128, (T.side + a.epi_rows - 1) / a.epi_rows);
@@ -1752,7 +1804,9 @@ std::vector<i8> ReductionEngine::solve_units(const std::vector<int>& rows) {
       DRZG_CUDA(cudaMemcpyAsync(Bg_.p + (size_t)pos[s] * bcap_ + s, one.data(), 1, cudaMemcpyHostToDevice, st_));
     dev::StepArgs a = make_args(0, nb, 0);
     a.B = nb;
+    chunk_steps_ = (double)nb;
     dixon(a);
+    chunk_steps_ = 0;
     DRZG_CUDA(cudaGetLastError());
     hY.resize((size_t)Ld * nLp_ * bcap_);
     DRZG_CUDA(cudaMemcpyAsync(hY.data(), Y_.p, hY.size(), cudaMemcpyDeviceToHost, st_));

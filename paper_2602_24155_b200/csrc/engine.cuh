@@ -226,6 +226,7 @@ class ReductionEngine {
   // per sub-batch, gather once from the pool, keep the state in W between
   // steps, flush to the pool where each chunk ends; returns matvecs
   i64 run_sweep(const std::vector<i64>& k_sorted);
+  int chunk_max_states() const;
   dev::StepArgs make_args(int b0, int nb, int y);
   void dixon(dev::StepArgs& a);
   void timed(double* acc, const std::function<void()>& f);
@@ -243,6 +244,9 @@ class ReductionEngine {
   bool fast_ = false;   // fp32-reciprocal residues (host-checked operand bound)
   bool sparse_carry_ = false;  // carry GEMM over the nonzero K blocks of Jp only
   bool fused_ = false;         // whole solve in one launch (nLp <= 256; DRZG_FUSED=0 disables)
+  bool chunk_ = false;         // ... every step of a chunk in that launch, T_x in-kernel (DRZG_CHUNK=0 disables)
+  bool chunk_now_ = false;     // the current dixon() call is a whole-chunk launch
+  double chunk_steps_ = 0;     // state-steps of the current dixon() call (accounting)
   bool flow_ = false;          // whole solve as one dataflow launch (larger systems; DRZG_FLOW=0 disables)
   bool flow2_ = false;         // ... on CTA pairs, M = 256 tiles (DRZG_FLOW2=0 keeps single-CTA tiles)
   DevBuf<int> kb2_ptr_, kb2_idx_;  // per 256-row tile: union of its 128-row tiles' nonzero K blocks

@@ -324,15 +324,22 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
   const int* ginv = a.ginv;
   for (int g = g0 + warp; g < g1; g += 8) {
     const int eb = tp_s[g - g0], nt = tp_s[g - g0 + 1] - eb;
+    // a row no solution index feeds (1742 of the fourfold's 3003) is zero in
+    // every step's output: the step-1 epilogue zeroed its next-step operand
+    // row, and no one writes that row of Bg again during the chunk
+    if (a.y >= 2 && nt == 0 && all_cont) continue;
     // next step's operand row of side row g (per state's v), or W at chunk end
     int rn[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? __ldg(ginv + (size_t)vds[j] * side + g) : -1;
+    // the write target of whole-lane words, fixed per row
+    const bool lane_word = none_cont || (all_cont && same_v);
+    int8_t* dst = none_cont ? c.W + (size_t)g * c.P + s4
+                            : (rn[0] >= 0 ? c.Bg + (size_t)rn[0] * c.P + s4 : nullptr);
+    const size_t dstride = none_cont ? c.wplane : c.plane;
     auto put = [&](int t, uint32_t word) {
-      if (none_cont) {
-        *reinterpret_cast<uint32_t*>(c.W + (size_t)t * c.wplane + (size_t)g * c.P + s4) = word;
-      } else if (all_cont && same_v) {
-        if (rn[0] >= 0) *reinterpret_cast<uint32_t*>(c.Bg + (size_t)t * c.plane + (size_t)rn[0] * c.P + s4) = word;
+      if (lane_word) {
+        if (dst) *reinterpret_cast<uint32_t*>(dst + (size_t)t * dstride) = word;
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {

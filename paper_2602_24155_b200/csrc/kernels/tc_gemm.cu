@@ -922,6 +922,69 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t addr) {
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+
+// chunk mode: steps of block b (its first state's k; states are sorted by k
+// descending), else one
+__device__ __forceinline__ int fused_steps(const FusedArgs& fa, int b, int NS) {
+  if (!fa.chunk) return 1;
+  const long long k = __ldg(reinterpret_cast<const long long*>(fa.ks) + (size_t)b * NS);
+  return k < 1 ? 1 : (int)k;
+}
+
+// chunk mode: w' = T_x y for the block's states at step y (the T_x
+// epilogue of the reduction step, reduction.hpp:394-423 / DESIGN.md): side
+// row g of state s gets sum over the solution indices r feeding g of
+// (x_i + mu_i) y[r], x = u0 - y v, carry-normalised into Ld balanced digits;
+// written to the next step's operand row ginv[v][g] of Bg while the chunk
+// continues (y < k), to W at its last step (y == k), nothing after it.
+// Thread `et` of the 16 epilogue warps: state et % NS, rows g = et / NS + j
+// (512 / NS).  y comes from shared memory (the block's Ld planes, sYall).
+__device__ __forceinline__ void fused_tx_phase(const FusedArgs& fa, int b, int y, int NS, int et,
+                                               const int8_t* sYall) {
+  constexpr int kThreads = 32 * fz::EPI_WARPS;
+  const int sl = et % NS, grp = et / NS, ngrp = kThreads / NS;
+  const int s = b * NS + sl;
+  if (s >= fa.N) return;
+  const long long ks = __ldg(reinterpret_cast<const long long*>(fa.ks) + s);
+  if (y > ks) return;
+  const bool cont = y < ks;
+  const int vd = __ldg(fa.vdir + s);
+  int x[6] = {0, 0, 0, 0, 0, 0};
+  for (int i2 = 0; i2 < fa.nv; ++i2) x[i2] = __ldg(fa.u0 + (size_t)s * fa.nv + i2) - y * __ldg(fa.dirs + (size_t)vd * fa.nv + i2);
+  const size_t P = (size_t)fa.P, plane = (size_t)fa.nLp * P, wplane = (size_t)fa.sidep * P;
+  const int h = fa.q >> 1;
+  for (int g = grp; g < fa.side; g += ngrp) {
+    const int tb = __ldg(fa.t_ptr + g), te = __ldg(fa.t_ptr + g + 1);
+    int rr[6], ww[6];
+    const int nt = te - tb < 6 ? te - tb : 6;
+    for (int e2 = 0; e2 < nt; ++e2) {
+      const int r = __ldg(fa.t_src + tb + e2);
+      rr[e2] = r;
+      ww[e2] = x[__ldg(fa.sol_i + r)] + __ldg(fa.sol_mu + r);
+    }
+    const int rn = cont ? __ldg(fa.ginv + (size_t)vd * fa.side + g) : -1;
+    int carry = 0;
+    for (int t = 0; t < fa.Ld; ++t) {
+      int acc = carry;
+      const int8_t* yt = sYall + (size_t)t * fa.nLp * NS + sl;
+      for (int e2 = 0; e2 < nt; ++e2) acc += ww[e2] * (int)yt[(size_t)rr[e2] * NS];
+      for (int e2 = 6; e2 < te - tb; ++e2) {  // wide rows (none in the BASELINE shapes)
+        const int r = __ldg(fa.t_src + tb + e2);
+        acc += (x[__ldg(fa.sol_i + r)] + __ldg(fa.sol_mu + r)) * (int)yt[(size_t)r * NS];
+      }
+      int rem;
+      int qt = fa.fq.divfloor(acc, rem);
+      if (rem > h) rem -= fa.q, ++qt;
+      carry = qt;
+      if (cont) {
+        if (rn >= 0) const_cast<int8_t*>(fa.Bg)[t * plane + (size_t)rn * P + s] = (int8_t)rem;
+      } else {
+        fa.W[t * wplane + (size_t)g * P + s] = (int8_t)rem;
+      }
+    }
+  }
+}
+
 template <int NS>
 __global__ void __launch_bounds__(fz::THREADS, 1)
     dixon_fused_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
@@ -935,6 +998,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
   uint8_t* sY = sIn + nt * fz::box_bytes(NS);
   uint8_t* sH = sY + nt * fz::box_bytes(NS);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sH + nt * fz::box_bytes(NS));
+  // chunk mode: every y plane of the block, [k][row][state], for the in-CTA T_x
+  int8_t* sYall = reinterpret_cast<int8_t*>(reinterpret_cast<uint8_t*>(bars) + 256);
   uint64_t* barA = bars;      // Cq, Jp loaded
   uint64_t* barB0 = bars + 1; // b_0 of the block loaded
   uint64_t* barD = bars + 2;  // digit product done
@@ -942,7 +1007,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
   uint64_t* barY = bars + 4;  // y_k drained (every epilogue warp)
   uint64_t* barIn = bars + 5; // in_{k+1}, h_{k+1} written (every epilogue warp)
   uint64_t* barFree = bars + 6;  // a block's last digit product done: sIn may be refilled
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7);
+  uint64_t* barTx = bars + 7;    // chunk mode: T_x of the block's step written (every epilogue warp)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Ld = fa.Ld;
   const int nblk = (fa.N + NS - 1) / NS;
@@ -955,6 +1021,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     mbar_init(smem_u32(barY), fz::EPI_WARPS);
     mbar_init(smem_u32(barIn), fz::EPI_WARPS);
     mbar_init(smem_u32(barFree), 1);
+    mbar_init(smem_u32(barTx), fz::EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmJ) : "memory");
@@ -979,21 +1046,25 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
           tma_load_2d(smem_u32(sJ + (mt * nt + kb) * fz::TILE), &tmJ, smem_u32(barA), kb * 128, mt * 128);
         }
       int i = 0;
-      for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
-        // the previous block's last digit product has consumed sIn (a
-        // barrier of its own: barD runs Ld phases per block, and a parity
-        // wait only tells the current phase from the one before it)
-        if (i) mbar_wait(smem_u32(barFree), (uint32_t)((i - 1) & 1));
-        mbar_expect_tx(smem_u32(barB0), (uint32_t)(nt * fz::box_bytes(NS)));
-        for (int kb = 0; kb < nt; ++kb)
-          tma_load_2d(smem_u32(sIn + kb * fz::box_bytes(NS)), &tmB0, smem_u32(barB0), b * NS, kb * 128);
-      }
+      for (int b = blockIdx.x; b < nblk; b += gridDim.x)
+        for (int y = 1, ny = fused_steps(fa, b, NS); y <= ny; ++y, ++i) {
+          // the previous item's last digit product has consumed sIn (a
+          // barrier of its own: barD runs Ld phases per item, and a parity
+          // wait only tells the current phase from the one before it)
+          if (i) mbar_wait(smem_u32(barFree), (uint32_t)((i - 1) & 1));
+          // chunk mode, later steps: the block's T_x wrote this step's b (Bg)
+          if (y > 1) mbar_wait(smem_u32(barTx), (uint32_t)((i - 1) & 1));
+          mbar_expect_tx(smem_u32(barB0), (uint32_t)(nt * fz::box_bytes(NS)));
+          for (int kb = 0; kb < nt; ++kb)
+            tma_load_2d(smem_u32(sIn + kb * fz::box_bytes(NS)), &tmB0, smem_u32(barB0), b * NS, kb * 128);
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       mbar_wait(smem_u32(barA), 0);
       int i = 0;
-      for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
+      for (int b = blockIdx.x; b < nblk; b += gridDim.x)
+        for (int y = 1, ny = fused_steps(fa, b, NS); y <= ny; ++y, ++i) {
         if (i) mbar_wait(smem_u32(barY), (uint32_t)((i * Ld - 1) & 1));  // last digit drained
         mbar_wait(smem_u32(barB0), (uint32_t)(i & 1));
         for (int k = 0; k < Ld; ++k) {
@@ -1047,7 +1118,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
     };
     stamp(0);
     int i = 0;
-    for (int b = blockIdx.x; b < nblk; b += gridDim.x, ++i) {
+    for (int b = blockIdx.x; b < nblk; b += gridDim.x)
+      for (int y = 1, ny = fused_steps(fa, b, NS); y <= ny; ++y, ++i) {
       const int n0 = b * NS + half * (NS / 2);
       constexpr int NCH = NS / 32;           // 16-state chunks per thread
       constexpr int PER = NCH >= 2 ? 2 : 1;  // chunks per TMEM load (32 or 16 columns)
@@ -1060,7 +1132,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
           const int8_t* src = fa.Bg + ((size_t)(k + 1) * fa.nLp + m) * P + n0;
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch)
-            b1[ch] = n0 + ch * 16 < fa.N ? __ldg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
+            b1[ch] = n0 + ch * 16 < fa.N ? __ldcg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
         }
         mbar_wait(smem_u32(barD), (uint32_t)(d & 1));
         if (i == 0) stamp(1 + 4 * k);
@@ -1091,7 +1163,10 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
               }
               const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
               if (carry) *reinterpret_cast<uint4*>(sY + swz<NS>(m, half * (NS / 2) + ch * 16)) = y4;
-              if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
+              if (fa.chunk)
+                *reinterpret_cast<uint4*>(sYall + ((size_t)k * fa.nLp + m) * NS + half * (NS / 2) + ch * 16) = y4;
+              else if (m < fa.nL && n0 + ch * 16 < fa.N)
+                *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
             }
           }
         }
@@ -1152,6 +1227,17 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(barIn));
         if (i == 0) stamp(4 + 4 * k);
+      }
+      if (fa.chunk) {
+        // every y plane of the block is in shared memory
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * fz::EPI_WARPS) : "memory");
+        fused_tx_phase(fa, b, y, NS, e * 32 + lane, sYall);
+        // generic writes of Bg before the producer's TMA reads of the next
+        // step, and before any warp's next-step reads of Bg and sYall
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"r"(32 * fz::EPI_WARPS) : "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(barTx));
       }
     }
   }
@@ -1308,7 +1394,7 @@ void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs&
   // kind::i8, D s32, B signed MN-major, N = NS, M = 128; A signed (Cq) / unsigned (Jp)
   const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
   const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
-  const int smem = tc::fz::smem_bytes(nt, NS);
+  const int smem = tc::fz::smem_bytes(nt, NS) + (fa.chunk ? fa.Ld * fa.nLp * NS : 0);
   smem_opt_in(tc::dixon_fused_kernel<NS>, smem);
   const int nblk = (fa.N + NS - 1) / NS;
   static const bool one_block = std::getenv("DRZG_FUSED_ONEBLOCK") != nullptr;  // debug: one block per CTA
@@ -1318,6 +1404,8 @@ void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs&
 }  // namespace
 
 bool dixon_fused_ok(int nLp) { return nLp % 128 == 0 && nLp <= 256; }
+// whole-chunk launches keep the block's Ld y planes in shared memory too
+bool dixon_chunk_ok(int nLp, int Ld) { return dixon_fused_ok(nLp) && tc::fz::smem_bytes(nLp / 128, 32) + Ld * nLp * 32 <= 227 * 1024; }
 
 void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st) {
   DRZG_REQUIRE(dixon_fused_ok(fa.nLp), "dixon_fused: system order must be 128 or 256");
@@ -1333,7 +1421,7 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
   // (large batches: 64-state blocks beat 128 too, 82 vs 86 ms of fused time
   // per K3 zeta function -- the per-digit epilogue phase is what a block
   // waits on, and it halves; DRZG_FUSED_NS=128 keeps the 128-state variant)
-  const int ns = ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : 64);
+  const int ns = fa.chunk ? 32 : ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : 64);
   if (ns == 32)
     launch_fused<32>(mc, mj, fa, sms, st);
   else if (ns == 64)

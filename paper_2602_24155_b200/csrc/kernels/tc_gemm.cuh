@@ -65,8 +65,22 @@ struct FusedArgs {
   const int8_t* Bg = nullptr;  // Ld x nLp x P gathered digits (plane 0 is read through TMA)
   int8_t* Y = nullptr;         // Ld x nLp x P: y_k out
   long long* trace = nullptr;  // debug: %globaltimer stamps of CTA 0's first epilogue thread
+  // chunk mode: every step of each state's chunk in this launch.  After a
+  // block's Dixon solve the CTA applies T_x itself (w' = T_x y, reduction
+  // step epilogue) and writes the next step's operand Bg (through ginv) or,
+  // at the state's last step, W; the block's next step then reloads b_0.
+  // States are sorted by k descending, so a block runs k of its first state.
+  int chunk = 0;
+  const int64_t* ks = nullptr;  // N: chunk length of each state
+  const int* vdir = nullptr;    // N
+  const int* u0 = nullptr;      // N x nv (exponent at the chunk start)
+  const int* dirs = nullptr;    // ndir x nv
+  const int *t_ptr = nullptr, *t_src = nullptr, *sol_i = nullptr, *sol_mu = nullptr, *ginv = nullptr;
+  int8_t* W = nullptr;          // Ld x sidep x P
+  int side = 0, sidep = 0, nv = 0;
 };
 bool dixon_fused_ok(int nLp);
+bool dixon_chunk_ok(int nLp, int Ld);
 void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStream_t st);
 
 

@@ -99,3 +99,84 @@ def gather_frobenius(F_local, b: int, cols: Sequence[int], world: int, all_cols:
     outs = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(outs, t)
     return decode_blocks([o.tolist() for o in outs], all_cols, b, width)
+
+
+# --------------------------------------------------------------------------
+# the same gather behind the C ABI (include/drzg.h drzg_gather_F): one
+# ncclAllGather issued by libdrzg.so itself; torch.distributed only ships the
+# NCCL unique id from rank 0 to the others.
+
+_COMM = {}
+
+
+def nccl_comm(world: int, rank: int, device: int):
+    """the process's drzg_comm (created once per (world, rank, device))"""
+    import ctypes
+    import torch.distributed as dist
+    from . import lib, DrzgError, _err
+    key = (world, rank, device)
+    if key in _COMM:
+        return _COMM[key]
+    L = lib()
+    buf = (ctypes.c_uint8 * 128)()
+    if rank == 0 and L.drzg_nccl_unique_id(buf) != 0:
+        raise DrzgError(_err())
+    obj = [bytes(buf)]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
+    L.drzg_comm_init.restype = ctypes.c_void_p
+    h = L.drzg_comm_init(world, (ctypes.c_uint8 * 128)(*obj[0]), rank, device)
+    if not h:
+        raise DrzgError(_err())
+    _COMM[key] = h
+    return h
+
+
+def gather_frobenius_nccl(F_local, b: int, cols: Sequence[int], world: int, rank: int, device: int,
+                          width: int = 6) -> List[int]:
+    """drzg_gather_F: every rank gets the full F (Python ints)"""
+    import ctypes
+    import json
+    from . import lib, DrzgError, _err
+    L = lib()
+    L.drzg_gather_F.restype = ctypes.c_void_p
+    arr = (ctypes.c_char_p * (b * b))(*[str(x).encode() for x in F_local])
+    ca = (ctypes.c_int32 * max(1, len(cols)))(*cols)
+    ptr = L.drzg_gather_F(ctypes.c_void_p(nccl_comm(world, rank, device)), b, arr, ca, len(cols), width)
+    if not ptr:
+        raise DrzgError(_err())
+    s = ctypes.cast(ptr, ctypes.c_char_p).value.decode()
+    L.drzg_free(ctypes.c_void_p(ptr))
+    return [int(x) for x in json.loads(s)["F"]]
+
+
+def gather_frobenius_host(blocks, b: int, owners: Sequence[Sequence[int]], width: int = 6) -> List[int]:
+    """drzg_gather_F_host: the C++ encode/decode of the gather for several
+    ranks' blocks at once (no NCCL; CPU tests)"""
+    import ctypes
+    import json
+    from . import lib, DrzgError, _err
+    L = lib()
+    L.drzg_gather_F_host.restype = ctypes.c_void_p
+    flat = [str(x).encode() for blk in blocks for x in blk]
+    cols = [j for o in owners for j in o]
+    ptrs = [0]
+    for o in owners:
+        ptrs.append(ptrs[-1] + len(o))
+    ptr = L.drzg_gather_F_host(len(blocks), b, (ctypes.c_char_p * len(flat))(*flat),
+                               (ctypes.c_int32 * max(1, len(cols)))(*cols), (ctypes.c_int32 * len(ptrs))(*ptrs),
+                               width)
+    if not ptr:
+        raise DrzgError(_err())
+    s = ctypes.cast(ptr, ctypes.c_char_p).value.decode()
+    L.drzg_free(ctypes.c_void_p(ptr))
+    return [int(x) for x in json.loads(s)["F"]]
+
+
+def replayed_column_weights(ledger_fixture: str) -> List[float]:
+    """per-column matvecs of the reference's replayed ledger (scripts/
+    replay_ledger.py): the exact work of each column, for partition_columns"""
+    import json
+    with open(ledger_fixture) as f:
+        g = json.load(f)
+    return [float(c[0]) for c in g["columns"]]

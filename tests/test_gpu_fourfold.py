@@ -74,3 +74,13 @@ def test_fourfold_columns_assemble_to_reference_F():
             for j in cols:
                 F[i * b + j] = fr["F"][i * b + j]
     assert F == g["F"]
+
+
+def test_nccl_gather_behind_the_c_abi():
+    """drzg_comm_init + drzg_gather_F on one rank (the driver's GPU tests run
+    on one GPU): the NCCL all_gather path in libdrzg.so round-trips F"""
+    from paper_2602_24155_b200 import parallel
+    g = golden("k3_f11_s1.json")
+    b = g["b"]
+    F = parallel.gather_frobenius_nccl(g["F"], b, list(range(b)), world=1, rank=0, device=0)
+    assert [str(x) for x in F] == list(g["F"])

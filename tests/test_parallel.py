@@ -65,3 +65,29 @@ def test_gather_world2_gloo():
     for p in procs:
         p.join(timeout=30)
     assert res == {0: True, 1: True}
+
+
+def test_gather_host_cxx_matches_fixture():
+    """the C++ side of drzg_gather_F (limb encode + owner decode) assembles the
+    reference's K3 F from three ranks' column blocks"""
+    g = golden("k3_f11_s1.json")
+    b, F = g["b"], g["F"]
+    owners = [parallel.partition_columns(g["n"], g["d"], 3, r) for r in range(3)]
+    blocks = [[F[i * b + j] if j in o else "0" for i in range(b) for j in range(b)] for o in owners]
+    assert [str(x) for x in parallel.gather_frobenius_host(blocks, b, owners)] == list(F)
+    import pytest
+    with pytest.raises(Exception):
+        parallel.gather_frobenius_host(blocks[:2], b, owners[:2])  # a column without owner
+
+
+def test_partition_by_replayed_ledger():
+    """fourfold columns balanced by the reference's replayed per-column matvecs"""
+    import os
+    from conftest import GOLD
+    w = parallel.replayed_column_weights(os.path.join(GOLD, "ledger_replay_fourfold.json"))
+    assert len(w) == 22
+    for world in (2, 4, 8):
+        parts = [parallel.partition_columns(5, 3, world, r, weights=w) for r in range(world)]
+        assert sorted(j for p in parts for j in p) == list(range(22))
+        loads = [sum(w[j] for j in p) for p in parts]
+        assert max(loads) / (sum(w) / world) < 1.25
