@@ -215,7 +215,10 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   const char* fz = std::getenv("DRZG_FUSED");
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
   const char* ck = std::getenv("DRZG_CHUNK");
-  chunk_ = fused_ && dixon_chunk_ok(nLp_, T.dp.Ld) && !(ck && std::string(ck) == "0");
+  // whole-chunk launches are opt-in: over 58 K3 zeta functions they gave a
+  // 0.244 s median against 0.230 s step by step (their T_x runs inside the
+  // block's CTA, serialised with its Dixon solve)
+  chunk_ = fused_ && dixon_chunk_ok(nLp_, T.dp.Ld) && ck && std::string(ck) == "1";
   const char* fl = std::getenv("DRZG_FLOW");
   flow_ = use_tc_ && sparse_carry_ && !fused_ && nLp_ % 128 == 0 && !(fl && std::string(fl) == "0");
   const char* f2e = std::getenv("DRZG_FLOW2");
@@ -1127,25 +1130,29 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         // leave cores to the launcher and the seed preparers (an oversubscribed
         // launcher starves the device)
         const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_ > 6 ? host_threads_ - 4 : 2, nf / 4096 + 1));
-        std::vector<std::thread> pool;
         std::vector<std::exception_ptr> errs(nth);
-        for (int t = 0; t < nth; ++t)
-          pool.emplace_back([&, t] {
-            try {
-              for (size_t i = t * nf / nth; i < (t + 1) * nf / nth; ++i) {
-                Expo v;
-                i64 k;
-                pchunk_move(T.d, n_, (i64)p_, front[f0 + i].u, front[f0 + i].pole, T.S, &v, &k);
-                DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
-                DRZG_REQUIRE(legal(T.d, front[f0 + i].u, v, k, T.S), "reduce_chunk: illegal move");
-                vd[i] = (int)rank_of(v);
-                kk[i] = k;
-              }
-            } catch (...) {
-              errs[t] = std::current_exception();
+        auto moves = [&](int t) {
+          try {
+            for (size_t i = t * nf / nth; i < (t + 1) * nf / nth; ++i) {
+              Expo v;
+              i64 k;
+              pchunk_move(T.d, n_, (i64)p_, front[f0 + i].u, front[f0 + i].pole, T.S, &v, &k);
+              DRZG_REQUIRE(k >= 1, "p-chunk: no admissible move");
+              DRZG_REQUIRE(legal(T.d, front[f0 + i].u, v, k, T.S), "reduce_chunk: illegal move");
+              vd[i] = (int)rank_of(v);
+              kk[i] = k;
             }
-          });
-        for (auto& th : pool) th.join();
+          } catch (...) {
+            errs[t] = std::current_exception();
+          }
+        };
+        if (nth == 1) {
+          moves(0);  // small sweeps: no thread start-up on the policy's critical path
+        } else {
+          std::vector<std::thread> pool;
+          for (int t = 0; t < nth; ++t) pool.emplace_back(moves, t);
+          for (auto& th : pool) th.join();
+        }
         for (auto& e2 : errs)
           if (e2) std::rethrow_exception(e2);
       }

@@ -127,12 +127,22 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       size_t c1 = c0;
       double need = 0;
       const double w0 = now_s();
+      // group sizes from the dense bound on a column's terms (sum over j of
+      // |Homog_{dj}|, what frobenius_terms yields for a dense f^j): no wait
+      // for columns that will not be in this group
+      auto terms_bound = [&](size_t c) {
+        const int m = B.pole_of[cols[c]];
+        double t = 0;
+        for (int j = 0; j < plan.N_m[m]; ++j) t += (double)mono_count(X.nv(), X.d * j);
+        return t;
+      };
       while (c1 < cols.size()) {
-        double add = 0.6 * (double)wait_column(c1).nterms * slot_bytes;
+        double add = 0.6 * terms_bound(c1) * slot_bytes;
         if (c1 > c0 && need + add > budget) break;
         need += add;
         ++c1;
       }
+      for (size_t c = c0; c < c1; ++c) wait_column(c);
       seed_wait += now_s() - w0;
       std::vector<ColumnSeeds> grp;
       {
