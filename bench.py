@@ -424,7 +424,10 @@ def main():
     budget = FOURFOLD_COUNT_BUDGET if args.config == "fourfold" else 0
     # columns partitioned across ranks (longest-processing-time by pole order)
     from paper_2602_24155_b200 import parallel
-    all_cols = [parallel.partition_columns(n, d, world, r) for r in range(world)]
+    weights = None
+    if args.config == "fourfold":  # the reference's replayed per-column work
+        weights = parallel.replayed_column_weights(os.path.join(GOLD, "ledger_replay_fourfold.json"))
+    all_cols = [parallel.partition_columns(n, d, world, r, weights=weights) for r in range(world)]
     mine = all_cols[rank] if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -448,8 +451,8 @@ def main():
             return z["seconds"], z, z["frobenius"]
         t0 = time.time()
         fr = drzg.frobenius(p, n, d, coeffs, r_uniform=r_uniform, columns=mine, device=local, profile=profile)
-        # one NCCL all_gather of the column blocks (62-bit limbs; see parallel.py)
-        F = parallel.gather_frobenius(fr["F"], b, mine, world, all_cols, device=torch.device("cuda", local))
+        # one ncclAllGather of the column blocks issued by libdrzg.so (drzg_gather_F)
+        F = parallel.gather_frobenius_nccl(fr["F"], b, mine, world, rank, local)
         z = None
         if rank == 0:
             # run_zeta's battery on the gathered F: Q recovery, sign tie-break,

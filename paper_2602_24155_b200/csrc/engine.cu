@@ -400,7 +400,7 @@ void ReductionEngine::grow_pool(int need) {
   size_t fr = 0, tot = 0;
   if (!pool_) {
     // reserve address space for the whole device once
-    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    mem_info(&fr, &tot, "engine.cu:1");
     vmm_reserved_ = (tot + gran - 1) / gran * gran;
     CUdeviceptr base = 0;
     DRZG_CU(V.reserve(&base, vmm_reserved_, gran, 0, 0));
@@ -410,9 +410,16 @@ void ReductionEngine::grow_pool(int need) {
   }
   int ncap = std::max(need, cap_ + std::max(1024, cap_ / 2));
   size_t want = (size_t)ncap * slot_stride_;
+  if (want <= vmm_mapped_) {
+    // the (cached) mapping already covers it: no sync, no driver query
+    int ncap2 = (int)std::min<size_t>(vmm_mapped_ / (size_t)slot_stride_, (size_t)INT32_MAX);
+    for (int s = ncap2 - 1; s >= cap_; --s) free_.push_back(s);
+    cap_ = ncap2;
+    return;
+  }
   DRZG_CUDA(cudaStreamSynchronize(st_));
   if (want > vmm_mapped_) trim_mempool(dev);  // unused stream-ordered reserve back to the driver
-  DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  mem_info(&fr, &tot, "engine.cu:2");
   size_t margin = (size_t)2 << 30;
   std::unique_lock<std::mutex> tmp_lock(tmp_mu_, std::defer_lock);
   if (want > vmm_mapped_ + (fr > margin ? fr - margin : 0)) tmp_lock.lock();  // no sweep is launching now
@@ -427,7 +434,7 @@ void ReductionEngine::grow_pool(int need) {
     bcap_ = 0;
     DRZG_CUDA(cudaStreamSynchronize(st_));
     trim_mempool(dev);
-    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    mem_info(&fr, &tot, "engine.cu:3");
   }
   size_t room = vmm_mapped_ + (fr > margin ? fr - margin : 0);
   if (want > room) want = std::max<size_t>(room, (size_t)need * (size_t)slot_stride_);  // settle for what fits
@@ -493,13 +500,19 @@ void ReductionEngine::ensure_batch(int B) {
   const int Ld = T_->dp.Ld;
   size_t per = (size_t)(2 * Ld + 1) * nLp_ + sizeof(int16_t) * nLp_ + (size_t)Ld * sidep_;
   size_t fr = 0, tot = 0;
-  DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  const size_t tot_mem = device_total_memory();
+  if (tot_mem && (double)round_up(B, 64) * (double)per < 0.02 * (double)tot_mem) {
+    // small batches: temporaries for exactly this batch, no driver query
+    fr = tot = tot_mem;
+  } else {
+    mem_info(&fr, &tot, "engine.cu:4");
+  }
   if (fr * 0.8 < tot * 0.12) {
     int dev = 0;
     DRZG_CUDA(cudaGetDevice(&dev));
     DRZG_CUDA(cudaStreamSynchronize(st_));
     trim_mempool(dev);
-    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    mem_info(&fr, &tot, "engine.cu:5");
   }
   // temporaries get at most half of what is free, in multiples of 64 states
   // temporaries: at most 80% of what is free and 12% of the device, so the
@@ -979,10 +992,16 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     // live states never exceed the seeds materialised so far: size the pool
     // for all of them when that fits 60% of free HBM (the rest feeds the
     // batch temporaries), else take the 60% and grow only if needed
-    size_t fr = 0, tot = 0;
-    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
-    size_t budget = (size_t)(fr * 0.40) / (size_t)slot_stride_;
-    grow_pool((int)std::max<size_t>(1024, std::min<size_t>(total_seeds / 3 + 1, budget)));
+    const size_t want = std::max<size_t>(1024, total_seeds / 3 + 1);
+    const size_t tot_mem = device_total_memory();
+    if (tot_mem && (double)want * (double)slot_stride_ < 0.05 * (double)tot_mem) {
+      grow_pool((int)want);  // small: no need to ask the driver what is free
+    } else {
+      size_t fr = 0, tot = 0;
+      mem_info(&fr, &tot, "engine.cu:6");
+      size_t budget = (size_t)(fr * 0.40) / (size_t)slot_stride_;
+      grow_pool((int)std::max<size_t>(1024, std::min<size_t>(want, budget)));
+    }
   }
 
   // DRZG_TIMELINE: device time of every sweep and the device idle time
@@ -1736,7 +1755,7 @@ void ReductionEngine::run_rounds(std::vector<ColumnSeeds>& cols, std::vector<std
   // waves that fit the pool; var-by-var combines across all of a column's
   // states, so a column runs whole
   size_t fr = 0, tot = 0;
-  DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+  mem_info(&fr, &tot, "engine.cu:7");
   const size_t wave = std::max<size_t>(1024, (size_t)(fr * 0.4) / (size_t)slot_stride_);
   for (int c = 0; c < ncol; ++c) {
     std::vector<Live> sts;

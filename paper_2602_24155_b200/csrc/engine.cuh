@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -27,6 +30,29 @@ namespace drzg {
       throw ::drzg::contract_error(std::string("CUDA: ") + cudaGetErrorString(err_), __FILE__, \
                                    __LINE__);                                                 \
   } while (0)
+
+// cudaMemGetInfo, timed: DRZG_VERBOSE reports calls slower than 5 ms (tail hunting)
+inline void mem_info(size_t* fr, size_t* tot, const char* where) {
+  const auto t0 = std::chrono::steady_clock::now();
+  DRZG_CUDA(cudaMemGetInfo(fr, tot));
+  const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  static const bool verbose = std::getenv("DRZG_VERBOSE") != nullptr;
+  if (verbose && s > 0.005) std::fprintf(stderr, "[drzg] slow cudaMemGetInfo (%s): %.3f s\n", where, s);
+}
+
+// total memory of the current device (cached): small requests skip
+// cudaMemGetInfo, which can take tens of milliseconds while the device is busy
+inline size_t device_total_memory() {
+  static size_t tot[64] = {0};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d < 0 || d >= 64) return 0;
+  if (!tot[d]) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) == cudaSuccess) tot[d] = prop.totalGlobalMem;
+  }
+  return tot[d];
+}
 
 // host<->device traffic and kernel launches of the current call (reported
 // with every result: the e2e byte counts and the launch count of the bench)

@@ -328,15 +328,23 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
     // every step's output: the step-1 epilogue zeroed its next-step operand
     // row, and no one writes that row of Bg again during the chunk
     if (a.y >= 2 && nt == 0 && all_cont) continue;
-    // next step's operand row of side row g (per state's v), or W at chunk end
-    int rn[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? __ldg(ginv + (size_t)vds[j] * side + g) : -1;
-    // the write target of whole-lane words, fixed per row
+    // the write target of whole-lane words, fixed per row: W at chunk end, or
+    // the next step's operand row of g under the lane's (shared) v
     const bool lane_word = none_cont || (all_cont && same_v);
-    int8_t* dst = none_cont ? c.W + (size_t)g * c.P + s4
-                            : (rn[0] >= 0 ? c.Bg + (size_t)rn[0] * c.P + s4 : nullptr);
+    int8_t* dst = nullptr;
+    if (none_cont) {
+      dst = c.W + (size_t)g * c.P + s4;
+    } else if (lane_word) {
+      const int r0 = __ldg(ginv + (size_t)vds[0] * side + g);
+      dst = r0 >= 0 ? c.Bg + (size_t)r0 * c.P + s4 : nullptr;
+    }
     const size_t dstride = none_cont ? c.wplane : c.plane;
+    // mixed lanes: per-state rows (rare: states are sorted by (k, v))
+    int rn[4] = {-1, -1, -1, -1};
+    if (!lane_word) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) rn[j] = conts[j] ? __ldg(ginv + (size_t)vds[j] * side + g) : -1;
+    }
     auto put = [&](int t, uint32_t word) {
       if (lane_word) {
         if (dst) *reinterpret_cast<uint32_t*>(dst + (size_t)t * dstride) = word;

@@ -45,6 +45,10 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   HostMod hm = HostMod::make(p, plan.M);
   double t1 = now_s();
   out.t.tables = t1 - t0;
+  const bool verbose = std::getenv("DRZG_VERBOSE") != nullptr;
+  auto mark = [&](const char* what) {
+    if (verbose) std::fprintf(stderr, "[drzg] frobenius wall %s %.3f\n", what, now_s() - t0);
+  };
 
   std::vector<int> cols;
   for (int j = 0; j < (int)B.b; ++j) {
@@ -107,6 +111,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     throw;
   }
   double t2 = now_s();
+  mark("prepared");
 
   // columns run through the device engine in groups whose states fit HBM:
   // live states stay below ~60% of a group's seeds (SURVEY 8a peaks), and a
@@ -117,9 +122,24 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     const double te0 = now_s();
     ReductionEngine eng(T, n, p, st);
     if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] engine setup %.3f s\n", now_s() - te0);
+    mark("engine");
     eng.clock.on = opt.profile;
     size_t fr = 0, tot = 0;
-    DRZG_CUDA(cudaMemGetInfo(&fr, &tot));
+    {
+      // the grouping budget: free memory matters only when the columns' seeds
+      // could approach it (the driver query is slow on a busy device)
+      double all = 0;
+      for (size_t c = 0; c < cols.size(); ++c) {
+        const int m = B.pole_of[cols[c]];
+        for (int j = 0; j < plan.N_m[m]; ++j) all += (double)mono_count(X.nv(), X.d * j);
+      }
+      const double slot = (double)T.dp.Ld * ((T.side + 15) / 16 * 16);
+      const size_t tm = device_total_memory();
+      if (tm && all * slot < 0.05 * (double)tm)
+        fr = tot = tm;
+      else
+        mem_info(&fr, &tot, "pipeline.cu:1");
+    }
     const double slot_bytes = (double)T.dp.Ld * ((T.side + 15) / 16 * 16);
     const double budget = 0.5 * (double)fr;
     size_t c0 = 0;
@@ -144,6 +164,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       }
       for (size_t c = c0; c < c1; ++c) wait_column(c);
       seed_wait += now_s() - w0;
+      mark("group seeds");
       std::vector<ColumnSeeds> grp;
       {
         std::lock_guard<std::mutex> lk(smu);
@@ -174,8 +195,10 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     join_pool();
     throw;
   }
+  mark("engine closed");
   join_pool();
   double t3 = now_s();
+  mark("expansion joined");
   if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] engine teardown %.3f s\n", t3 - td0);
   // seeds: the host time the device waited for expansions (the rest overlapped)
   out.t.seeds = (t2 - t1) + seed_wait;
