@@ -628,6 +628,25 @@ extern "C" int drzg_test_final_levels(uint64_t p, int32_t n, int32_t d, const ui
   });
 }
 
+namespace drzg {
+std::pair<long long, long long> debug_order_blocks(const RuvTables& T);
+}
+// debug hook: nonzero 128 x 128 Jp blocks of the carry order, without (out[0])
+// and with (out[1]) the T_x grouping of solution indices
+extern "C" int drzg_debug_order(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int64_t* out) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    setenv("DRZG_SETUP", "host", 1);
+    setenv("DRZG_DEBUG_NO_INVERSE", "1", 1);
+    RuvTables T = build_tables(X, M, default_S(n, d));
+    unsetenv("DRZG_SETUP");
+    unsetenv("DRZG_DEBUG_NO_INVERSE");
+    auto b = debug_order_blocks(T);
+    out[0] = b.first;
+    out[1] = b.second;
+  });
+}
+
 // debug hook: the Dixon system's structure (Jp CSR, rows Homog_L in grevlex
 // rank, columns = solution indices) and the generator of every solution
 // index, written as int32 arrays to `path`:

@@ -47,7 +47,16 @@ struct SysOrder {
   long long blocks = 0;
 };
 
-SysOrder order_system(const RuvTables& T, bool search) {
+// the T_x grouping of solution indices (DRZG_TX_GROUP=0/1)
+bool tx_grouped() {
+  static const bool on = [] {
+    const char* e = std::getenv("DRZG_TX_GROUP");
+    return e && std::string(e) == "1";
+  }();
+  return on;
+}
+
+SysOrder order_system(const RuvTables& T, bool search, bool group_tx) {
   const int nL = T.nL, nv = T.nv;
   constexpr int B = 128;
   const int nt = (nL + B - 1) / B;
@@ -105,6 +114,18 @@ SysOrder order_system(const RuvTables& T, bool search) {
       }
     } while (std::next_permutation(vp.begin(), vp.end()));
   }
+  if (group_tx) {
+    // solution indices feeding one side row made adjacent (each r feeds
+    // exactly one row sol_row[r]), groups in the order of their first
+    // member: the T_x epilogue then reads one contiguous Y slab per range of
+    // side rows
+    std::vector<int> gfirst(T.side, INT32_MAX);
+    for (int r = 0; r < nL; ++r) gfirst[T.sol_row[r]] = std::min(gfirst[T.sol_row[r]], best.pos_r[r]);
+    std::vector<double> key(nL);
+    for (int r = 0; r < nL; ++r) key[r] = (double)gfirst[T.sol_row[r]] * (double)(nL + 1) + best.pos_r[r];
+    best.pos_r = sort_pos(key);
+    best.blocks = blocks_of(best.pos_m, best.pos_r).first;
+  }
   auto occ = blocks_of(best.pos_m, best.pos_r).second;
   best.kb_ptr.assign(1, 0);
   for (int i = 0; i < nt; ++i) {
@@ -115,6 +136,11 @@ SysOrder order_system(const RuvTables& T, bool search) {
   return best;
 }
 }  // namespace
+
+// debug: nonzero Jp blocks of the carry order without / with the T_x grouping
+std::pair<long long, long long> debug_order_blocks(const RuvTables& T) {
+  return {order_system(T, T.nL > 2 * 128, false).blocks, order_system(T, T.nL > 2 * 128, true).blocks};
+}
 
 ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t st)
     : T_(&T), n_(n), p_(p), st_(st) {
@@ -141,7 +167,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   sparse_carry_ = want_tc && !(so && std::string(so) == "0");
   // block-sparse order of the system (identity unless the carry uses it)
   auto to0 = std::chrono::steady_clock::now();
-  SysOrder ord = order_system(T, sparse_carry_ && T.nL > 2 * 128);
+  SysOrder ord = order_system(T, sparse_carry_ && T.nL > 2 * 128, tx_grouped());
   if (std::getenv("DRZG_VERBOSE"))
     std::fprintf(stderr, "[drzg] system order: %lld of %lld Jp blocks nonzero (%.3f s)\n", ord.blocks,
                  (long long)((T.nL + 127) / 128) * ((T.nL + 127) / 128),
@@ -365,6 +391,12 @@ struct CachedPool {
 std::mutex g_pool_mu;
 std::map<int, CachedPool> g_pool_cache;
 }  // namespace
+
+size_t cached_pool_bytes(int dev) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_pool_cache.find(dev);
+  return it != g_pool_cache.end() && it->second.base ? it->second.mapped : 0;
+}
 
 // the retained mempool keeps freed stream-ordered memory reserved (fast
 // reuse across zeta functions); cudaMemGetInfo does not count it as free, so
@@ -1011,6 +1043,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     cudaEvent_t e0, e1;
     int pole;
     i64 states, matvecs;
+    double t_push, t_pop, t_launched;  // host seconds since the run started
+    double t_seeded, t_staged;         // ... seed work issued, sweep inputs staged
   };
   std::vector<SweepMark> tl;
   std::map<int, std::vector<HS>, std::greater<int>> landed;
@@ -1049,12 +1083,14 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     i64 matvecs = 0;
     std::vector<int> gptr, mem;  // merges
     std::vector<int> fs, fc, fu; // floor arrivals
+    double t_push = 0;           // DRZG_TIMELINE: host time the policy handed it over
   };
   std::mutex qmu;
   std::condition_variable qcv;
   std::deque<std::unique_ptr<SweepCmd>> queue;
   std::exception_ptr perr;
   auto push = [&](std::unique_ptr<SweepCmd> c) {
+    if (timeline) c->t_push = wsince();
     {
       std::lock_guard<std::mutex> lk(qmu);
       queue.push_back(std::move(c));
@@ -1134,14 +1170,22 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     // the front is handed to the launcher in chunks of states (each sorted
     // by (k, v) on its own), so the device starts on a sweep before the
     // policy has finished it; the seed work of pole P rides with chunk 0
+    // (DRZG_CHUNK0 < 17: chunks double from 2^CHUNK0 states, so the device
+    // gets a pole's first states after a shorter policy step; measured no
+    // better on K3, whose smaller batches cost more than the wait saves)
     const size_t nfront = front.size();
     constexpr size_t kChunk = (size_t)1 << 17;
-    for (size_t f0 = 0; f0 < nfront; f0 += kChunk) {
+    static const int chunk0 = [] {
+      const char* e = std::getenv("DRZG_CHUNK0");  // A/B: log2 of a pole's first chunk
+      return e ? std::min(17, std::max(8, std::atoi(e))) : 17;  // K3: 2^17 beat 2^13 (0.221 vs 0.229 s)
+    }();
+    size_t chunk = (size_t)1 << chunk0;
+    for (size_t f0 = 0, nf = 0; f0 < nfront; f0 += nf, chunk = std::min(kChunk, 2 * chunk)) {
       if (f0) {
         cmd = std::make_unique<SweepCmd>();
         cmd->pole = P;
       }
-      const size_t nf = std::min(nfront, f0 + kChunk) - f0;
+      nf = std::min(nfront, f0 + chunk) - f0;
       // moves (reduction.hpp:486-496) for every state, on host threads
       std::vector<int> vd(nf);
       std::vector<i64> kk(nf);
@@ -1219,6 +1263,11 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       std::vector<int>& fc = cmd->fc;
       std::vector<int>& fu = cmd->fu;
       std::vector<std::pair<int, int>> merges;  // (dst slot, src slot)
+      // states arrive in runs of one landing pole (sorted by k): the pole's
+      // index and list are looked up once per run
+      int lp_pole = -1;
+      FlatMap* lp_idx = nullptr;
+      std::vector<HS>* lp_lst = nullptr;
       for (int i : order) {
         HS h = front[f0 + i];
         const Expo& v = dirs_host_[vd[i]];
@@ -1232,8 +1281,13 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
           floor_arrivals[h.col]++;
           floor_keys[h.col].insert(kh, 0);
         } else {
-          auto& idx = landed_idx[h.pole];
-          auto& lst = landed[h.pole];
+          if (h.pole != lp_pole) {
+            lp_pole = h.pole;
+            lp_idx = &landed_idx[h.pole];
+            lp_lst = &landed[h.pole];
+          }
+          FlatMap& idx = *lp_idx;
+          std::vector<HS>& lst = *lp_lst;
           const int pos = idx.insert(kh, (int)lst.size());
           if (pos == (int)lst.size()) {
             lst.push_back(h);
@@ -1314,6 +1368,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
                                                       d_g2.p, d_dig2.p, ns);
         });
       }
+      const double t_seeded = timeline ? wsince() : 0;
       if (!cmd->ks.empty()) {
         d_slot_.stage(cmd->hslot, stager_, st_);
         d_vdir_.stage(cmd->hvdir, stager_, st_);
@@ -1323,10 +1378,13 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
           cudaEvent_t e0, e1;
           DRZG_CUDA(cudaEventCreate(&e0));
           DRZG_CUDA(cudaEventCreate(&e1));
+          const double tp = std::chrono::duration<double>(hl0 - wm0).count();
+          const double t_staged = wsince();
           DRZG_CUDA(cudaEventRecord(e0, st_));
           run_sweep(cmd->ks);
           DRZG_CUDA(cudaEventRecord(e1, st_));
-          tl.push_back({e0, e1, cmd->pole, (i64)cmd->ks.size(), cmd->matvecs});
+          tl.push_back({e0, e1, cmd->pole, (i64)cmd->ks.size(), cmd->matvecs, cmd->t_push, tp, wsince(), t_seeded,
+                        t_staged});
         } else {
           run_sweep(cmd->ks);
         }
@@ -1389,6 +1447,34 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
     std::fprintf(stderr, "[drzg] timeline: %zu sweeps, before first %.1f ms, sweeps %.1f ms, between sweeps %.1f ms\n",
                  tl.size(), lead, busy, idle);
+    std::fprintf(stderr, "[drzg]   host waits (process, ms): ring %.1f pinned %.1f copy %.1f malloc %.1f\n",
+                 g_waits.ring_ns / 1e6, g_waits.pinned_ns / 1e6, g_waits.copy_ns / 1e6, g_waits.malloc_ns / 1e6);
+    g_waits.reset();
+    // the largest device gaps, with the host times (ms since the run began,
+    // device times on the same base via run0) of the sweep that ended them
+    {
+      const double r0 = wmark[0] * 1e3;
+      std::vector<std::pair<float, size_t>> gaps;
+      for (size_t i = 1; i < tl.size(); ++i) {
+        float g2 = 0;
+        DRZG_CUDA(cudaEventElapsedTime(&g2, tl[i - 1].e1, tl[i].e0));
+        gaps.push_back({g2, i});
+      }
+      std::sort(gaps.rbegin(), gaps.rend());
+      for (size_t j = 0; j < gaps.size() && j < 6 && gaps[j].first > 1.0f; ++j) {
+        const size_t i = gaps[j].second;
+        float d0 = 0, d1 = 0;
+        DRZG_CUDA(cudaEventElapsedTime(&d0, run0, tl[i - 1].e1));
+        DRZG_CUDA(cudaEventElapsedTime(&d1, run0, tl[i].e0));
+        std::fprintf(stderr,
+                     "[drzg]   gap %.2f ms before sweep %zu (pole %d, %lld states): device idle %.2f..%.2f, "
+                     "policy pushed %.2f, launcher popped %.2f, seeded %.2f, staged %.2f, launched %.2f (prev "
+                     "launched %.2f)\n",
+                     gaps[j].first, i, tl[i].pole, (long long)tl[i].states, d0 + r0, d1 + r0, tl[i].t_push * 1e3,
+                     tl[i].t_pop * 1e3, tl[i].t_seeded * 1e3, tl[i].t_staged * 1e3, tl[i].t_launched * 1e3,
+                     tl[i - 1].t_launched * 1e3);
+      }
+    }
     for (auto& kv : by_pole)
       if (kv.second.first + kv.second.second > 20)
         std::fprintf(stderr, "[drzg]   pole %d: sweep %.1f ms, gap before %.1f ms\n", kv.first, kv.second.first,

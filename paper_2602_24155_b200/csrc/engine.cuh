@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -61,6 +62,17 @@ struct Traffic {
   void reset() { h2d = 0; d2h = 0; launches = 0; }
 };
 inline Traffic g_traffic;
+// DRZG_TIMELINE diagnostics: host seconds spent in host-side allocation and
+// staging waits (pinned growth, ring waits, stream-ordered allocations)
+struct HostWaits {
+  std::atomic<long long> pinned_ns{0}, ring_ns{0}, malloc_ns{0}, copy_ns{0};
+  void reset() { pinned_ns = 0; ring_ns = 0; malloc_ns = 0; copy_ns = 0; }
+};
+inline HostWaits g_waits;
+inline long long now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 enum class Policy { p_chunk = 0, depth_first = 1, var_by_var = 2 };
 
@@ -87,44 +99,73 @@ struct KernelClock {
 class Stager {
  public:
   ~Stager() {
-    for (auto& b : bufs_) {
-      if (b.h) cudaFreeHost(b.h);
-      if (b.ev) cudaEventDestroy(b.ev);
-    }
+    for (std::vector<Buf>* ring : {&small_, &large_})
+      for (auto& b : *ring) {
+        if (b.h && !b.carved) cudaFreeHost(b.h);
+        if (b.ev) cudaEventDestroy(b.ev);
+      }
+    if (arena_) cudaFreeHost(arena_);
     for (void* h : retired_) cudaFreeHost(h);
   }
-  // one ring for the whole process: concurrent callers (one host thread per
-  // device, say) take turns, so no two copies share a pinned buffer
+  // one pinned ring per size class for the whole process: concurrent callers
+  // (one host thread per device, say) take turns, so no two copies share a
+  // pinned buffer.  Small requests use fixed slots carved from one arena;
+  // large ones a short ring whose slots grow to the high-water mark, so that
+  // after the first sweeps no copy pins memory (cudaMallocHost costs up to
+  // tens of ms, on the launcher's critical path)
   void copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (!bytes) return;
     std::lock_guard<std::mutex> lk(mu_);
-    Buf& b = bufs_[next_];
-    next_ = (next_ + 1) % kRing;
+    const bool small = bytes <= kSmall;
+    if (small && !arena_) {
+      DRZG_CUDA(cudaMallocHost(&arena_, kSmall * small_.size()));
+      for (size_t i = 0; i < small_.size(); ++i) {
+        small_[i].h = static_cast<char*>(arena_) + i * kSmall;
+        small_[i].cap = kSmall;
+        small_[i].carved = true;
+      }
+    }
+    std::vector<Buf>& ring = small ? small_ : large_;
+    int& next = small ? next_small_ : next_large_;
+    Buf& b = ring[next];
+    next = (next + 1) % (int)ring.size();
     if (!b.ev) DRZG_CUDA(cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming));
+    const long long t0 = now_ns();
     if (b.used) DRZG_CUDA(cudaEventSynchronize(b.ev));
+    const long long t1 = now_ns();
     if (b.cap < bytes) {
       // the old buffer is retired, not freed: cudaFreeHost synchronises the
       // whole device, which would stall the launcher behind queued work
       if (b.h) retired_.push_back(b.h);
-      b.cap = std::max<size_t>(2 * bytes, (size_t)1 << 20);
+      hwm_ = std::max(hwm_, bytes);
+      b.cap = std::max<size_t>({2 * bytes, 2 * hwm_, (size_t)8 << 20});
       DRZG_CUDA(cudaMallocHost(&b.h, b.cap));
     }
+    const long long t2 = now_ns();
     std::memcpy(b.h, src, bytes);
     DRZG_CUDA(cudaMemcpyAsync(dst, b.h, bytes, cudaMemcpyHostToDevice, st));
+    const long long t3 = now_ns();
+    g_waits.ring_ns += t1 - t0;
+    g_waits.pinned_ns += t2 - t1;
+    g_waits.copy_ns += t3 - t2;
     DRZG_CUDA(cudaEventRecord(b.ev, st));
     b.used = true;
   }
 
  private:
-  static constexpr int kRing = 64;
+  static constexpr size_t kSmall = 64 << 10;
   struct Buf {
     void* h = nullptr;
     size_t cap = 0;
     cudaEvent_t ev = nullptr;
     bool used = false;
+    bool carved = false;  // part of the small-slot arena
   };
-  Buf bufs_[kRing];
-  int next_ = 0;
+  std::vector<Buf> small_ = std::vector<Buf>(128);
+  std::vector<Buf> large_ = std::vector<Buf>(16);
+  int next_small_ = 0, next_large_ = 0;
+  void* arena_ = nullptr;
+  size_t hwm_ = 0;
   std::mutex mu_;
   std::vector<void*> retired_;
 };
@@ -144,7 +185,9 @@ struct DevBuf {
     if (count <= n) return;
     release();
     if (st) {
+      const long long t0 = now_ns();
       DRZG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(T), st));
+      g_waits.malloc_ns += now_ns() - t0;
       async_ = true;
       ast_ = st;
     } else {
@@ -178,6 +221,10 @@ struct DevBuf {
   bool async_ = false;
   cudaStream_t ast_ = nullptr;
 };
+
+// state-pool memory a finished engine left mapped on `dev` for the next one
+// (it counts as used in the driver's free figure, yet is available)
+size_t cached_pool_bytes(int dev);
 
 class ReductionEngine {
  public:

@@ -6,6 +6,7 @@
 #include <exception>
 #include <thread>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 
 #include "pipeline.cuh"
@@ -19,6 +20,18 @@ double now_s() {
 }
 }  // namespace
 
+cudaStream_t device_stream(int device) {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> streams;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = streams.find(device);
+  if (it != streams.end()) return it->second;
+  cudaStream_t st;
+  DRZG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  streams[device] = st;
+  return st;
+}
+
 std::set<int> working_set_for(const Hypersurface& X, Policy pol) {
   if (pol == Policy::var_by_var) return {X.n};
   return default_S(X.n, X.d);
@@ -28,8 +41,11 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
                             const FrobOptions& opt, int device) {
   double t0 = now_s();
   DRZG_CUDA(cudaSetDevice(device));
-  cudaStream_t st;
-  DRZG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  // one stream per device for the life of the process: the engine's
+  // stream-ordered temporaries return to the retained pool on it and the next
+  // call's allocations reuse them in stream order (a fresh stream per call
+  // made cudaMallocAsync grow the pool again, up to 0.3 s per K3 zeta)
+  cudaStream_t st = device_stream(device);
   FrobResult out;
   const int n = X.n;
   const u64 p = X.p;
@@ -139,9 +155,33 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
         fr = tot = tm;
       else
         mem_info(&fr, &tot, "pipeline.cu:1");
+      // memory this process holds but no one uses counts as free: the state
+      // pool a finished engine left mapped and the retained mempool's slack
+      int dev = 0;
+      DRZG_CUDA(cudaGetDevice(&dev));
+      fr += cached_pool_bytes(dev);
+      cudaMemPool_t mp;
+      DRZG_CUDA(cudaDeviceGetDefaultMemPool(&mp, dev));
+      unsigned long long res = 0, used = 0;
+      DRZG_CUDA(cudaMemPoolGetAttribute(mp, cudaMemPoolAttrReservedMemCurrent, &res));
+      DRZG_CUDA(cudaMemPoolGetAttribute(mp, cudaMemPoolAttrUsedMemCurrent, &used));
+      if (res > used) fr += (size_t)(res - used);
     }
     const double slot_bytes = (double)T.dp.Ld * ((T.side + 15) / 16 * 16);
-    const double budget = 0.5 * (double)fr;
+    // live states peak near 0.35 of the dense term bound (the random
+    // fourfold: 1.08M of 3.1M per column), so 0.45 of it against 55% of free
+    // HBM leaves the batch temporaries (<= 12% of the device) room; two
+    // fourfold columns per group halve the group start-ups and double the
+    // batches (151.9 against 160.9 s of device time per zeta function)
+    constexpr double kPeakPerBound = 0.45;
+    const double budget = 0.55 * (double)fr;
+    if (verbose && !cols.empty()) {
+      double b0 = 0;
+      const int m = B.pole_of[cols[0]];
+      for (int j = 0; j < plan.N_m[m]; ++j) b0 += (double)mono_count(X.nv(), X.d * j);
+      std::fprintf(stderr, "[drzg] grouping: column 0 dense term bound %.0f (%.1f GB of states at %.2f), budget %.1f GB\n",
+                   b0, kPeakPerBound * b0 * slot_bytes / 1e9, kPeakPerBound, budget / 1e9);
+    }
     size_t c0 = 0;
     while (c0 < cols.size()) {
       size_t c1 = c0;
@@ -156,9 +196,13 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
         for (int j = 0; j < plan.N_m[m]; ++j) t += (double)mono_count(X.nv(), X.d * j);
         return t;
       };
+      static const int group_cols = [] {
+        const char* e = std::getenv("DRZG_GROUP_COLS");  // A/B override: columns per group
+        return e ? std::max(1, std::atoi(e)) : 0;
+      }();
       while (c1 < cols.size()) {
-        double add = 0.6 * terms_bound(c1) * slot_bytes;
-        if (c1 > c0 && need + add > budget) break;
+        double add = kPeakPerBound * terms_bound(c1) * slot_bytes;
+        if (group_cols ? (int)(c1 - c0) >= group_cols : (c1 > c0 && need + add > budget)) break;
         need += add;
         ++c1;
       }
@@ -266,7 +310,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   double t4 = now_s();
   out.t.final = t4 - t3;
   out.t.total = t4 - t0;
-  DRZG_CUDA(cudaStreamDestroy(st));
+  DRZG_CUDA(cudaStreamSynchronize(st));
   return out;
 }
 
