@@ -165,6 +165,20 @@ def zeta(p, n, d, coeffs, policy="p-chunk", r_uniform=0, nm=0, verify_counts=Tru
                                  int(verify_counts), ctypes.c_int64(count_budget), device, int(profile)))
 
 
+def zeta_batch(p, n, d, coeffs_list, workers=4, device=0, **kw):
+    """zeta functions of many hypersurfaces over one field (BASELINE configs[3]:
+    64 cubic threefolds), `workers` at a time on one device: each call runs on
+    its own host thread and stream (ctypes releases the GIL), so one
+    hypersurface's host phases and small kernels overlap another's device
+    work; the dataflow kernels take turns (kernels/tc_gemm.cu gated launch).
+    Returns the results in input order."""
+    from concurrent.futures import ThreadPoolExecutor
+    if workers <= 1 or len(coeffs_list) <= 1:
+        return [zeta(p, n, d, co, device=device, **kw) for co in coeffs_list]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(lambda co: zeta(p, n, d, co, device=device, **kw), coeffs_list))
+
+
 def zeta_from_F(p, n, d, coeffs, F, b, r_uniform=0, nm=0, escalations=0, verify_counts=True, count_budget=0):
     """run_zeta's battery (zeta.hpp:456-535) on a given F, e.g. one gathered
     from several GPUs: {"status": "ok", "Q": ...} or {"status": "escalate"}"""

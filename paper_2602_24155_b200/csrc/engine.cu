@@ -232,12 +232,25 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
   }
   sparse_carry_ = sparse_carry_ && use_tc_;
   DRZG_REQUIRE((size_t)dev::kGatherStates * sidep_ <= 200 * 1024, "engine: side too large for the gather staging");
-  DRZG_CUDA(cudaFuncSetAttribute(dev::gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)std::min<size_t>((size_t)dev::kGatherStates * sidep_, 200 * 1024)));
-  // the flush transpose stages Ld x 64 rows x 32 states (50 KB at the quintic
-  // surface's 25 digit planes: above the 48 KB default)
-  DRZG_CUDA(cudaFuncSetAttribute(dev::flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 T.dp.Ld * dev::kFlushRows * dev::kFlushStates));
+  // the shared-memory opt-ins are per (kernel, device) and process-wide:
+  // set once per device at the largest size any engine launches (an engine
+  // of another shape on a concurrent thread must not lower it under a launch)
+  // -- the gather stages 32 states x sidep; the flush transpose Ld x 64 rows
+  // x 32 states (50 KB at the quintic surface's 25 digit planes)
+  {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    int dev = 0;
+    DRZG_CUDA(cudaGetDevice(&dev));
+    DRZG_REQUIRE(dev >= 0 && dev < 64, "engine: device index out of range");
+    std::lock_guard<std::mutex> lk(mu);
+    if (!done[dev]) {
+      DRZG_CUDA(cudaFuncSetAttribute(dev::gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      DRZG_CUDA(cudaFuncSetAttribute(dev::flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     dev::kLdMax * dev::kFlushRows * dev::kFlushStates));
+      done[dev] = true;
+    }
+  }
   const char* fz = std::getenv("DRZG_FUSED");
   fused_ = use_tc_ && dixon_fused_ok(nLp_) && !(fz && std::string(fz) == "0");
   const char* ck = std::getenv("DRZG_CHUNK");
@@ -389,13 +402,18 @@ struct CachedPool {
   std::vector<std::pair<size_t, std::pair<size_t, unsigned long long>>> chunks;  // off, (bytes, handle)
 };
 std::mutex g_pool_mu;
-std::map<int, CachedPool> g_pool_cache;
+// per device: the pools finished engines left (one per engine that was alive
+// at once: concurrent calls each keep theirs), at most half the device mapped
+std::map<int, std::vector<CachedPool>> g_pool_cache;
 }  // namespace
 
 size_t cached_pool_bytes(int dev) {
   std::lock_guard<std::mutex> lk(g_pool_mu);
+  size_t b = 0;
   auto it = g_pool_cache.find(dev);
-  return it != g_pool_cache.end() && it->second.base ? it->second.mapped : 0;
+  if (it != g_pool_cache.end())
+    for (const auto& c : it->second) b += c.mapped;
+  return b;
 }
 
 // the retained mempool keeps freed stream-ordered memory reserved (fast
@@ -414,12 +432,16 @@ void ReductionEngine::grow_pool(int need) {
   if (!pool_) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     auto it = g_pool_cache.find(dev);
-    if (it != g_pool_cache.end() && it->second.base) {
-      pool_ = it->second.base;
-      vmm_reserved_ = it->second.reserved;
-      vmm_mapped_ = it->second.mapped;
-      for (auto& c : it->second.chunks) vmm_chunks_.push_back({c.first, c.second.first, c.second.second});
-      g_pool_cache.erase(it);
+    if (it != g_pool_cache.end() && !it->second.empty()) {
+      // the largest cached pool
+      auto& v = it->second;
+      auto best = std::max_element(v.begin(), v.end(),
+                                   [](const CachedPool& a, const CachedPool& b) { return a.mapped < b.mapped; });
+      pool_ = best->base;
+      vmm_reserved_ = best->reserved;
+      vmm_mapped_ = best->mapped;
+      for (auto& c : best->chunks) vmm_chunks_.push_back({c.first, c.second.first, c.second.second});
+      v.erase(best);
       pool_dev_ = dev;
     }
   }
@@ -432,7 +454,8 @@ void ReductionEngine::grow_pool(int need) {
   size_t fr = 0, tot = 0;
   if (!pool_) {
     // reserve address space for the whole device once
-    mem_info(&fr, &tot, "engine.cu:1");
+    tot = device_total_memory();
+    if (!tot) mem_info(&fr, &tot, "engine.cu:1");
     vmm_reserved_ = (tot + gran - 1) / gran * gran;
     CUdeviceptr base = 0;
     DRZG_CU(V.reserve(&base, vmm_reserved_, gran, 0, 0));
@@ -452,6 +475,23 @@ void ReductionEngine::grow_pool(int need) {
   DRZG_CUDA(cudaStreamSynchronize(st_));
   if (want > vmm_mapped_) trim_mempool(dev);  // unused stream-ordered reserve back to the driver
   mem_info(&fr, &tot, "engine.cu:2");
+  if (want > vmm_mapped_ + fr / 2) {
+    // other engines' cached pools give their memory back before this one
+    // settles for less
+    std::vector<CachedPool> drop;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      drop.swap(g_pool_cache[dev]);
+    }
+    for (auto& c : drop) {
+      for (auto& k : c.chunks) {
+        V.unmap(reinterpret_cast<CUdeviceptr>(c.base) + k.first, k.second.first);
+        V.release((CUmemGenericAllocationHandle)k.second.second);
+      }
+      V.addr_free(reinterpret_cast<CUdeviceptr>(c.base), c.reserved);
+    }
+    if (!drop.empty()) mem_info(&fr, &tot, "engine.cu:2b");
+  }
   size_t margin = (size_t)2 << 30;
   std::unique_lock<std::mutex> tmp_lock(tmp_mu_, std::defer_lock);
   if (want > vmm_mapped_ + (fr > margin ? fr - margin : 0)) tmp_lock.lock();  // no sweep is launching now
@@ -498,12 +538,17 @@ void ReductionEngine::release_pool() {
   cudaStreamSynchronize(st_);
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    CachedPool& c = g_pool_cache[pool_dev_];
-    if (!c.base && !std::getenv("DRZG_NO_POOL_CACHE")) {
+    auto& v = g_pool_cache[pool_dev_];
+    size_t cached = 0;
+    for (const auto& c0 : v) cached += c0.mapped;
+    const size_t tot = device_total_memory();
+    if (!std::getenv("DRZG_NO_POOL_CACHE") && (v.empty() || !tot || cached + vmm_mapped_ <= tot / 2)) {
+      CachedPool c;
       c.base = pool_;
       c.reserved = vmm_reserved_;
       c.mapped = vmm_mapped_;
       for (auto& k : vmm_chunks_) c.chunks.push_back({k.off, {k.bytes, k.handle}});
+      v.push_back(std::move(c));
       vmm_chunks_.clear();
       pool_ = nullptr;
       return;

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
@@ -61,7 +62,9 @@ struct Traffic {
   std::atomic<long long> h2d{0}, d2h{0}, launches{0};
   void reset() { h2d = 0; d2h = 0; launches = 0; }
 };
-inline Traffic g_traffic;
+// per host thread: a call's launches and copies are issued on the calling thread,
+// so concurrent calls (a batch on several threads) count their own
+inline thread_local Traffic g_traffic;
 // DRZG_TIMELINE diagnostics: host seconds spent in host-side allocation and
 // staging waits (pinned growth, ring waits, stream-ordered allocations)
 struct HostWaits {
@@ -107,9 +110,10 @@ class Stager {
     if (arena_) cudaFreeHost(arena_);
     for (void* h : retired_) cudaFreeHost(h);
   }
-  // one pinned ring per size class for the whole process: concurrent callers
-  // (one host thread per device, say) take turns, so no two copies share a
-  // pinned buffer.  Small requests use fixed slots carved from one arena;
+  // one pinned ring per size class and host thread (engines stage from the
+  // thread that launches their kernels, so a ring only ever waits on its own
+  // stream's copies; the mutex guards misuse).  Small requests use fixed
+  // slots carved from one arena;
   // large ones a short ring whose slots grow to the high-water mark, so that
   // after the first sweeps no copy pins memory (cudaMallocHost costs up to
   // tens of ms, on the launcher's critical path)
@@ -138,7 +142,7 @@ class Stager {
       // whole device, which would stall the launcher behind queued work
       if (b.h) retired_.push_back(b.h);
       hwm_ = std::max(hwm_, bytes);
-      b.cap = std::max<size_t>({2 * bytes, 2 * hwm_, (size_t)8 << 20});
+      b.cap = std::max<size_t>({2 * bytes, 2 * hwm_, (size_t)2 << 20});
       DRZG_CUDA(cudaMallocHost(&b.h, b.cap));
     }
     const long long t2 = now_ns();
@@ -161,8 +165,8 @@ class Stager {
     bool used = false;
     bool carved = false;  // part of the small-slot arena
   };
-  std::vector<Buf> small_ = std::vector<Buf>(128);
-  std::vector<Buf> large_ = std::vector<Buf>(16);
+  std::vector<Buf> small_ = std::vector<Buf>(64);
+  std::vector<Buf> large_ = std::vector<Buf>(8);
   int next_small_ = 0, next_large_ = 0;
   void* arena_ = nullptr;
   size_t hwm_ = 0;
@@ -360,13 +364,16 @@ class ReductionEngine {
   // pinned staging ring shared by every engine of the process: pinning and
   // unpinning host memory costs milliseconds per megabyte, so it is paid once
   // (never freed; the process exit releases it)
-  static Stager& shared_stager() {
-    static Stager* s = new Stager();
-    return *s;
+  // per host thread (concurrent calls never wait on each other's rings); the
+  // engine shares ownership, so it may outlive the thread that built it
+  static std::shared_ptr<Stager> thread_stager() {
+    thread_local std::shared_ptr<Stager> s = std::make_shared<Stager>();
+    return s;
   }
-  Stager& stager_ = shared_stager();
+  std::shared_ptr<Stager> stager_owner_ = thread_stager();
+  Stager& stager_ = *stager_owner_;
   double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
-  unsigned host_threads_ = usable_cores();
+  unsigned host_threads_ = call_cores();
   std::vector<Expo> dirs_host_;
   std::vector<int> pos_m_, pos_r_;  // system order of Homog_L rows / solution indices
 };

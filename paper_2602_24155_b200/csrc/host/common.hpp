@@ -6,6 +6,8 @@
 #pragma once
 
 #include <sched.h>
+#include <algorithm>
+#include <atomic>
 #include <thread>
 
 #include <cstdint>
@@ -109,6 +111,22 @@ inline unsigned usable_cores() {
     return h ? h : 1u;
   }();
   return n;
+}
+
+// calls in flight in this process (frobenius_matrix on several host threads,
+// e.g. a batch of hypersurfaces): their host thread pools share the cores
+inline std::atomic<int>& active_calls() {
+  static std::atomic<int> a{0};
+  return a;
+}
+struct ActiveCall {
+  ActiveCall() { active_calls().fetch_add(1); }
+  ~ActiveCall() { active_calls().fetch_sub(1); }
+};
+// this call's share of the cores
+inline unsigned call_cores() {
+  const int a = std::max(1, active_calls().load());
+  return std::max(1u, usable_cores() / (unsigned)a);
 }
 
 }  // namespace drzg

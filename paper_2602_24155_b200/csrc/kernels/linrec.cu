@@ -14,6 +14,8 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -311,6 +313,21 @@ namespace {
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw contract_error(std::string(what) + ": " + cudaGetErrorString(e), __FILE__, __LINE__);
 }
+// the dynamic shared-memory opt-in of a kernel on the current device only
+// ever rises: it is process-wide, and a concurrent call with a smaller system
+// must not lower it under another thread's launch
+template <class K>
+void raise_smem_limit(K* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> have;
+  int dev = 0;
+  check(cudaGetDevice(&dev), "device");
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& h = have[{reinterpret_cast<const void*>(kernel), dev}];
+  if (h >= bytes) return;
+  check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "smem attr");
+  h = bytes;
+}
 }  // namespace
 
 void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uint64_t* dB, int64_t tmax,
@@ -340,16 +357,11 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
   dim3 grid((side + warps - 1) / warps);
   size_t smem = vec * 8;
   if (smem > 48 * 1024) {
-    check(cudaFuncSetAttribute(dev::linrec_dense_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-          "smem attr");
-    check(cudaFuncSetAttribute(dev::linrec_dense_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-          "smem attr");
-    check(cudaFuncSetAttribute(dev::linrec_dense_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-          "smem attr");
-    check(cudaFuncSetAttribute(dev::linrec_dense_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-          "smem attr");
-    check(cudaFuncSetAttribute(dev::linrec_csr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-          "smem attr");
+    raise_smem_limit(dev::linrec_dense_kernel<1>, smem);
+    raise_smem_limit(dev::linrec_dense_kernel<2>, smem);
+    raise_smem_limit(dev::linrec_dense_kernel<3>, smem);
+    raise_smem_limit(dev::linrec_dense_kernel<4>, smem);
+    raise_smem_limit(dev::linrec_csr_kernel, smem);
   }
   cudaEvent_t e0, e1;
   if (kernel_ms) {
@@ -368,8 +380,7 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
     int dev = 0, sms = 0, per_sm = 0;
     check(cudaGetDevice(&dev), "device");
     check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
-    check(cudaFuncSetAttribute(dev::linrec_dense_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-          "smem attr");
+    raise_smem_limit(dev::linrec_dense_persistent, smem);
     check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::linrec_dense_persistent, 256, smem), "occupancy");
     DRZG_REQUIRE(per_sm >= 1, "linrec: persistent kernel does not fit an SM");
     const int rows_per_block = 8;

@@ -20,15 +20,28 @@ double now_s() {
 }
 }  // namespace
 
+// one stream per (host thread, device), kept for the thread's life: the
+// engine's stream-ordered temporaries return to the retained pool on it and
+// the next call's allocations reuse them in stream order (a fresh stream per
+// call made cudaMallocAsync grow the pool again, up to 0.3 s per K3 zeta);
+// calls on different host threads (a batch of hypersurfaces) overlap
 cudaStream_t device_stream(int device) {
-  static std::mutex mu;
-  static std::map<int, cudaStream_t> streams;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = streams.find(device);
-  if (it != streams.end()) return it->second;
+  struct Streams {
+    std::map<int, cudaStream_t> by_dev;
+    ~Streams() {
+      for (auto& kv : by_dev) {
+        cudaSetDevice(kv.first);
+        cudaStreamSynchronize(kv.second);
+        cudaStreamDestroy(kv.second);
+      }
+    }
+  };
+  thread_local Streams s;
+  auto it = s.by_dev.find(device);
+  if (it != s.by_dev.end()) return it->second;
   cudaStream_t st;
   DRZG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  streams[device] = st;
+  s.by_dev[device] = st;
   return st;
 }
 
@@ -40,11 +53,8 @@ std::set<int> working_set_for(const Hypersurface& X, Policy pol) {
 FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan, const std::set<int>& S,
                             const FrobOptions& opt, int device) {
   double t0 = now_s();
+  ActiveCall active;  // concurrent calls split the host cores
   DRZG_CUDA(cudaSetDevice(device));
-  // one stream per device for the life of the process: the engine's
-  // stream-ordered temporaries return to the retained pool on it and the next
-  // call's allocations reuse them in stream order (a fresh stream per call
-  // made cudaMallocAsync grow the pool again, up to 0.3 s per K3 zeta)
   cudaStream_t st = device_stream(device);
   FrobResult out;
   const int n = X.n;
@@ -86,7 +96,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   FinalReducer fin(X, B, T.dp, hm);
   // while the device runs, the engine's policy, launcher and seed-preparer
   // threads need cores too: expansion takes half of them
-  const int nexp = std::max(1, std::min<int>((int)cols.size(), (int)std::max(1u, usable_cores() / 2)));
+  const int nexp = std::max(1, std::min<int>((int)cols.size(), (int)std::max(1u, call_cores() / 2)));
   std::atomic<size_t> next{0};
   std::vector<std::thread> pool;
   auto join_pool = [&] {
@@ -251,7 +261,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   const int gsize = (int)mono_count(X.nv(), T.D - 1);
   std::vector<std::vector<Z>> colres(cols.size());
   {
-    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)usable_cores()));
+    const int nth = std::max(1, std::min<int>((int)cols.size(), (int)call_cores()));
     std::atomic<size_t> next{0};
     std::vector<std::exception_ptr> errs(nth);
     std::vector<std::thread> pool;
