@@ -221,7 +221,9 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     i64 maxnt = 0;  // solution indices feeding one side row
     for (int g2 = 0; g2 < T.side; ++g2) maxnt = std::max<i64>(maxnt, T.t_ptr[g2 + 1] - T.t_ptr[g2]);
     bound = std::max<i64>(bound, std::max<i64>(T.nv, maxnt) * (4096 + wmax) * half + 4096);
-    fast_ = bound < ((i64)1 << 22);
+    // (and the T_x weights x_i + mu_i, exponents below 4096, fit the 16-bit
+    // halves the epilogue's dp2a products take)
+    fast_ = bound < ((i64)1 << 22) && 4096 + wmax < (1 << 15);
     if (want_tc && maxv < 256) {
       std::vector<int8_t> Jd((size_t)nLp_ * nLp_, 0);
       for (int r = 0; r < T.nL; ++r)

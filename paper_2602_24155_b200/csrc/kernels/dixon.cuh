@@ -226,9 +226,11 @@ __device__ __forceinline__ void epi_row(const EpiCtx& c, const long long (&roff)
     int dg[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      // wg[e][j] is the 16-bit weight packed into the half that meets byte j
+      // of the word: one dp2a per product, no byte extraction
       int xp = tqb[j];
 #pragma unroll
-      for (int e = 0; e < NT; ++e) xp += wg[e][j] * sbyte(cur[e], j);
+      for (int e = 0; e < NT; ++e) xp = j < 2 ? __dp2a_lo(wg[e][j], (int)cur[e], xp) : __dp2a_hi(wg[e][j], (int)cur[e], xp);
       const int tq = (int)__umulhi((unsigned)xp, c.m32);
       dg[j] = xp - tq * c.q - c.h;
       tqb[j] = tq + c.bias;
@@ -375,7 +377,12 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
         const int ii = tm.y & 0xFF, mu = tm.y >> 8;
         roff[e] = (long long)tm.x * a.P + s4;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) wg[e][j] = xs_s[ii][lane * 4 + j] + mu;
+        for (int j = 0; j < 4; ++j) {
+          // |x_i + mu| < 2^15 on the multiply-high path (exponents < 4096):
+          // states 0, 2 in the low half, 1, 3 in the high half (dp2a lo/hi)
+          const int w = xs_s[ii][lane * 4 + j] + mu;
+          wg[e][j] = (j & 1) ? (int)((unsigned)w << 16) : (w & 0xFFFF);
+        }
       }
       uint32_t out[LD];
       switch (nt) {
@@ -390,8 +397,15 @@ __global__ void __launch_bounds__(256, 2) epilogue_kernel(StepArgs a) {
         case 5: epi_row<LD, 5>(c, roff, wg, out); break;
         default: epi_row<LD, 6>(c, roff, wg, out); break;
       }
+      if (lane_word) {
+        if (dst) {
 #pragma unroll
-      for (int t = 0; t < LD; ++t) put(t, out[t]);
+          for (int t = 0; t < LD; ++t) *reinterpret_cast<uint32_t*>(dst + (size_t)t * dstride) = out[t];
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < LD; ++t) put(t, out[t]);
+      }
     } else {
       // wide rows (none in the BASELINE shapes) or operands beyond the
       // multiply-high range: plane loop over the terms, exact 64-bit division
