@@ -10,6 +10,7 @@
 
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "tables.hpp"
@@ -116,7 +117,7 @@ struct ColumnSeeds {
 struct PowerCache {
   std::mutex mu;
   std::map<std::pair<int, int>, std::vector<HPoly>> cache;
-  const std::vector<HPoly>& get(const Hypersurface& X, int N, int s) {
+  const std::vector<HPoly>& get(const Hypersurface& X, int N, int s, int threads = 1) {
     std::lock_guard<std::mutex> lk(mu);
     auto key = std::make_pair(N, s);
     auto it = cache.find(key);
@@ -130,13 +131,13 @@ struct PowerCache {
     out.push_back(one);
     HPoly fr = X.f;
     for (auto& c : fr.c) c %= m;
-    for (int j = 1; j < N; ++j) out.push_back(poly_mul_small(out.back(), fr, m));
+    for (int j = 1; j < N; ++j) out.push_back(poly_mul_small_par(out.back(), fr, m, threads));
     return cache.emplace(key, std::move(out)).first->second;
   }
 };
 
 inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan,
-                                 const RuvTables& T, const HostMod& hm, PowerCache& pc, int col) {
+                                 const RuvTables& T, const HostMod& hm, PowerCache& pc, int col, int threads = 1) {
   ColumnSeeds out;
   out.col = col;
   int m = B.pole_of[col];
@@ -165,7 +166,7 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
       if (t % (i64)p == 0 && t / (i64)p >= m) kappa[(int)t] = cur;
     }
   }
-  const auto& powers = pc.get(X, N, s);
+  const auto& powers = pc.get(X, N, s, threads);
   const Expo one = Expo::ones(nv);
   const Expo& beta = B.mons[col];
   const DigitPlan& dp = T.dp;
@@ -181,31 +182,68 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
     SeedBucket& bk = out.by_pole[P];
     const HPoly& fj = powers[j];
     const auto& tab = fj.table();
-    for (int a = 0; a < fj.size(); ++a) {
-      if (!fj.c[a]) continue;
-      u128 dc = small_s ? (Dj[j] * fj.c[a]) % smod : mulm128(Dj[j], fj.c[a], smod);
-      if (dc == 0) continue;
-      ++out.nterms;
-      Expo full = beta + tab.mons[a] + one;
-      for (int i = 0; i < nv; ++i) full[i] *= (int)p;  // E + 1
-      Expo u;
-      DRZG_REQUIRE(seed_u(full, T.D, T.S, &u), "seed: cannot honor the working set");
-      Expo wm = full - u;
-      DRZG_REQUIRE(wm.nonneg() && wm.total() == T.D, "seed: bad split");
-      for (int i = 0; i < nv; ++i) bk.u.push_back(u[i]);
-      bk.g.push_back((i32)rank_of(wm));
-      size_t off = bk.dig.size();
-      bk.dig.resize(off + dp.Ld);
-      if (fast_digits) {
-        // dc < p^s and kappa < p^M < 2^80: the product fits 128 bits when
-        // s bits + 80 < 128, one reduction
-        const u128 v = (dc >> 47) == 0 ? (dc * kap128) % hm.m128 : mulm128(dc, kap128, hm.m128);
-        split.digits(v, bk.dig.data() + off);
-      } else if (!hm.wide) {
-        to_digits_u128(mulm128(dc, kap128, hm.m128), dp, bk.dig.data() + off);
-      } else {
-        to_digits_z((Z::from_u128(dc) * kap).mod(hm.mz), dp, bk.dig.data() + off);
+    // seeds of monomials [a0, a1) of f^j, appended to `dst` in order
+    auto expand = [&](int a0, int a1, SeedBucket& dst, i64& nterms) {
+      for (int a = a0; a < a1; ++a) {
+        if (!fj.c[a]) continue;
+        u128 dc = small_s ? (Dj[j] * fj.c[a]) % smod : mulm128(Dj[j], fj.c[a], smod);
+        if (dc == 0) continue;
+        ++nterms;
+        Expo full = beta + tab.mons[a] + one;
+        for (int i = 0; i < nv; ++i) full[i] *= (int)p;  // E + 1
+        Expo u;
+        DRZG_REQUIRE(seed_u(full, T.D, T.S, &u), "seed: cannot honor the working set");
+        Expo wm = full - u;
+        DRZG_REQUIRE(wm.nonneg() && wm.total() == T.D, "seed: bad split");
+        for (int i = 0; i < nv; ++i) dst.u.push_back(u[i]);
+        dst.g.push_back((i32)rank_of(wm));
+        size_t off = dst.dig.size();
+        dst.dig.resize(off + dp.Ld);
+        if (fast_digits) {
+          // dc < p^s and kappa < p^M < 2^80: the product fits 128 bits when
+          // s bits + 80 < 128, one reduction
+          const u128 v = (dc >> 47) == 0 ? (dc * kap128) % hm.m128 : mulm128(dc, kap128, hm.m128);
+          split.digits(v, dst.dig.data() + off);
+        } else if (!hm.wide) {
+          to_digits_u128(mulm128(dc, kap128, hm.m128), dp, dst.dig.data() + off);
+        } else {
+          to_digits_z((Z::from_u128(dc) * kap).mod(hm.mz), dp, dst.dig.data() + off);
+        }
       }
+    };
+    const int na = fj.size();
+    const int nth = std::max(1, std::min(threads, na / 8192));
+    if (nth == 1) {
+      expand(0, na, bk, out.nterms);
+      continue;
+    }
+    // the column's monomials split over `threads` workers, concatenated in
+    // order (the first columns of a run are on the device's critical path)
+    std::vector<SeedBucket> part(nth);
+    std::vector<i64> cnt(nth, 0);
+    std::vector<std::exception_ptr> err(nth);
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          expand((int)((i64)na * t / nth), (int)((i64)na * (t + 1) / nth), part[t], cnt[t]);
+        } catch (...) {
+          err[t] = std::current_exception();
+        }
+      });
+    try {
+      expand(0, (int)((i64)na / nth), part[0], cnt[0]);
+    } catch (...) {
+      err[0] = std::current_exception();
+    }
+    for (auto& th : pool) th.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+    for (int t = 0; t < nth; ++t) {
+      out.nterms += cnt[t];
+      bk.u.insert(bk.u.end(), part[t].u.begin(), part[t].u.end());
+      bk.g.insert(bk.g.end(), part[t].g.begin(), part[t].g.end());
+      bk.dig.insert(bk.dig.end(), part[t].dig.begin(), part[t].dig.end());
     }
   }
   return out;

@@ -3,6 +3,8 @@
 // Frobenius expansion, reference homog.hpp:21-142).
 #pragma once
 
+#include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "mono.hpp"
@@ -48,6 +50,45 @@ inline HPoly poly_mul_small(const HPoly& a, const HPoly& f, u128 m) {
     for (const auto& t : ft) acc[(size_t)rank_of(ta.mons[i] + t.e)] += a.c[i] * t.c;
   }
   for (size_t i = 0; i < acc.size(); ++i) r.c[i] = acc[i] % m;
+  return r;
+}
+
+// the same product on `threads` host threads: each accumulates a range of a's
+// terms into its own targets, then the ranges' sums are reduced per target
+// (a target still receives at most |f terms| products in total, so the bound
+// above holds for the sum)
+inline HPoly poly_mul_small_par(const HPoly& a, const HPoly& f, u128 m, int threads) {
+  const int nth = std::max(1, std::min(threads, a.size() / 4096));
+  if (nth == 1) return poly_mul_small(a, f, m);
+  HPoly r(a.nv, a.deg + f.deg);
+  auto ft = f.terms();
+  const auto& ta = a.table();
+  const size_t nr = r.c.size();
+  std::vector<std::vector<u128>> acc(nth);
+  auto run = [&](int t) {
+    acc[t].assign(nr, 0);
+    const int i0 = (int)((i64)a.size() * t / nth), i1 = (int)((i64)a.size() * (t + 1) / nth);
+    for (int i = i0; i < i1; ++i) {
+      if (!a.c[i]) continue;
+      for (const auto& tm : ft) acc[t][(size_t)rank_of(ta.mons[i] + tm.e)] += a.c[i] * tm.c;
+    }
+  };
+  auto reduce = [&](int t) {
+    const size_t k0 = nr * t / nth, k1 = nr * (t + 1) / nth;
+    for (size_t k = k0; k < k1; ++k) {
+      u128 v = 0;
+      for (int u = 0; u < nth; ++u) v += acc[u][k];
+      r.c[k] = v % m;
+    }
+  };
+  auto parallel = [&](auto& phase) {
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t) pool.emplace_back([&, t] { phase(t); });
+    phase(0);
+    for (auto& th : pool) th.join();
+  };
+  parallel(run);
+  parallel(reduce);
   return r;
 }
 

@@ -97,27 +97,55 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   // while the device runs, the engine's policy, launcher and seed-preparer
   // threads need cores too: expansion takes half of them
   const int nexp = std::max(1, std::min<int>((int)cols.size(), (int)std::max(1u, call_cores() / 2)));
-  std::atomic<size_t> next{0};
+  // The first columns are on the device's critical path (the first group
+  // starts when its seeds exist): they are expanded one at a time with all
+  // the expansion threads on each (monomials of f^j split between them); the
+  // rest one column per thread, overlapped with the device.
+  // (only columns large enough to split: a column's dense term bound above
+  // 2^18 monomials, as for the fourfold's 3.1 M; small ones, K3's, stay one
+  // per thread)
+  size_t first = 0;
+  while (first < std::min<size_t>(2, cols.size())) {
+    const int m = B.pole_of[cols[first]];
+    double tb = 0;
+    for (int j = 0; j < plan.N_m[m]; ++j) tb += (double)mono_count(X.nv(), X.d * j);
+    if (tb < (double)(1 << 18)) break;
+    ++first;
+  }
+  std::atomic<size_t> next{first};
+  std::atomic<bool> first_done{false};
   std::vector<std::thread> pool;
   auto join_pool = [&] {
     for (auto& th : pool)
       if (th.joinable()) th.join();
   };
+  auto expand_one = [&](size_t i, int threads) {
+    try {
+      ColumnSeeds cs = expand_column(X, B, plan, T, hm, pc, cols[i], threads);
+      std::lock_guard<std::mutex> lk(smu);
+      seeds[i] = std::move(cs);
+      ready[i] = 1;
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(smu);
+      if (!serr) serr = std::current_exception();
+      ready[i] = 1;
+    }
+    scv.notify_all();
+  };
   for (int t = 0; t < nexp; ++t)
-    pool.emplace_back([&] {
-      for (size_t i = next++; i < cols.size(); i = next++) {
-        try {
-          ColumnSeeds cs = expand_column(X, B, plan, T, hm, pc, cols[i]);
+    pool.emplace_back([&, t] {
+      if (t == 0) {
+        for (size_t i = 0; i < first; ++i) expand_one(i, nexp);
+        {
           std::lock_guard<std::mutex> lk(smu);
-          seeds[i] = std::move(cs);
-          ready[i] = 1;
-        } catch (...) {
-          std::lock_guard<std::mutex> lk(smu);
-          if (!serr) serr = std::current_exception();
-          ready[i] = 1;
+          first_done = true;
         }
         scv.notify_all();
+      } else {
+        std::unique_lock<std::mutex> lk(smu);
+        scv.wait(lk, [&] { return first_done.load() || serr; });
       }
+      for (size_t i = next++; i < cols.size(); i = next++) expand_one(i, 1);
     });
   auto wait_column = [&](size_t i) -> ColumnSeeds& {
     std::unique_lock<std::mutex> lk(smu);
