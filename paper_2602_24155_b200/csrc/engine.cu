@@ -713,6 +713,17 @@ void ReductionEngine::dixon(dev::StepArgs& a) {
     ++clock.gemm_launches;
     clock.gemm_macs += (double)T.dp.Ld * T.nL * T.nL * chunk_steps_;
     clock.carry_macs += (double)(T.dp.Ld - 1) * T.nL * T.nL * chunk_steps_;
+    static const bool hist = std::getenv("DRZG_FUSED_HIST") != nullptr;
+    if (hist) {
+      // state-steps by 64-state blocks per SM of the launch (0: < 1 ... 4: >= 8)
+      static double h[5] = {0, 0, 0, 0, 0};
+      static long long calls = 0;
+      const double per = (double)nb / 64.0 / sms_;
+      h[per < 1 ? 0 : per < 2 ? 1 : per < 4 ? 2 : per < 8 ? 3 : 4] += nb;
+      if (++calls % 985 == 0)
+        std::fprintf(stderr, "[drzg] fused launch states by 64-blocks per SM: <1 %.0f, 1-2 %.0f, 2-4 %.0f, 4-8 %.0f, >=8 %.0f\n",
+                     h[0], h[1], h[2], h[3], h[4]);
+    }
     return;
   }
   if (flow_) {

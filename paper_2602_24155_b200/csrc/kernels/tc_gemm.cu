@@ -1246,6 +1246,274 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
   if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+
+// Two blocks in flight per CTA ("ping-pong"): the fused solve above, with two
+// NS-state blocks (parities p = 0, 1) processed in lockstep through their
+// digits.  Each has its own in/y/h shared-memory boxes and TMEM accumulators
+// (digit products at columns 128 p, carry products at 256 + 128 p), so while
+// the epilogue warps drain one block's phase the MMA unit computes the other
+// block's: the per-digit MMA waits (~0.9 us each of a ~3.9 us digit) leave
+// the critical path.  Order per digit k: D(0,k) D(1,k) | Y(0,k) -> C(0,k),
+// Y(1,k) -> C(1,k) | In(0,k) -> D(0,k+1), In(1,k) -> D(1,k+1).  Barrier phase
+// of pair j, digit k: j Ld + k (D, Y), j (Ld - 1) + k (C, In), j (B0, Free).
+// Same products and epilogue arithmetic per block: identical results.
+namespace fz {
+__host__ __device__ constexpr int smem_bytes_pp(int nt, int NS) { return 2 * nt * nt * TILE + 6 * nt * box_bytes(NS) + 1024 + 256; }
+}  // namespace fz
+
+template <int NS>
+__global__ void __launch_bounds__(fz::THREADS, 1)
+    dixon_fused_pp_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmJ,
+                          const __grid_constant__ CUtensorMap tmB0, uint32_t idesc_c, uint32_t idesc_j, FusedArgs fa) {
+  static_assert(NS <= 64, "two blocks' accumulators must fit 128 TMEM columns each");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nt = fa.nLp / 128;
+  uint8_t* sC = base;
+  uint8_t* sJ = sC + nt * nt * fz::TILE;
+  uint8_t* sIn[2];
+  uint8_t* sY[2];
+  uint8_t* sH[2];
+  {
+    uint8_t* q0 = sJ + nt * nt * fz::TILE;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      sIn[p] = q0;
+      sY[p] = q0 + nt * fz::box_bytes(NS);
+      sH[p] = q0 + 2 * nt * fz::box_bytes(NS);
+      q0 += 3 * nt * fz::box_bytes(NS);
+    }
+  }
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH[1] + nt * fz::box_bytes(NS));
+  uint64_t* barA = bars;
+  uint64_t* barB0 = bars + 1;    // [2] b_0 of the block loaded
+  uint64_t* barD = bars + 3;     // [2] digit product done
+  uint64_t* barC = bars + 5;     // [2] carry product done
+  uint64_t* barY = bars + 7;     // [2] y_k drained
+  uint64_t* barIn = bars + 9;    // [2] in_{k+1}, h_{k+1} written
+  uint64_t* barFree = bars + 11; // [2] the block's last digit product done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int Ld = fa.Ld;
+  const int nblk = (fa.N + NS - 1) / NS;
+  const int nmine = blockIdx.x < nblk ? (nblk - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int npairs = (nmine + 1) / 2;
+  auto blk = [&](int j, int p) { return blockIdx.x + (2 * j + p) * gridDim.x; };
+  auto has = [&](int j, int p) { return 2 * j + p < nmine; };
+
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(barA), 1);
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(smem_u32(barB0 + p), 1);
+      mbar_init(smem_u32(barD + p), 1);
+      mbar_init(smem_u32(barC + p), 1);
+      mbar_init(smem_u32(barY + p), fz::EPI_WARPS);
+      mbar_init(smem_u32(barIn + p), fz::EPI_WARPS);
+      mbar_init(smem_u32(barFree + p), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmJ) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB0) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(smem_u32(barA), (uint32_t)(2 * nt * nt * fz::TILE));
+      for (int mt = 0; mt < nt; ++mt)
+        for (int kb = 0; kb < nt; ++kb) {
+          tma_load_2d(smem_u32(sC + (mt * nt + kb) * fz::TILE), &tmC, smem_u32(barA), kb * 128, mt * 128);
+          tma_load_2d(smem_u32(sJ + (mt * nt + kb) * fz::TILE), &tmJ, smem_u32(barA), kb * 128, mt * 128);
+        }
+      for (int j = 0; j < npairs; ++j)
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          if (!has(j, p)) continue;
+          if (j) mbar_wait(smem_u32(barFree + p), (uint32_t)((j - 1) & 1));
+          mbar_expect_tx(smem_u32(barB0 + p), (uint32_t)(nt * fz::box_bytes(NS)));
+          for (int kb = 0; kb < nt; ++kb)
+            tma_load_2d(smem_u32(sIn[p] + kb * fz::box_bytes(NS)), &tmB0, smem_u32(barB0 + p), blk(j, p) * NS,
+                        kb * 128);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      mbar_wait(smem_u32(barA), 0);
+      for (int j = 0; j < npairs; ++j)
+        for (int k = 0; k < Ld; ++k) {
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            if (!has(j, p)) continue;
+            if (k == 0) {
+              if (j) mbar_wait(smem_u32(barY + p), (uint32_t)((j * Ld - 1) & 1));  // previous block drained
+              mbar_wait(smem_u32(barB0 + p), (uint32_t)(j & 1));
+            } else {
+              mbar_wait(smem_u32(barIn + p), (uint32_t)((j * (Ld - 1) + k - 1) & 1));
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int mt = 0; mt < nt; ++mt)
+              for (int kb = 0; kb < nt; ++kb) {
+                const uint32_t a0 = smem_u32(sC + (mt * nt + kb) * fz::TILE),
+                               b0 = smem_u32(sIn[p] + kb * fz::box_bytes(NS));
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_i8(tmem + (uint32_t)(128 * p + mt * NS), sw128_desc(a0 + kk * 32), mn_desc<NS>(b0 + kk * 32 * NS),
+                         idesc_c, (kb | kk) != 0);
+              }
+            mma_commit(smem_u32(barD + p));
+            if (k + 1 == Ld) mma_commit(smem_u32(barFree + p));
+          }
+          if (k + 1 == Ld) continue;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            if (!has(j, p)) continue;
+            mbar_wait(smem_u32(barY + p), (uint32_t)((j * Ld + k) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            for (int mt = 0; mt < nt; ++mt)
+              for (int kb = 0; kb < nt; ++kb) {
+                const uint32_t a0 = smem_u32(sJ + (mt * nt + kb) * fz::TILE),
+                               b0 = smem_u32(sY[p] + kb * fz::box_bytes(NS));
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                  mma_i8(tmem + (uint32_t)(256 + 128 * p + mt * NS), sw128_desc(a0 + kk * 32),
+                         mn_desc<NS>(b0 + kk * 32 * NS), idesc_j, (kb | kk) != 0);
+              }
+            mma_commit(smem_u32(barC + p));
+          }
+        }
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4, quarter = e & 3, mt = (e >> 2) & 1, half = e >> 3;
+    const int m = mt * 128 + quarter * 32 + lane;
+    const bool active = mt < nt;
+    const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
+    const size_t P = (size_t)fa.P;
+    constexpr int NCH = NS / 32;
+    constexpr int PER = NCH >= 2 ? 2 : 1;
+    for (int j = 0; j < npairs; ++j)
+      for (int k = 0; k < Ld; ++k) {
+        const bool carry = k + 1 < Ld;
+        uint4 b1[2][NCH];
+        // y_k of both blocks
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          if (!has(j, p)) continue;
+          const int n0 = blk(j, p) * NS + half * (NS / 2);
+          if (carry && active) {
+            const int8_t* src = fa.Bg + ((size_t)(k + 1) * fa.nLp + m) * P + n0;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+              b1[p][ch] =
+                  n0 + ch * 16 < fa.N ? __ldcg(reinterpret_cast<const uint4*>(src + ch * 16)) : make_uint4(0, 0, 0, 0);
+          }
+          mbar_wait(smem_u32(barD + p), (uint32_t)((j * Ld + k) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (active) {
+            int8_t* yg = fa.Y + ((size_t)k * fa.nLp + m) * P + n0;
+#pragma unroll
+            for (int hh = 0; hh < NCH / PER; ++hh) {
+              int v[32];
+              if constexpr (PER == 2)
+                tmem_ld32(lanebase + (uint32_t)(128 * p + mt * NS + half * (NS / 2) + hh * 32), v);
+              else
+                tmem_ld16(lanebase + (uint32_t)(128 * p + mt * NS + half * (NS / 2) + hh * 16), v);
+#pragma unroll
+              for (int c2 = 0; c2 < PER; ++c2) {
+                const int ch = hh * PER + c2;
+                uint32_t w4[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                  uint32_t word = 0;
+#pragma unroll
+                  for (int bb = 0; bb < 4; ++bb) {
+                    const int x = v[c2 * 16 + q4 * 4 + bb];
+                    int tdrop;
+                    word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_split(x, tdrop) : fa.fq.bal(x)) << (8 * bb);
+                  }
+                  w4[q4] = word;
+                }
+                const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                if (carry) *reinterpret_cast<uint4*>(sY[p] + swz<NS>(m, half * (NS / 2) + ch * 16)) = y4;
+                if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
+              }
+            }
+          }
+          fence_async_smem();
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(barY + p));
+        }
+        if (!carry) continue;
+        // in_{k+1}, h_{k+1} of both blocks
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          if (!has(j, p)) continue;
+          if (k == 0) mbar_wait(smem_u32(barB0 + p), (uint32_t)(j & 1));  // b_0 (TMA) is r_0
+          mbar_wait(smem_u32(barC + p), (uint32_t)((j * (Ld - 1) + k) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (active) {
+#pragma unroll
+            for (int hh = 0; hh < NCH / PER; ++hh) {
+              int v[32];
+              if constexpr (PER == 2)
+                tmem_ld32(lanebase + (uint32_t)(256 + 128 * p + mt * NS + half * (NS / 2) + hh * 32), v);
+              else
+                tmem_ld16(lanebase + (uint32_t)(256 + 128 * p + mt * NS + half * (NS / 2) + hh * 16), v);
+#pragma unroll
+              for (int c2 = 0; c2 < PER; ++c2) {
+                const int ch = hh * PER + c2;
+                const uint32_t off = swz<NS>(m, half * (NS / 2) + ch * 16);
+                const uint4 lo = *reinterpret_cast<const uint4*>(sIn[p] + off);
+                const uint4 hi = k ? *reinterpret_cast<const uint4*>(sH[p] + off) : make_uint4(0, 0, 0, 0);
+                const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
+                const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
+                const uint32_t b1w[4] = {b1[p][ch].x, b1[p][ch].y, b1[p][ch].z, b1[p][ch].w};
+                uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  const int sh = 8 * (jj & 3);
+                  const int r = (int)(int8_t)(low[jj >> 2] >> sh) + fa.q * (int)(int8_t)(hiw[jj >> 2] >> sh);
+                  const int b1j = (int)(int8_t)(b1w[jj >> 2] >> sh);
+                  const int x = v[c2 * 16 + jj];
+                  int cnew, inb, hq;
+                  if (fa.fast) {
+                    cnew = fa.fq.div_exact_inv(r - x);
+                    inb = fa.fq.bal_split(b1j + cnew, hq);
+                  } else {
+                    int rem;
+                    cnew = fa.fq.divfloor(r - x, rem);
+                    hq = fa.fq.divfloor(b1j + cnew, inb);
+                    if (inb > (fa.q >> 1)) inb -= fa.q, ++hq;
+                  }
+                  in4[jj >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
+                  h4[jj >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
+                }
+                *reinterpret_cast<uint4*>(sIn[p] + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+                *reinterpret_cast<uint4*>(sH[p] + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+              }
+            }
+          }
+          fence_async_smem();
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(barIn + p));
+        }
+      }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 }  // namespace tc
 
 namespace {
@@ -1412,6 +1680,22 @@ const CUtensorMap& cached_map(MapCache& c, const void* p, int a, int b, F make) 
 }
 
 template <int NS>
+void launch_fused_pp(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs& fa, int sms, cudaStream_t st) {
+  const int nt = fa.nLp / 128;
+  thread_local MapCache bcache;
+  const CUtensorMap& mb = cached_map(bcache, fa.Bg, fa.nLp, fa.P, [&] {
+    return make_map_box(fa.Bg, fa.nLp, fa.P, fa.P, NS, 128,
+                        NS == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  });
+  const uint32_t common = (2u << 4) | (1u << 10) | (1u << 16) | ((uint32_t)(NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  const uint32_t idesc_c = common | (1u << 7), idesc_j = common;
+  const int smem = tc::fz::smem_bytes_pp(nt, NS);
+  smem_opt_in(tc::dixon_fused_pp_kernel<NS>, smem);
+  const int nblk = (fa.N + NS - 1) / NS;
+  tc::dixon_fused_pp_kernel<NS><<<std::min(nblk, sms), tc::fz::THREADS, smem, st>>>(mc, mj, mb, idesc_c, idesc_j, fa);
+}
+
+template <int NS>
 void launch_fused(const CUtensorMap& mc, const CUtensorMap& mj, const FusedArgs& fa, int sms, cudaStream_t st) {
   const int nt = fa.nLp / 128;
   thread_local MapCache bcache;
@@ -1452,7 +1736,16 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
   // per K3 zeta function -- the per-digit epilogue phase is what a block
   // waits on, and it halves; DRZG_FUSED_NS=128 keeps the 128-state variant)
   const int ns = fa.chunk ? 32 : ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : 64);
-  if (ns == 32)
+  // two 64-state blocks in flight per CTA once every CTA has two or more
+  // (DRZG_FUSED_PP=0 keeps one block per CTA)
+  static const bool pp_on = [] {
+    const char* e = std::getenv("DRZG_FUSED_PP");
+    return !(e && std::string(e) == "0");
+  }();
+  if (pp_on && !fa.chunk && !ns_env && fa.N >= 2 * 64 * sms &&
+      tc::fz::smem_bytes_pp(fa.nLp / 128, 64) <= 227 * 1024) {
+    launch_fused_pp<64>(mc, mj, fa, sms, st);
+  } else if (ns == 32)
     launch_fused<32>(mc, mj, fa, sms, st);
   else if (ns == 64)
     launch_fused<64>(mc, mj, fa, sms, st);
