@@ -1155,6 +1155,9 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
     qcv.notify_one();
   };
+  // leave cores to the launcher and the seed preparers (an oversubscribed
+  // launcher starves the device)
+  ForkJoin move_pool((int)(host_threads_ > 6 ? host_threads_ - 4 : 2));
   std::thread policy([&] {
     try {
   for (;;) {
@@ -1248,9 +1251,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       std::vector<int> vd(nf);
       std::vector<i64> kk(nf);
       {
-        // leave cores to the launcher and the seed preparers (an oversubscribed
-        // launcher starves the device)
-        const int nth = (int)std::max<size_t>(1, std::min<size_t>(host_threads_ > 6 ? host_threads_ - 4 : 2, nf / 4096 + 1));
+        const int nth = (int)std::max<size_t>(1, std::min<size_t>(move_pool.size(), nf / 4096 + 1));
         std::vector<std::exception_ptr> errs(nth);
         auto moves = [&](int t) {
           try {
@@ -1267,13 +1268,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
             errs[t] = std::current_exception();
           }
         };
-        if (nth == 1) {
-          moves(0);  // small sweeps: no thread start-up on the policy's critical path
-        } else {
-          std::vector<std::thread> pool;
-          for (int t = 0; t < nth; ++t) pool.emplace_back(moves, t);
-          for (auto& th : pool) th.join();
-        }
+        if (nth == 1)
+          moves(0);  // small sweeps: no hand-off on the policy's critical path
+        else
+          move_pool.run(nth, moves);
         for (auto& e2 : errs)
           if (e2) std::rethrow_exception(e2);
       }
@@ -1326,12 +1324,26 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       int lp_pole = -1;
       FlatMap* lp_idx = nullptr;
       std::vector<HS>* lp_lst = nullptr;
-      for (int i : order) {
+      // landing keys first, then the inserts with the probe lines of the
+      // keys kPf positions ahead prefetched (the per-pole maps outgrow the caches)
+      std::vector<u64> lkey(nf);
+      for (size_t o = 0; o < nf; ++o) {
+        const int i = order[o];
+        Expo u = front[f0 + i].u;
+        const Expo& v = dirs_host_[vd[i]];
+        for (int j = 0; j < nv; ++j) u[j] -= (int)(kk[i] * v[j]);
+        lkey[o] = key(front[f0 + i].col, u);
+      }
+      constexpr size_t kPf = 8;
+      for (size_t o = 0; o < nf; ++o) {
+        const int i = order[o];
+        if (o + kPf < nf && lp_idx && front[f0 + order[o + kPf]].pole - (int)kk[order[o + kPf]] == lp_pole)
+          lp_idx->prefetch(lkey[o + kPf]);
         HS h = front[f0 + i];
         const Expo& v = dirs_host_[vd[i]];
         for (int j = 0; j < nv; ++j) h.u[j] -= (int)(kk[i] * v[j]);
         h.pole -= (int)kk[i];
-        const u64 kh = key(h.col, h.u);
+        const u64 kh = lkey[o];
         if (h.pole == n_) {
           fs.push_back(h.slot);
           fc.push_back(h.col);

@@ -9,6 +9,10 @@
 #include <algorithm>
 #include <atomic>
 #include <thread>
+#include <vector>
+#include <mutex>
+#include <functional>
+#include <condition_variable>
 
 #include <cstdint>
 #include <stdexcept>
@@ -112,6 +116,68 @@ inline unsigned usable_cores() {
   }();
   return n;
 }
+
+// A fork-join pool kept for a whole run: run(parts, f) calls f(0..parts-1),
+// part 0 on the calling thread, and returns when all are done (the p-chunk
+// policy's per-sweep moves; spawning threads per sweep cost ~0.5 ms a sweep)
+class ForkJoin {
+ public:
+  explicit ForkJoin(int threads) {
+    for (int t = 1; t < threads; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  ~ForkJoin() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  void run(int parts, const std::function<void(int)>& f) {
+    parts = std::max(1, std::min(parts, size()));
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      f_ = &f;
+      parts_ = parts;
+      pending_ = parts - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    f_ = nullptr;
+  }
+
+ private:
+  void loop(int t) {
+    unsigned long long seen = 0;
+    for (;;) {
+      const std::function<void(int)>* f = nullptr;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        if (t >= parts_) continue;
+        f = f_;
+      }
+      (*f)(t);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* f_ = nullptr;
+  int parts_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+};
 
 // calls in flight in this process (frobenius_matrix on several host threads,
 // e.g. a batch of hypersurfaces): their host thread pools share the cores

@@ -43,6 +43,9 @@ class FlatMap {
       }
     }
   }
+  // the first probe line of a later find/insert of k (the sweeps' landing
+  // loop prefetches a few keys ahead: the per-pole maps outgrow the caches)
+  void prefetch(u64 k) const { __builtin_prefetch(&keys_[hash(k) & mask_]); }
   void swap(FlatMap& o) {
     keys_.swap(o.keys_);
     vals_.swap(o.vals_);

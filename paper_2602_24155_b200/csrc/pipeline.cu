@@ -1,4 +1,8 @@
 // Frobenius assembly + zeta driver (see pipeline.cuh).
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -94,9 +98,10 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   std::condition_variable scv;
   std::exception_ptr serr;
   FinalReducer fin(X, B, T.dp, hm);
-  // while the device runs, the engine's policy, launcher and seed-preparer
-  // threads need cores too: expansion takes half of them
-  const int nexp = std::max(1, std::min<int>((int)cols.size(), (int)std::max(1u, call_cores() / 2)));
+  // expansion takes every core, at a lower scheduling priority (nice +10):
+  // before the first group nothing else needs the host, and once the device
+  // runs the engine's policy, launcher and seed-preparer threads preempt it
+  const int nexp = std::max(1, std::min<int>((int)cols.size(), (int)call_cores()));
   // The first columns are on the device's critical path (the first group
   // starts when its seeds exist): they are expanded one at a time with all
   // the expansion threads on each (monomials of f^j split between them); the
@@ -134,6 +139,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   };
   for (int t = 0; t < nexp; ++t)
     pool.emplace_back([&, t] {
+      setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);  // best effort
       if (t == 0) {
         for (size_t i = 0; i < first; ++i) expand_one(i, nexp);
         {
