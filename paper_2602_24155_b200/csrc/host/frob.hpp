@@ -179,6 +179,19 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
     int P = (int)p * (m + j);
     const Z& kap = kappa.at(P);
     u128 kap128 = hm.wide ? 0 : kap.to_u128();
+    // wide moduli (p^M >= 2^80, e.g. the quintic surface's 7^49): kappa's
+    // base-q digits once per pole; a seed's digits are then those of dc *
+    // kappa mod q^Ld by one schoolbook pass (q^Ld is a multiple of p^M, so
+    // this is the same residue mod p^M as the reference's dc * kappa mod p^M)
+    std::vector<u64> kapd;
+    if (hm.wide) {
+      Z v = kap.mod(hm.mz), qz((long)dp.q);
+      for (int t = 0; t < dp.Ld; ++t) {
+        Z r = v.mod(qz);
+        kapd.push_back((u64)r.to_long());
+        v = (v - r).divexact(qz);
+      }
+    }
     SeedBucket& bk = out.by_pole[P];
     const HPoly& fj = powers[j];
     const auto& tab = fj.table();
@@ -206,6 +219,21 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
           split.digits(v, dst.dig.data() + off);
         } else if (!hm.wide) {
           to_digits_u128(mulm128(dc, kap128, hm.m128), dp, dst.dig.data() + off);
+        } else if ((dc >> 119) == 0) {
+          // balanced digits of (sum_t kapd[t] q^t) * dc mod q^Ld (kapd[t] < 2^8,
+          // dc < 2^119: every partial product and carry fits 128 bits)
+          const u128 d64 = dc;
+          u128 carry = 0;
+          int bc = 0;  // balancing borrow into the next digit
+          const int h = dp.q / 2;
+          for (int t = 0; t < dp.Ld; ++t) {
+            const u128 acc = (u128)kapd[t] * d64 + carry;  // < 2^127 + 2^120
+            int r = (int)(acc % (u128)dp.q) + bc;
+            carry = acc / (u128)dp.q;
+            bc = 0;
+            if (r > h) r -= dp.q, bc = 1;
+            dst.dig[off + t] = (i8)r;
+          }
         } else {
           to_digits_z((Z::from_u128(dc) * kap).mod(hm.mz), dp, dst.dig.data() + off);
         }

@@ -226,6 +226,15 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       std::fprintf(stderr, "[drzg] grouping: column 0 dense term bound %.0f (%.1f GB of states at %.2f), budget %.1f GB\n",
                    b0, kPeakPerBound * b0 * slot_bytes / 1e9, kPeakPerBound, budget / 1e9);
     }
+    bool heavy = false;
+    {
+      double all_terms = 0;
+      for (size_t c = 0; c < cols.size(); ++c) {
+        const int m = B.pole_of[cols[c]];
+        for (int j = 0; j < plan.N_m[m]; ++j) all_terms += (double)mono_count(X.nv(), X.d * j);
+      }
+      heavy = all_terms > (double)(1 << 24);
+    }
     size_t c0 = 0;
     while (c0 < cols.size()) {
       size_t c1 = c0;
@@ -244,9 +253,14 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
         const char* e = std::getenv("DRZG_GROUP_COLS");  // A/B override: columns per group
         return e ? std::max(1, std::atoi(e)) : 0;
       }();
+      // a heavy expansion (the quintic surface: 52 columns of ~2M terms each)
+      // starts the device on a quarter of the columns, the rest expanding
+      // meanwhile
+      const size_t first_cap = heavy && c0 == 0 ? std::max<size_t>(2, (cols.size() + 3) / 4) : cols.size();
       while (c1 < cols.size()) {
         double add = kPeakPerBound * terms_bound(c1) * slot_bytes;
-        if (group_cols ? (int)(c1 - c0) >= group_cols : (c1 > c0 && need + add > budget)) break;
+        if (group_cols ? (int)(c1 - c0) >= group_cols : (c1 > c0 && (need + add > budget || c1 - c0 >= first_cap)))
+          break;
         need += add;
         ++c1;
       }
