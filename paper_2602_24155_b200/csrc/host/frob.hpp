@@ -113,15 +113,15 @@ struct ColumnSeeds {
   std::map<int, SeedBucket> by_pole;  // pole -> seeds
 };
 
-// f^0..f^{N-1} mod p^s, cached per (N, s) for one hypersurface
+// f^0..f^{N-1} mod p^s, cached per (N, s) for one hypersurface.  prime()
+// computes the chain once at the largest (N, s) the run needs (the products
+// split over threads); every other (N, s) is then that chain's prefix reduced
+// mod p^s, one pass over the coefficients instead of a chain of products
 struct PowerCache {
   std::mutex mu;
   std::map<std::pair<int, int>, std::vector<HPoly>> cache;
-  const std::vector<HPoly>& get(const Hypersurface& X, int N, int s, int threads = 1) {
-    std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(N, s);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
+  std::pair<int, int> base{0, 0};
+  static std::vector<HPoly> chain(const Hypersurface& X, int N, int s, int threads) {
     Z smod = Z::pow(X.p, (u64)s);
     DRZG_REQUIRE(smod < (Z(1) << 96), "power series modulus above 2^96");
     u128 m = smod.to_u128();
@@ -132,7 +132,29 @@ struct PowerCache {
     HPoly fr = X.f;
     for (auto& c : fr.c) c %= m;
     for (int j = 1; j < N; ++j) out.push_back(poly_mul_small_par(out.back(), fr, m, threads));
-    return cache.emplace(key, std::move(out)).first->second;
+    return out;
+  }
+  void prime(const Hypersurface& X, int N, int s, int threads) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(N, s);
+    if (cache.find(key) == cache.end()) cache.emplace(key, chain(X, N, s, threads));
+    base = key;
+  }
+  const std::vector<HPoly>& get(const Hypersurface& X, int N, int s, int threads = 1) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(N, s);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (base.first >= N && base.second >= s) {
+      // p^s divides p^{s_base}: reduce the primed chain's prefix
+      const u128 m = Z::pow(X.p, (u64)s).to_u128();
+      const auto& b = cache.at(base);
+      std::vector<HPoly> out(b.begin(), b.begin() + N);
+      for (auto& h : out)
+        for (auto& c : h.c) c %= m;
+      return cache.emplace(key, std::move(out)).first->second;
+    }
+    return cache.emplace(key, chain(X, N, s, threads)).first->second;
   }
 };
 

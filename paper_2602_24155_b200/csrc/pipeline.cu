@@ -92,6 +92,15 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   // columns starts as soon as its own seeds exist, while later columns are
   // still being expanded.  The final reducer's levels are built meanwhile.
   PowerCache pc;
+  // the power series at the largest (N_m, s_m) of the run's columns, once, on
+  // every expansion thread (the columns then reduce its prefix); expansion
+  // thread 0 primes it while this thread builds the final reducer
+  int Nmax = 0, smax = 0;
+  for (int j : cols) {
+    const int m = B.pole_of[j];
+    Nmax = std::max(Nmax, plan.N_m[m]);
+    smax = std::max(smax, plan.s_m[m]);
+  }
   std::vector<ColumnSeeds> seeds(cols.size());
   std::vector<char> ready(cols.size(), 0);
   std::mutex smu;
@@ -141,6 +150,12 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     pool.emplace_back([&, t] {
       setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);  // best effort
       if (t == 0) {
+        try {
+          pc.prime(X, Nmax, smax, nexp);
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(smu);
+          if (!serr) serr = std::current_exception();
+        }
         for (size_t i = 0; i < first; ++i) expand_one(i, nexp);
         {
           std::lock_guard<std::mutex> lk(smu);
