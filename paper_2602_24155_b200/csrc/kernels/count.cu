@@ -12,6 +12,8 @@
 #include "count.cuh"
 
 namespace drzg {
+cudaStream_t device_stream(int device);  // pipeline.cu
+
 namespace dev {
 
 struct CountArgs {
@@ -80,8 +82,11 @@ i64 count_points_device(const Hypersurface& X, int r, i64 budget) {
     powt[v * (X.d + 1)] = 1;
     for (int e = 1; e <= X.d; ++e) powt[v * (X.d + 1) + e] = (unsigned short)F.mul[powt[v * (X.d + 1) + e - 1] * q + v];
   }
-  cudaStream_t st;
-  ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  // the calling thread's stream on this device (pipeline.cu): its retained
+  // stream-ordered allocations serve these buffers without regrowing the pool
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "device");
+  cudaStream_t st = device_stream(dev);
   unsigned short *da, *dm, *dp;
   int *dtc, *dte;
   unsigned long long* dout;
@@ -130,7 +135,6 @@ i64 count_points_device(const Hypersurface& X, int r, i64 budget) {
   cudaFreeAsync(dte, st);
   cudaFreeAsync(dout, st);
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
   return (i64)cnt;
 }
 

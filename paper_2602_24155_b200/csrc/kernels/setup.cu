@@ -17,6 +17,7 @@
 #include "setup.cuh"
 
 namespace drzg {
+cudaStream_t device_stream(int device);  // pipeline.cu
 namespace dev {
 
 // first column c in [0, cols) with row[c] % p != 0, or -1; one block
@@ -119,7 +120,11 @@ std::vector<int> inverse_table(int m, int p) {
 std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<u32>& m) {
   DRZG_REQUIRE((int64_t)rows * ((int64_t)(p - 1) * (p - 1) + p) < (1ll << 31), "pivot_scan_device: lazy bound");
   cudaStream_t st;
-  ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "device");
+    st = device_stream(dev);  // the thread's stream: retained allocations, no pool regrowth
+  }
   int *da = nullptr, *dpiv = nullptr, *dinv = nullptr, *dfac = nullptr;
   size_t nn = (size_t)rows * cols;
   ck(cudaMallocAsync(&dfac, (rows + 1) * sizeof(int), st), "alloc");
@@ -156,14 +161,18 @@ std::vector<int> pivot_scan_device(u64 p, int rows, int cols, const std::vector<
   cudaFreeAsync(dinv, st);
   cudaFreeAsync(dfac, st);
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
+  cudaStreamSynchronize(st);
   return piv;
 }
 
 std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32>& a) {
   DRZG_REQUIRE(q < 256 && (int64_t)n * (int64_t)(q * q) < (1ll << 31), "inverse_mod_q_device: lazy bound");
   cudaStream_t st;
-  ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+  {
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "device");
+    st = device_stream(dev);  // the thread's stream: retained allocations, no pool regrowth
+  }
   const int w = 2 * n;
   std::vector<int> h((size_t)n * w, 0);
   for (int i = 0; i < n; ++i) {
@@ -207,7 +216,7 @@ std::vector<u32> inverse_mod_q_device(u64 p, u64 q, int n, const std::vector<u32
   cudaFreeAsync(dinv, st);
   cudaFreeAsync(dfac, st);
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
+  cudaStreamSynchronize(st);
   std::vector<u32> inv((size_t)n * n);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) inv[(size_t)i * n + j] = (u32)h[(size_t)i * w + n + j];
