@@ -211,6 +211,11 @@ char* drzg_gather_F(drzg_comm* comm, int32_t b, const char* const* F_local, cons
 char* drzg_gather_F_host(int32_t nranks, int32_t b, const char* const* F_blocks, const int32_t* cols,
                          const int32_t* col_ptr, int32_t width);
 
+/* Fedder's F-splitting criterion, one of run_zeta's invariants (zeta.hpp:
+ * 336-350): *out = 1 / 0, or -1 where run_zeta leaves it undefined (d > n+1).
+ * Host only.  0 on success. */
+int drzg_fsplit(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -527,6 +527,14 @@ char* ref_frobenius(u64 p, int n, int d, const u64* coeffs, const char* policy, 
   });
 }
 
+// Fedder's F-splitting criterion of run_zeta's invariants (zeta.hpp:336-350,
+// 536-539): 1 / 0, or -1 where run_zeta leaves it undefined (d > n + 1)
+int ref_fsplit(u64 p, int n, int d, const u64* coeffs) {
+  Hypersurface X = make_x(p, n, d, coeffs);
+  if (d > X.nv()) return -1;
+  return fedder_is_fsplit(X) ? 1 : 0;
+}
+
 // full driver (zeta.hpp:438-549)
 char* ref_zeta(u64 p, int n, int d, const u64* coeffs, const char* policy, const char* pep,
                int threads, int r_uniform, int nm_override, int verify_counts) {

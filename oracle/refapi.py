@@ -86,6 +86,13 @@ def mono_table(nv, deg):
     return _js(lib().ref_mono_table(nv, deg))["mons"]
 
 
+def fsplit(p, n, d, coeffs):
+    """the reference's fedder_is_fsplit (zeta.hpp:336-350); None where
+    run_zeta leaves it undefined (d > n + 1)"""
+    v = lib().ref_fsplit(ctypes.c_uint64(p), n, d, _u64(coeffs))
+    return None if v < 0 else bool(v)
+
+
 def hypersurface(p, n, d, seed=1, mode="random", policy="p-chunk"):
     return _js(lib().ref_hypersurface(ctypes.c_uint64(p), n, d, ctypes.c_uint64(seed), mode.encode(),
                                       policy.encode()))["coeffs"]

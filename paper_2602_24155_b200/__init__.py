@@ -198,6 +198,14 @@ def random_hypersurface(p, n, d, seed=1, policy="p-chunk", fermat=False):
     return [int(x) for x in out]
 
 
+def fsplit(p, n, d, coeffs):
+    """Fedder's F-splitting criterion as run_zeta reports it (zeta.hpp:336-350):
+    True / False, or None where it is undefined (d > n + 1)"""
+    out = ctypes.c_int32()
+    _check(lib().drzg_fsplit(ctypes.c_uint64(p), n, d, _u64arr(coeffs), ctypes.byref(out)))
+    return None if out.value < 0 else bool(out.value)
+
+
 def count_points(p, n, d, coeffs, r, budget=200_000_000):
     """brute-force #X(F_{p^r}) (reference oracle.hpp:190-245)"""
     out = ctypes.c_int64()

@@ -631,6 +631,16 @@ extern "C" int drzg_test_final_levels(uint64_t p, int32_t n, int32_t d, const ui
 namespace drzg {
 std::pair<long long, long long> debug_order_blocks(const RuvTables& T);
 }
+// Fedder's F-splitting criterion as run_zeta's invariants report it (host
+// only): 1 / 0, or -1 where it is undefined (d > n + 1); reference
+// zeta.hpp:336-350
+extern "C" int drzg_fsplit(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t* out) {
+  return guard_int([&] {
+    Hypersurface X = Hypersurface::make(p, n, d, coeff_vec(n, d, coeffs));
+    *out = d > X.nv() ? -1 : (fedder_is_fsplit(X) ? 1 : 0);
+  });
+}
+
 // debug hook: nonzero 128 x 128 Jp blocks of the carry order, without (out[0])
 // and with (out[1]) the T_x grouping of solution indices
 extern "C" int drzg_debug_order(uint64_t p, int32_t n, int32_t d, const uint64_t* coeffs, int32_t M, int64_t* out) {

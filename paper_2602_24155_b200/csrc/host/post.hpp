@@ -357,7 +357,24 @@ inline bool fedder_is_fsplit(const Hypersurface& X) {
   HPoly pw = X.f;
   for (auto& c : pw.c) c %= pm;
   HPoly fr = pw;
-  for (u64 t = 2; t <= X.p - 1; ++t) pw = poly_mul_small(pw, fr, pm);
+  // a term with an exponent above p - 1 never comes back into the box (the
+  // products only raise exponents): pruning them keeps the powers small
+  auto prune = [&](HPoly& h) {
+    const auto& tab = h.table();
+    for (int i = 0; i < h.size(); ++i) {
+      if (!h.c[i]) continue;
+      for (int v = 0; v < X.nv(); ++v)
+        if (tab.mons[i][v] > (int)X.p - 1) {
+          h.c[i] = 0;
+          break;
+        }
+    }
+  };
+  prune(pw);
+  for (u64 t = 2; t <= X.p - 1; ++t) {
+    pw = poly_mul_small(pw, fr, pm);
+    prune(pw);
+  }
   for (const auto& t : pw.terms()) {
     bool small = true;
     for (int i = 0; i < X.nv(); ++i)

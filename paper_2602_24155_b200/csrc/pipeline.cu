@@ -401,7 +401,9 @@ std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const 
                         const ZetaOptions& opt, ZetaOut& res) {
   res.hodge = hodge_numbers(X.n, X.d);
   Z cp_mod = Z::pow(X.p, (u64)(plan.M + X.n));
+  const double tb0 = now_s();
   std::vector<Z> dres = berkowitz(F, (int)b, cp_mod);
+  if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] charpoly %.4f s\n", now_s() - tb0);
   Recovered rec = recover_Q(dres, plan);
   if (rec.status == 2) return rec.reason;
   auto cands = std::move(rec.candidates);
@@ -441,7 +443,9 @@ std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const 
       CountCheck ck;
       ck.r = r;
       ck.from_zeta = counts_from_zeta(a, X.p, X.n, r);
+      const double tc0 = now_s();
       ck.from_count = Z((long)count_points_any(X, r, opt.count_budget));
+      if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] count r=%d %.4f s\n", r, now_s() - tc0);
       ck.ok = ck.from_zeta == ck.from_count;
       counts_ok = counts_ok && ck.ok;
       checks.push_back(ck);
@@ -455,8 +459,10 @@ std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const 
   res.inv = classify(np, res.hodge, X.n, X.d);
   res.domino = domino_number(np, res.hodge, X.n);
   if (X.d <= X.nv()) {
+    const double tf0 = now_s();
     res.inv.fsplit_defined = true;
     res.inv.fsplit = fedder_is_fsplit(X);
+    if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] fsplit %.4f s\n", now_s() - tf0);
   }
   res.counts = checks;
   res.plan = plan;
@@ -471,6 +477,7 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
   if (!check_smooth(X, S)) throw std::runtime_error("input not smooth for the requested working set");
   Basis B = compute_basis(X);
   PrecisionPlan plan = choose_precision(X.p, X.n, X.d, opt.overrides);
+  if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] zeta setup %.4f s\n", now_s() - t0);
   ZetaOut res;
   for (;;) {
     FrobOptions fo;
