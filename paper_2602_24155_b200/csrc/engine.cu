@@ -1032,6 +1032,19 @@ class SeedPreparer {
 };
 }  // namespace
 
+namespace {
+// seed-preparer threads (DRZG_PREP_THREADS overrides; default a quarter of
+// the cores, at most 4)
+unsigned prep_threads_for(unsigned host_threads) {
+  static const int env = [] {
+    const char* e = std::getenv("DRZG_PREP_THREADS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return (unsigned)env;
+  return std::max(1u, std::min(host_threads / 4, 4u));
+}
+}  // namespace
+
 void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std::vector<i64>>& G, Ledger& led) {
   const RuvTables& T = *T_;
   const int nv = T.nv, Ld = T.dp.Ld, ncol = (int)cols.size();
@@ -1123,7 +1136,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   // (descending pole): key sort, grouping by (column, u) and by side row g,
   // and the carried digit sums of each group's entries
   auto prep_owner = std::make_unique<SeedPreparer>(cols, top0, [&](int c, const Expo& u) { return key(c, u); }, nv, Ld,
-                                                   T.dp.q, std::max(1u, std::min(host_threads_ / 4, 4u)));
+                                                   T.dp.q, prep_threads_for(host_threads_));
   SeedPreparer& prep = *prep_owner;
   // The policy (moves, landing, combines, seeds, slot bookkeeping) never
   // needs a device result, so it runs on its own thread as far ahead as it
@@ -1196,10 +1209,17 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       p_add.assign(1, 0);
       for (int c = 0; c < ncol; ++c) {
         if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
+        const auto hw0 = std::chrono::steady_clock::now();
         PrepBucket& pb = prep.wait(c, P);
+        prep_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - hw0).count();
         led.combines += pb.combines;
         const size_t ng = pb.key.size();
+        // the landed-state index outgrows the caches: probe lines prefetched ahead
+        constexpr size_t kPf = 8;
+        if (!pb.first)
+          for (size_t gi = 0; gi < std::min(ng, kPf); ++gi) front_idx.prefetch(pb.key[gi]);
         for (size_t gi = 0; gi < ng; ++gi) {
+          if (!pb.first && gi + kPf < ng) front_idx.prefetch(pb.key[gi + kPf]);
           const int fpos = pb.first ? -1 : front_idx.find(pb.key[gi]);
           const int e0 = pb.eptr[gi], e1 = pb.eptr[gi + 1];
           if (fpos >= 0) {
@@ -1555,8 +1575,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
   }
   if (std::getenv("DRZG_VERBOSE"))
-    std::fprintf(stderr, "[drzg] host s: seeds %.3f combine %.3f moves %.3f launch %.3f land %.3f\n", host_t_[0],
-                 host_t_[1], host_t_[2], host_t_[3], host_t_[4]);
+    std::fprintf(stderr, "[drzg] host s: seeds %.3f (waiting for the preparers %.3f) combine %.3f moves %.3f launch %.3f land %.3f\n",
+                 host_t_[0], prep_wait_s_, host_t_[1], host_t_[2], host_t_[3], host_t_[4]);
   std::vector<long long> hG(dG.n);
   DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
   g_traffic.d2h += (long long)(dG.n * sizeof(long long));
