@@ -973,6 +973,20 @@ class SeedPreparer {
     PrepBucket& pb = *jb.pb;
     const int nv = nv_, Ld = Ld_, q = q_;
     const size_t ns = bk.size();
+    if (pb.first) {
+      // a column's first sweep keeps its seeds apart: every seed is its own
+      // group with its one side row, and its digits are already balanced
+      // (expand_column), so the bucket is taken over as it stands
+      pb.u = std::move(bk.u);
+      pb.eg = std::move(bk.g);
+      pb.ed = std::move(bk.dig);
+      pb.eptr.resize(ns + 1);
+      for (size_t i = 0; i <= ns; ++i) pb.eptr[i] = (int)i;
+      SeedBucket().u.swap(bk.u);
+      SeedBucket().g.swap(bk.g);
+      SeedBucket().dig.swap(bk.dig);
+      return;
+    }
     std::vector<u64> kv(ns);
     for (size_t i = 0; i < ns; ++i) {
       Expo u(nv);
@@ -1213,7 +1227,32 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         PrepBucket& pb = prep.wait(c, P);
         prep_wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - hw0).count();
         led.combines += pb.combines;
-        const size_t ng = pb.key.size();
+        const size_t ng = pb.eptr.size() - 1;  // (first buckets carry no keys: never looked up)
+        if (pb.first) {
+          // a column's first bucket: every seed is its own fresh state (no
+          // lookups), one side row each -- bulk copies, slots taken at once
+          if (free_.size() < ng) grow_pool(cap_ + (int)(ng - free_.size()));
+          const size_t f0n = front.size(), s0n = s_new.size();
+          const int g0n = (int)g_new.size();
+          front.resize(f0n + ng);
+          s_new.resize(s0n + ng);
+          for (size_t gi = 0; gi < ng; ++gi) {
+            HS& h = front[f0n + gi];
+            h.col = c;
+            h.u = Expo(nv);
+            for (int t = 0; t < nv; ++t) h.u[t] = pb.u[gi * nv + t];
+            h.pole = P;
+            h.slot = alloc_slot();
+            s_new[s0n + gi] = h.slot;
+          }
+          g_new.insert(g_new.end(), pb.eg.begin(), pb.eg.end());
+          d_new.insert(d_new.end(), pb.ed.begin(), pb.ed.end());
+          p_new.reserve(p_new.size() + ng);
+          for (size_t gi = 0; gi < ng; ++gi) p_new.push_back(g0n + pb.eptr[gi + 1]);
+          prep.release(c, P);
+          ++sit[c];
+          continue;
+        }
         // the landed-state index outgrows the caches: probe lines prefetched ahead
         constexpr size_t kPf = 8;
         if (!pb.first)
