@@ -23,6 +23,7 @@
 
 namespace drzg {
 void set_last_error(const std::string& s);
+cudaStream_t device_stream(int device);  // pipeline.cu
 
 namespace {
 struct Nccl {
@@ -173,8 +174,7 @@ char* drzg_gather_F(drzg_comm* c, int32_t b, const char* const* F_local, const i
     std::vector<int> own(cols, cols + ncols);
     std::vector<int64_t> mine = encode_columns(b, F, own, width);
     const size_t per = mine.size();
-    cudaStream_t st;
-    DRZG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    cudaStream_t st = device_stream(cm.device);  // the thread's stream (retained allocations)
     int64_t *dsend = nullptr, *drecv = nullptr;
     DRZG_CUDA(cudaMallocAsync(&dsend, per * 8, st));
     DRZG_CUDA(cudaMallocAsync(&drecv, per * 8 * cm.nranks, st));
@@ -185,7 +185,6 @@ char* drzg_gather_F(drzg_comm* c, int32_t b, const char* const* F_local, const i
     DRZG_CUDA(cudaFreeAsync(dsend, st));
     DRZG_CUDA(cudaFreeAsync(drecv, st));
     DRZG_CUDA(cudaStreamSynchronize(st));
-    DRZG_CUDA(cudaStreamDestroy(st));
     std::vector<Z> full = decode_blocks(b, all, cm.nranks, width);
     std::ostringstream os;
     os << "{\"F\":[";
