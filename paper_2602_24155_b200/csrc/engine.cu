@@ -233,7 +233,7 @@ ReductionEngine::ReductionEngine(const RuvTables& T, int n, u64 p, cudaStream_t 
     }
   }
   sparse_carry_ = sparse_carry_ && use_tc_;
-  DRZG_REQUIRE((size_t)dev::kGatherStates * sidep_ <= 200 * 1024, "engine: side too large for the gather staging");
+  DRZG_REQUIRE(dev::gather_smem_bytes(sidep_) <= 200 * 1024, "engine: side too large for the gather staging");
   // the shared-memory opt-ins are per (kernel, device) and process-wide:
   // set once per device at the largest size any engine launches (an engine
   // of another shape on a concurrent thread must not lower it under a launch)
@@ -835,7 +835,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
       // fused Dixon solve with T_x in-kernel), then W -> pool for all
       dev::StepArgs a = make_args(b0, nb, 1);
       const int gb = (nb + dev::kGatherStates - 1) / dev::kGatherStates;
-      const size_t gsm = (size_t)dev::kGatherStates * sidep_;
+      const size_t gsm = dev::gather_smem_bytes(sidep_);
       timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gb, dev::kGatherThreads, gsm, st_>>>(a); });
       i64 steps = 0;
       for (int i = 0; i < nb; ++i) steps += ks[b0 + i];
@@ -863,7 +863,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
       dev::StepArgs a = make_args(b0, By, (int)y);
       if (y == 1) {
         const int gb = (By + dev::kGatherStates - 1) / dev::kGatherStates;
-        const size_t gsm = (size_t)dev::kGatherStates * sidep_;
+        const size_t gsm = dev::gather_smem_bytes(sidep_);
         timed(&clock.gather_ms, [&] { dev::gather_kernel<<<gb, dev::kGatherThreads, gsm, st_>>>(a); });
       }  // later steps: the previous epilogue already wrote this step's operand
       chunk_steps_ = (double)By;

@@ -40,8 +40,13 @@ __device__ __forceinline__ int balmod(int x, int q) {
 // (Digit 0 of a pool state is balanced, so b_0 is the first digit GEMM's
 // operand as it stands and the first carry's residual r_0.)
 constexpr int kGatherStates = 32, kGatherThreads = 512;
+// shared memory holds the block's plane transposed, [g][32 states], rows
+// padded to 36 bytes so the transposing stores and the row reads are free of
+// bank conflicts
+constexpr int kGatherPitch = 36;
+inline size_t gather_smem_bytes(int sidep) { return (size_t)sidep * kGatherPitch; }
 __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepArgs a) {
-  extern __shared__ int8_t planes[];  // kGatherStates x sidep
+  extern __shared__ __align__(16) int8_t planes[];  // sidep x kGatherPitch: [g][state]
   __shared__ int vd[kGatherStates];
   __shared__ long long base[kGatherStates];
   __shared__ int uniform_v;
@@ -60,40 +65,54 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepArgs a) {
     uniform_v = u;
   }
   const size_t P = (size_t)a.P, plane = (size_t)a.nLp * P;
-  const int words = sidep / 16;
+  const int words = sidep / 4;          // 4-row groups g4 of a slot plane
+  const int groups = (words + 7) / 8;   // 8 g4 x 4 state quads per warp-wide work unit
   for (int t = 0; t < a.Ld; ++t) {
     __syncthreads();  // the previous plane is consumed (and uniform_v is set)
-    for (int e = tid; e < kGatherStates * words; e += kGatherThreads) {
-      const int i = e / words, w = e - i * words;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (base[i] >= 0) v = __ldg(reinterpret_cast<const uint4*>(a.pool + base[i] + (size_t)t * sidep) + w);
-      reinterpret_cast<uint4*>(planes + (size_t)i * sidep)[w] = v;
+    // transposing load: a lane takes rows 4 g4 .. 4 g4 + 3 of four states
+    // (one quad), 4 x 4 bytes, and stores them as four words of [g][state];
+    // a warp reads 32 contiguous bytes of each of its 4 quads' 16 states
+    for (int e = tid; e < groups * 32 * 2; e += kGatherThreads) {
+      const int qh = e / (groups * 32), rest = e - qh * groups * 32;
+      const int gq = rest >> 5, lane = rest & 31;
+      const int g4 = gq * 8 + (lane >> 2), q = (lane & 3) + 4 * qh;
+      if (g4 >= words) continue;
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const long long bs = base[q * 4 + k];
+        w[k] = bs >= 0 ? __ldg(reinterpret_cast<const uint32_t*>(a.pool + bs + (size_t)t * sidep) + g4) : 0u;
+      }
+      const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140), hi01 = __byte_perm(w[0], w[1], 0x7362);
+      const uint32_t lo23 = __byte_perm(w[2], w[3], 0x5140), hi23 = __byte_perm(w[2], w[3], 0x7362);
+      int8_t* dst = planes + (size_t)(4 * g4) * kGatherPitch + 4 * q;
+      *reinterpret_cast<uint32_t*>(dst) = __byte_perm(lo01, lo23, 0x5410);
+      *reinterpret_cast<uint32_t*>(dst + kGatherPitch) = __byte_perm(lo01, lo23, 0x7632);
+      *reinterpret_cast<uint32_t*>(dst + 2 * kGatherPitch) = __byte_perm(hi01, hi23, 0x5410);
+      *reinterpret_cast<uint32_t*>(dst + 3 * kGatherPitch) = __byte_perm(hi01, hi23, 0x7632);
     }
     __syncthreads();
     const int uv = uniform_v;
     for (int r = tid; r < nL; r += kGatherThreads) {
       uint32_t wd[8];
       if (uv >= 0) {
+        // one state direction: the row's 32 bytes are one padded row of the
+        // transposed plane
         const int g = __ldg(a.gidx + (size_t)uv * nL + r);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint32_t word = 0;
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            word |= (uint32_t)(uint8_t)(g >= 0 ? planes[(size_t)(q * 4 + b) * sidep + g] : 0) << (8 * b);
-          wd[q] = word;
-        }
+        for (int q8 = 0; q8 < 8; ++q8)
+          wd[q8] = g >= 0 ? *reinterpret_cast<const uint32_t*>(planes + (size_t)g * kGatherPitch + 4 * q8) : 0u;
       } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q8 = 0; q8 < 8; ++q8) {
           uint32_t word = 0;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            const int i = q * 4 + b;
+            const int i = q8 * 4 + b;
             const int g = vd[i] >= 0 ? __ldg(a.gidx + (size_t)vd[i] * nL + r) : -1;
-            word |= (uint32_t)(uint8_t)(g >= 0 ? planes[(size_t)i * sidep + g] : 0) << (8 * b);
+            word |= (uint32_t)(uint8_t)(g >= 0 ? planes[(size_t)g * kGatherPitch + i] : 0) << (8 * b);
           }
-          wd[q] = word;
+          wd[q8] = word;
         }
       }
       uint4* dst = reinterpret_cast<uint4*>(a.Bg + (size_t)t * plane + (size_t)r * P + s0);
