@@ -392,6 +392,59 @@ def fourfold_leg(drzg, torch, local, peak):
     }
 
 
+def fourfold_leg_dist(drzg, torch, dist, world, rank, local):
+    """ONE complete zeta function of configs[4] with its columns partitioned
+    over the ranks (longest-processing-time on the reference's replayed
+    per-column matvecs), F assembled by drzg_gather_F (one ncclAllGather), and
+    run_zeta's battery (drzg_zeta_from_F: Q, Newton >= Hodge, both point
+    counts) on rank 0.  Time = max over ranks of the whole call sequence.
+    Returns the result on rank 0, None elsewhere."""
+    from paper_2602_24155_b200 import parallel
+    p, n, d, seed, desc = CONFIGS["fourfold"]
+    coeffs = drzg.random_hypersurface(p, n, d, seed=seed)
+    b = sum(hodge_counts(n, d))
+    weights = parallel.replayed_column_weights(os.path.join(GOLD, "ledger_replay_fourfold.json"))
+    mine = parallel.partition_columns(n, d, world, rank, weights=weights)
+    t0 = time.time()
+    drzg.frobenius(p, n, d, coeffs, columns=mine[:1], device=local)  # tables, state pool, allocations
+    parallel.nccl_comm(world, rank, local)  # communicator set up outside the timed region
+    warm = time.time() - t0
+    with ClockSampler(local, "_fourfold") as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark()
+        t1 = time.time()
+        fr = drzg.frobenius(p, n, d, coeffs, columns=mine, device=local)
+        F = parallel.gather_frobenius_nccl(fr["F"], b, mine, world, rank, local)
+        z = None
+        if rank == 0:
+            z = drzg.zeta_from_F(p, n, d, coeffs, [str(x) for x in F], b, count_budget=FOURFOLD_COUNT_BUDGET)
+        torch.cuda.synchronize()
+        wall = time.time() - t1
+    clocks = clk.summary()
+    led = [fr["matvecs"], fr["startups"], fr["combines"], fr["kernels"]["device_ms"] / 1e3, wall]
+    if dist:
+        t = torch.tensor(led[:3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        m = torch.tensor(led[3:], dtype=torch.float64, device="cuda")
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        led = t.tolist() + m.tolist()
+    if rank != 0:
+        return None
+    ref = full_ledger("fourfold")
+    mine_led = {"matvecs": int(led[0]), "startups": int(led[1]), "combines": int(led[2])}
+    return {
+        "workload": desc + f", columns partitioned over {world} GPU(s), F gathered by one ncclAllGather",
+        "value": led[4], "unit": "s", "n_gpus": world, "warmup_s": warm, "device_s_max_rank": led[3],
+        "status": z["status"], "ledger": mine_led, "reference_ledger": ref,
+        "ledger_equal": bool(ref) and all(mine_led[k] == ref[k] for k in mine_led),
+        "Q_sha256": hashlib.sha256(json.dumps(z.get("Q")).encode()).hexdigest() if z.get("Q") else None,
+        "counts": z.get("counts"), "counts_ok": bool(z.get("counts")) and all(ok for (_, _, ok) in z["counts"]),
+        "clocks_rank0": clocks,
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -399,7 +452,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="k3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--fourfold-leg", default="auto", choices=["auto", "on", "off"])
+    ap.add_argument("--fourfold-leg", default="auto", choices=["auto", "on", "off", "dist"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
@@ -508,6 +561,13 @@ def main():
     clocks = clk.summary()
     # profiled pass: per-kernel CUDA-event times on the engine stream
     _, _, frp = step(profile=True)
+    # the metric's own configuration across all ranks (every rank takes part)
+    dist_leg = None
+    if args.config == "k3" and (args.fourfold_leg == "dist" or (args.fourfold_leg in ("auto", "on") and world > 1)):
+        try:
+            dist_leg = fourfold_leg_dist(drzg, torch, dist, world, rank, local)
+        except Exception as e:
+            dist_leg = {"error": str(e)} if rank == 0 else None
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -557,7 +617,10 @@ def main():
         "cpu_baseline": cpu, "clocks": clocks,
         "Q_head": (z["Q"][:4] if z and "Q" in z else None),
     }
-    leg = args.fourfold_leg == "on" or (args.fourfold_leg == "auto" and world == 1 and args.config == "k3")
+    if dist_leg is not None:
+        line["fourfold"] = dist_leg
+    leg = dist_leg is None and (args.fourfold_leg == "on" or (args.fourfold_leg == "auto" and world == 1 and
+                                                               args.config == "k3"))
     if leg:
         try:
             line["fourfold"] = fourfold_leg(drzg, torch, local, peak)
