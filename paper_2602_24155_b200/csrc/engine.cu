@@ -1186,6 +1186,12 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
   // launcher starves the device)
   ForkJoin move_pool((int)(host_threads_ > 6 ? host_threads_ - 4 : 2));
   std::thread policy([&] {
+    const auto pol0 = std::chrono::steady_clock::now();
+    struct PolicyWall {
+      std::chrono::steady_clock::time_point t0;
+      double* acc;
+      ~PolicyWall() { *acc += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+    } policy_wall{pol0, &policy_wall_s_};
     try {
   for (;;) {
     int P = -1;
@@ -1221,6 +1227,34 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       std::vector<int8_t>& d_new = cmd->d_new; std::vector<int8_t>& d_add = cmd->d_add;
       p_new.assign(1, 0);
       p_add.assign(1, 0);
+      // the lookups of this pole's seed groups against the landed states
+      // (cache-missing probes of a large index) on the move pool's threads
+      // first, when there are many (K3's seed poles p(m+j): ~10 ms of the
+      // device's wait otherwise); the index is only read
+      std::vector<std::vector<int>> fposv(ncol);
+      {
+        std::vector<int> heavy;
+        size_t total = 0;
+        for (int c = 0; c < ncol; ++c) {
+          if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
+          PrepBucket& pb = prep.wait(c, P);
+          if (pb.first || front_idx.empty()) continue;
+          heavy.push_back(c);
+          total += pb.key.size();
+        }
+        if (total >= 16384 && move_pool.size() > 1) {
+          const int nth = move_pool.size();
+          move_pool.run(nth, [&](int t) {
+            for (size_t h2 = t; h2 < heavy.size(); h2 += nth) {
+              const int c = heavy[h2];
+              PrepBucket& pb = prep.wait(c, P);
+              std::vector<int>& fp = fposv[c];
+              fp.resize(pb.key.size());
+              for (size_t gi = 0; gi < pb.key.size(); ++gi) fp[gi] = front_idx.find(pb.key[gi]);
+            }
+          });
+        }
+      }
       for (int c = 0; c < ncol; ++c) {
         if (sit[c] == cols[c].by_pole.rend() || sit[c]->first != P) continue;
         const auto hw0 = std::chrono::steady_clock::now();
@@ -1257,9 +1291,10 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         constexpr size_t kPf = 8;
         if (!pb.first)
           for (size_t gi = 0; gi < std::min(ng, kPf); ++gi) front_idx.prefetch(pb.key[gi]);
+        const std::vector<int>& fp = fposv[c];
         for (size_t gi = 0; gi < ng; ++gi) {
-          if (!pb.first && gi + kPf < ng) front_idx.prefetch(pb.key[gi + kPf]);
-          const int fpos = pb.first ? -1 : front_idx.find(pb.key[gi]);
+          if (fp.empty() && !pb.first && gi + kPf < ng) front_idx.prefetch(pb.key[gi + kPf]);
+          const int fpos = !fp.empty() ? fp[gi] : pb.first ? -1 : front_idx.find(pb.key[gi]);
           const int e0 = pb.eptr[gi], e1 = pb.eptr[gi + 1];
           if (fpos >= 0) {
             led.combines += 1;
@@ -1307,6 +1342,7 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       }
       nf = std::min(nfront, f0 + chunk) - f0;
       // moves (reduction.hpp:486-496) for every state, on host threads
+      const auto hp1m = std::chrono::steady_clock::now();
       std::vector<int> vd(nf);
       std::vector<i64> kk(nf);
       {
@@ -1334,8 +1370,12 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         for (auto& e2 : errs)
           if (e2) std::rethrow_exception(e2);
       }
+      const auto hm1 = std::chrono::steady_clock::now();
+      moves_only_s_ += std::chrono::duration<double>(hm1 - hp1m).count();
       // longest chunks first, then by direction: counting sort on (k, v)
-      std::vector<int> order(nf);
+      // (the front is read in its own order and the sorted arrays written by
+      // position: sequential reads of the 40-byte states, not random ones)
+      std::vector<int> order(nf), pos(nf);
       {
         const int ndir = T.ndir;
         i64 kmx = 1;
@@ -1344,7 +1384,11 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         auto bucket = [&](size_t i) { return (size_t)(kmx - kk[i]) * ndir + vd[i]; };
         for (size_t i = 0; i < nf; ++i) ++cnt[bucket(i) + 1];
         for (size_t b = 1; b < cnt.size(); ++b) cnt[b] += cnt[b - 1];
-        for (size_t i = 0; i < nf; ++i) order[cnt[bucket(i)]++] = (int)i;
+        for (size_t i = 0; i < nf; ++i) {
+          const int o = cnt[bucket(i)]++;
+          pos[i] = o;
+          order[o] = (int)i;
+        }
       }
       std::vector<int>& hslot = cmd->hslot;
       std::vector<int>& hvdir = cmd->hvdir;
@@ -1354,12 +1398,13 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       hvdir.resize(nf);
       hu0.resize(nf * nv);
       ks.resize(nf);
-      for (size_t o = 0; o < nf; ++o) {
-        const int i = order[o];
-        hslot[o] = front[f0 + i].slot;
+      for (size_t i = 0; i < nf; ++i) {
+        const int o = pos[i];
+        const HS& h = front[f0 + i];
+        hslot[o] = h.slot;
         hvdir[o] = vd[i];
         ks[o] = kk[i];
-        for (int j = 0; j < nv; ++j) hu0[o * nv + j] = front[f0 + i].u[j];
+        for (int j = 0; j < nv; ++j) hu0[(size_t)o * nv + j] = h.u[j];
       }
       auto hp3 = std::chrono::steady_clock::now();
       for (i64 k : ks) cmd->matvecs += k;  // run_sweep: one matvec per state per step
@@ -1378,31 +1423,36 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
       std::vector<int>& fc = cmd->fc;
       std::vector<int>& fu = cmd->fu;
       std::vector<std::pair<int, int>> merges;  // (dst slot, src slot)
-      // states arrive in runs of one landing pole (sorted by k): the pole's
-      // index and list are looked up once per run
-      int lp_pole = -1;
-      FlatMap* lp_idx = nullptr;
-      std::vector<HS>* lp_lst = nullptr;
-      // landing keys first, then the inserts with the probe lines of the
-      // keys kPf positions ahead prefetched (the per-pole maps outgrow the caches)
+      // states are landed in the front's own order (sequential reads); the
+      // landing pole's index and list are looked up once per chunk length k,
+      // and the probe lines of the keys kPf states ahead are prefetched (the
+      // per-pole maps outgrow the caches)
+      i64 kmax_c = 1;
+      for (i64 k : kk) kmax_c = std::max(kmax_c, k);
+      std::vector<FlatMap*> kidx((size_t)kmax_c + 1, nullptr);
+      std::vector<std::vector<HS>*> klst((size_t)kmax_c + 1, nullptr);
+      std::vector<char> kseen((size_t)kmax_c + 1, 0);
+      for (i64 k : kk) kseen[k] = 1;
+      for (i64 k = 1; k <= kmax_c; ++k)
+        if (kseen[k] && P - (int)k != n_) {
+          kidx[k] = &landed_idx[P - (int)k];
+          klst[k] = &landed[P - (int)k];
+        }
       std::vector<u64> lkey(nf);
-      for (size_t o = 0; o < nf; ++o) {
-        const int i = order[o];
+      for (size_t i = 0; i < nf; ++i) {
         Expo u = front[f0 + i].u;
         const Expo& v = dirs_host_[vd[i]];
         for (int j = 0; j < nv; ++j) u[j] -= (int)(kk[i] * v[j]);
-        lkey[o] = key(front[f0 + i].col, u);
+        lkey[i] = key(front[f0 + i].col, u);
       }
       constexpr size_t kPf = 8;
-      for (size_t o = 0; o < nf; ++o) {
-        const int i = order[o];
-        if (o + kPf < nf && lp_idx && front[f0 + order[o + kPf]].pole - (int)kk[order[o + kPf]] == lp_pole)
-          lp_idx->prefetch(lkey[o + kPf]);
+      for (size_t i = 0; i < nf; ++i) {
+        if (i + kPf < nf && kidx[kk[i + kPf]]) kidx[kk[i + kPf]]->prefetch(lkey[i + kPf]);
         HS h = front[f0 + i];
         const Expo& v = dirs_host_[vd[i]];
         for (int j = 0; j < nv; ++j) h.u[j] -= (int)(kk[i] * v[j]);
         h.pole -= (int)kk[i];
-        const u64 kh = lkey[o];
+        const u64 kh = lkey[i];
         if (h.pole == n_) {
           fs.push_back(h.slot);
           fc.push_back(h.col);
@@ -1410,18 +1460,13 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
           floor_arrivals[h.col]++;
           floor_keys[h.col].insert(kh, 0);
         } else {
-          if (h.pole != lp_pole) {
-            lp_pole = h.pole;
-            lp_idx = &landed_idx[h.pole];
-            lp_lst = &landed[h.pole];
-          }
-          FlatMap& idx = *lp_idx;
-          std::vector<HS>& lst = *lp_lst;
-          const int pos = idx.insert(kh, (int)lst.size());
-          if (pos == (int)lst.size()) {
+          FlatMap& idx = *kidx[kk[i]];
+          std::vector<HS>& lst = *klst[kk[i]];
+          const int pos_l = idx.insert(kh, (int)lst.size());
+          if (pos_l == (int)lst.size()) {
             lst.push_back(h);
           } else {
-            merges.emplace_back(lst[pos].slot, h.slot);
+            merges.emplace_back(lst[pos_l].slot, h.slot);
             led.combines += 1;
           }
         }
@@ -1445,7 +1490,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
         host_t_[0] += sec(hp0, hp1);
         host_t_[1] += sec(hp1, hp2);
-        host_t_[2] += sec(hp2, hp3);
+        host_t_[2] += sec(hp1m, hp3);  // this chunk's moves, sort and command arrays
+        (void)hp2;
         (void)hp4;  // launch time is accounted by the launcher
         host_t_[4] += sec(hp4, hp5);
       }
@@ -1614,8 +1660,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
     }
   }
   if (std::getenv("DRZG_VERBOSE"))
-    std::fprintf(stderr, "[drzg] host s: seeds %.3f (waiting for the preparers %.3f) combine %.3f moves %.3f launch %.3f land %.3f\n",
-                 host_t_[0], prep_wait_s_, host_t_[1], host_t_[2], host_t_[3], host_t_[4]);
+    std::fprintf(stderr, "[drzg] host s: seeds %.3f (waiting for the preparers %.3f) combine %.3f moves %.3f (the moves themselves %.3f) launch %.3f land %.3f; policy thread wall %.3f\n",
+                 host_t_[0], prep_wait_s_, host_t_[1], host_t_[2], moves_only_s_, host_t_[3], host_t_[4], policy_wall_s_);
   std::vector<long long> hG(dG.n);
   DRZG_CUDA(cudaMemcpyAsync(hG.data(), dG.p, dG.n * sizeof(long long), cudaMemcpyDeviceToHost, st_));
   g_traffic.d2h += (long long)(dG.n * sizeof(long long));

@@ -374,6 +374,8 @@ class ReductionEngine {
   Stager& stager_ = *stager_owner_;
   double host_t_[5] = {0, 0, 0, 0, 0};  // host phases of run_pchunk (s)
   double prep_wait_s_ = 0;              // ... of which the policy waited for seed preparers
+  double moves_only_s_ = 0;             // ... the move choices themselves (pchunk_move)
+  double policy_wall_s_ = 0;            // the policy thread's whole run
   unsigned host_threads_ = call_cores();
   std::vector<Expo> dirs_host_;
   std::vector<int> pos_m_, pos_r_;  // system order of Homog_L rows / solution indices
