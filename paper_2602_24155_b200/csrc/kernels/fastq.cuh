@@ -70,6 +70,25 @@ struct FastQ {
     t = tq - k22;
     return (int)xp - tq * q - h;
   }
+  // The packed variant of bal_split for |x| < 2^22 and odd q <= 255: with
+  // the offset K = k22 rounded up to a multiple of 256 (x + h + qK stays below
+  // 2^32 / q), tq = floor((x + h + qK) / q) has the quotient t in its low
+  // byte (t = tq - K, K = 0 mod 256), and raw = x + h + qK - q tq in [0, q)
+  // is the digit plus h: four raws are packed and h taken off bytewise
+  // (unbias4), no per-element subtractions
+  __device__ __forceinline__ unsigned hqk256() const {
+    return (unsigned)((q >> 1) + q * (((k22 + 255) >> 8) << 8));
+  }
+  __device__ __forceinline__ int split_raw(int x, unsigned hqk, int& tq) const {
+    const unsigned xp = (unsigned)x + hqk;
+    tq = (int)__umulhi(xp, m32);
+    return (int)xp - tq * q;
+  }
+  // bytes b in [0, q) -> b - h (two's complement), no carries between bytes:
+  // b + 128 - h stays in [1, 255] for q <= 255
+  __device__ __forceinline__ uint32_t unbias4(uint32_t packed) const {
+    return (packed + 0x01010101u * (unsigned)(0x80 - (q >> 1))) ^ 0x80808080u;
+  }
   // x / q for x divisible by q, |x| < 2^22
   __device__ __forceinline__ int div_exact_fast(int x) const {
     unsigned xp = (unsigned)(x + q * k22);

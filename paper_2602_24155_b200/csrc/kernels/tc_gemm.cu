@@ -181,6 +181,20 @@ __device__ __forceinline__ void epi_carry_prefetch(const TcEpiArgs& epi, int k, 
   if (k) asm volatile("prefetch.global.L2 [%0];" ::"l"(epi.H + (size_t)m * P + nb));
 }
 
+// sign-extended byte j of w (one PRMT: a selector nibble with bit 3 set
+// replicates the sign of the selected byte)
+__device__ __forceinline__ int sbyte_prmt(uint32_t w, int j) {
+  const unsigned sel = (unsigned)(j | ((8 | j) << 4) | ((8 | j) << 8) | ((8 | j) << 12));
+  unsigned r;
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
+  return (int)r;
+}
+// the low bytes of four ints as one word (three byte permutes)
+__device__ __forceinline__ uint32_t pack4_lo(int a, int b, int c, int d) {
+  return __byte_perm(__byte_perm((uint32_t)a, (uint32_t)b, 0x0040), __byte_perm((uint32_t)c, (uint32_t)d, 0x0040),
+                     0x5410);
+}
+
 template <bool COHERENT>
 __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
                                                int cend, uint32_t tb, int cstep = 32) {
@@ -217,6 +231,38 @@ __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int 
     const int nb = n0 + c;
     if (!mok || nb >= epi.N) continue;
     uint4 o_in[2], o_h[2];
+    if (epi.fast) {
+      // r - acc = (in - acc) + q h with q | (in - acc): c = (in - acc) q^-1 + h
+      // (mod 2^32, exact), x = b_{k+1} + c; in_{k+1} = bal(x) and its
+      // quotient from one multiply-high, packed four at a time
+      const unsigned hqk = epi.fq.hqk256();
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const uint32_t low[4] = {lo[x].x, lo[x].y, lo[x].z, lo[x].w};
+        const uint32_t hiw[4] = {hi[x].x, hi[x].y, hi[x].z, hi[x].w};
+        const uint32_t b1w[4] = {b1[x].x, b1[x].y, b1[x].z, b1[x].w};
+        uint32_t in4[4], h4[4];
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4) {
+          int raw[4], tq[4];
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int inb = sbyte_prmt(low[w4], jj);
+            const int hb = k ? sbyte_prmt(hiw[w4], jj) : 0;
+            const int b1j = sbyte_prmt(b1w[w4], jj);
+            const int c = epi.fq.div_exact_inv(inb - v[16 * x + 4 * w4 + jj]) + hb;
+            raw[jj] = epi.fq.split_raw(b1j + c, hqk, tq[jj]);
+          }
+          in4[w4] = epi.fq.unbias4(pack4_lo(raw[0], raw[1], raw[2], raw[3]));
+          h4[w4] = pack4_lo(tq[0], tq[1], tq[2], tq[3]);
+        }
+        o_in[x] = make_uint4(in4[0], in4[1], in4[2], in4[3]);
+        o_h[x] = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+      }
+      st256(epi.IN + (size_t)m * P + nb, o_in[0], o_in[1]);
+      if (wh) st256(epi.H + (size_t)m * P + nb, o_h[0], o_h[1]);
+      continue;
+    }
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
       const uint32_t low[4] = {lo[x].x, lo[x].y, lo[x].z, lo[x].w};
@@ -259,15 +305,23 @@ __device__ __forceinline__ void epi_digit_tile(const TcEpiArgs& epi, int k, int 
     const int nb = n0 + c;
     if (!mok || nb >= epi.N) continue;
     uint32_t w8[8];
-    int tdrop;
+    if (epi.fast) {
+      const unsigned hqk = epi.fq.hqk256();
 #pragma unroll
-    for (int q4 = 0; q4 < 8; ++q4) {
-      uint32_t word = 0;
+      for (int q4 = 0; q4 < 8; ++q4) {
+        int raw[4], tq;
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        word |= (uint32_t)(uint8_t)(int8_t)(epi.fast ? epi.fq.bal_split(v[q4 * 4 + b], tdrop) : epi.fq.bal(v[q4 * 4 + b]))
-                << (8 * b);
-      w8[q4] = word;
+        for (int b = 0; b < 4; ++b) raw[b] = epi.fq.split_raw(v[q4 * 4 + b], hqk, tq);
+        w8[q4] = epi.fq.unbias4(pack4_lo(raw[0], raw[1], raw[2], raw[3]));
+      }
+    } else {
+#pragma unroll
+      for (int q4 = 0; q4 < 8; ++q4) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) word |= (uint32_t)(uint8_t)(int8_t)epi.fq.bal(v[q4 * 4 + b]) << (8 * b);
+        w8[q4] = word;
+      }
     }
     st256(epi.Y + ((size_t)k * epi.nLp + m) * epi.P + nb, make_uint4(w8[0], w8[1], w8[2], w8[3]),
           make_uint4(w8[4], w8[5], w8[6], w8[7]));
