@@ -195,6 +195,63 @@ __device__ __forceinline__ uint32_t pack4_lo(int a, int b, int c, int d) {
                      0x5410);
 }
 
+// balanced digits of 16 int32 accumulators as four words
+__device__ __forceinline__ void digits16(const FastQ& fq, bool fast, const int* v, uint32_t (&w4)[4]) {
+  if (fast) {
+    const unsigned hqk = fq.hqk256();
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      int raw[4], tq;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) raw[b] = fq.split_raw(v[q4 * 4 + b], hqk, tq);
+      w4[q4] = fq.unbias4(pack4_lo(raw[0], raw[1], raw[2], raw[3]));
+    }
+  } else {
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) word |= (uint32_t)(uint8_t)(int8_t)fq.bal(v[q4 * 4 + b]) << (8 * b);
+      w4[q4] = word;
+    }
+  }
+}
+// the Dixon carry of 16 elements: c = (r - acc) / q with r = in + q h (h = 0
+// when !has_h), r' = b + c stored as in' = bal(r') and h' = (r' - in') / q
+__device__ __forceinline__ void carry16(const FastQ& fq, bool fast, bool has_h, const uint32_t (&low)[4],
+                                        const uint32_t (&hiw)[4], const uint32_t (&b1w)[4], const int* v,
+                                        uint32_t (&in4)[4], uint32_t (&h4)[4]) {
+  if (fast) {
+    const unsigned hqk = fq.hqk256();
+#pragma unroll
+    for (int w4 = 0; w4 < 4; ++w4) {
+      int raw[4], tq[4];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int c = fq.div_exact_inv(sbyte_prmt(low[w4], jj) - v[4 * w4 + jj]) + (has_h ? sbyte_prmt(hiw[w4], jj) : 0);
+        raw[jj] = fq.split_raw(sbyte_prmt(b1w[w4], jj) + c, hqk, tq[jj]);
+      }
+      in4[w4] = fq.unbias4(pack4_lo(raw[0], raw[1], raw[2], raw[3]));
+      h4[w4] = pack4_lo(tq[0], tq[1], tq[2], tq[3]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int w4 = 0; w4 < 4; ++w4) {
+    in4[w4] = h4[w4] = 0;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int r = sbyte_prmt(low[w4], jj) + (has_h ? fq.q * sbyte_prmt(hiw[w4], jj) : 0);
+      int rem, inb;
+      const int cnew = fq.divfloor(r - v[4 * w4 + jj], rem);  // exact
+      int hq = fq.divfloor(sbyte_prmt(b1w[w4], jj) + cnew, inb);
+      if (inb > (fq.q >> 1)) inb -= fq.q, ++hq;
+      in4[w4] |= (uint32_t)(uint8_t)(int8_t)inb << (8 * jj);
+      h4[w4] |= (uint32_t)(uint8_t)(int8_t)hq << (8 * jj);
+    }
+  }
+}
+
 template <bool COHERENT>
 __device__ __forceinline__ void epi_carry_tile(const TcEpiArgs& epi, int k, int m, bool mok, int n0, int cbeg,
                                                int cend, uint32_t tb, int cstep = 32) {
@@ -1204,17 +1261,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
             for (int c2 = 0; c2 < PER; ++c2) {
               const int ch = hh * PER + c2;
               uint32_t w4[4];
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                uint32_t word = 0;
-#pragma unroll
-                for (int bb = 0; bb < 4; ++bb) {
-                  const int x = v[c2 * 16 + q4 * 4 + bb];
-                  int tdrop;
-                  word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_split(x, tdrop) : fa.fq.bal(x)) << (8 * bb);
-                }
-                w4[q4] = word;
-              }
+              digits16(fa.fq, fa.fast, v + c2 * 16, w4);
               const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
               if (carry) *reinterpret_cast<uint4*>(sY + swz<NS>(m, half * (NS / 2) + ch * 16)) = y4;
               if (fa.chunk)
@@ -1251,26 +1298,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
               const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
               const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
               const uint32_t b1w[4] = {b1[ch].x, b1[ch].y, b1[ch].z, b1[ch].w};
-              uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const int sh = 8 * (j & 3);
-                const int r = (int)(int8_t)(low[j >> 2] >> sh) + fa.q * (int)(int8_t)(hiw[j >> 2] >> sh);
-                const int b1j = (int)(int8_t)(b1w[j >> 2] >> sh);
-                const int x = v[c2 * 16 + j];
-                int cnew, inb, hq;
-                if (fa.fast) {
-                  cnew = fa.fq.div_exact_inv(r - x);
-                  inb = fa.fq.bal_split(b1j + cnew, hq);
-                } else {
-                  int rem;
-                  cnew = fa.fq.divfloor(r - x, rem);
-                  hq = fa.fq.divfloor(b1j + cnew, inb);
-                  if (inb > (fa.q >> 1)) inb -= fa.q, ++hq;
-                }
-                in4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
-                h4[j >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
-              }
+              uint32_t in4[4], h4[4];
+              carry16(fa.fq, fa.fast, k != 0, low, hiw, b1w, v + c2 * 16, in4, h4);
               *reinterpret_cast<uint4*>(sIn + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
               *reinterpret_cast<uint4*>(sH + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
             }
@@ -1484,17 +1513,7 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
               for (int c2 = 0; c2 < PER; ++c2) {
                 const int ch = hh * PER + c2;
                 uint32_t w4[4];
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                  uint32_t word = 0;
-#pragma unroll
-                  for (int bb = 0; bb < 4; ++bb) {
-                    const int x = v[c2 * 16 + q4 * 4 + bb];
-                    int tdrop;
-                    word |= (uint32_t)(uint8_t)(int8_t)(fa.fast ? fa.fq.bal_split(x, tdrop) : fa.fq.bal(x)) << (8 * bb);
-                  }
-                  w4[q4] = word;
-                }
+                digits16(fa.fq, fa.fast, v + c2 * 16, w4);
                 const uint4 y4 = make_uint4(w4[0], w4[1], w4[2], w4[3]);
                 if (carry) *reinterpret_cast<uint4*>(sY[p] + swz<NS>(m, half * (NS / 2) + ch * 16)) = y4;
                 if (m < fa.nL && n0 + ch * 16 < fa.N) *reinterpret_cast<uint4*>(yg + ch * 16) = y4;
@@ -1531,26 +1550,8 @@ __global__ void __launch_bounds__(fz::THREADS, 1)
                 const uint32_t low[4] = {lo.x, lo.y, lo.z, lo.w};
                 const uint32_t hiw[4] = {hi.x, hi.y, hi.z, hi.w};
                 const uint32_t b1w[4] = {b1[p][ch].x, b1[p][ch].y, b1[p][ch].z, b1[p][ch].w};
-                uint32_t in4[4] = {0, 0, 0, 0}, h4[4] = {0, 0, 0, 0};
-#pragma unroll
-                for (int jj = 0; jj < 16; ++jj) {
-                  const int sh = 8 * (jj & 3);
-                  const int r = (int)(int8_t)(low[jj >> 2] >> sh) + fa.q * (int)(int8_t)(hiw[jj >> 2] >> sh);
-                  const int b1j = (int)(int8_t)(b1w[jj >> 2] >> sh);
-                  const int x = v[c2 * 16 + jj];
-                  int cnew, inb, hq;
-                  if (fa.fast) {
-                    cnew = fa.fq.div_exact_inv(r - x);
-                    inb = fa.fq.bal_split(b1j + cnew, hq);
-                  } else {
-                    int rem;
-                    cnew = fa.fq.divfloor(r - x, rem);
-                    hq = fa.fq.divfloor(b1j + cnew, inb);
-                    if (inb > (fa.q >> 1)) inb -= fa.q, ++hq;
-                  }
-                  in4[jj >> 2] |= (uint32_t)(uint8_t)(int8_t)inb << sh;
-                  h4[jj >> 2] |= (uint32_t)(uint8_t)(int8_t)hq << sh;
-                }
+                uint32_t in4[4], h4[4];
+                carry16(fa.fq, fa.fast, k != 0, low, hiw, b1w, v + c2 * 16, in4, h4);
                 *reinterpret_cast<uint4*>(sIn[p] + off) = make_uint4(in4[0], in4[1], in4[2], in4[3]);
                 *reinterpret_cast<uint4*>(sH[p] + off) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
               }
