@@ -1568,9 +1568,8 @@ void ReductionEngine::run_pchunk(std::vector<ColumnSeeds>& cols, std::vector<std
         d_mp.stage(cmd->gptr, stager_, st_);
         d_mm.stage(cmd->mem, stager_, st_);
         const size_t ng = cmd->gptr.size() - 1;
-        dim3 gm((unsigned)((T.side + 127) / 128) * ng);
         timed(&clock.other_ms, [&] {
-          dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, Ld, T.dp.q, d_mp.p, d_mm.p);
+          dev::launch_merge(pool_, slot_stride_, T.side, sidep_, Ld, FastQ::make(T.dp.q), d_mp.p, d_mm.p, (int)ng, st_);
         });
       }
       if (!cmd->fs.empty()) {
@@ -1848,9 +1847,8 @@ void ReductionEngine::combine_live(std::vector<Live>& sts, Ledger& led) {
     dp.upload(gptr, st_);
     dm.upload(mem, st_);
     const size_t ng = gptr.size() - 1;
-    dim3 gm((unsigned)((T.side + 127) / 128) * ng);
     timed(&clock.other_ms, [&] {
-      dev::merge_kernel<<<gm, 128, 0, st_>>>(pool_, slot_stride_, T.side, sidep_, T.dp.Ld, T.dp.q, dp.p, dm.p);
+      dev::launch_merge(pool_, slot_stride_, T.side, sidep_, T.dp.Ld, FastQ::make(T.dp.q), dp.p, dm.p, (int)ng, st_);
     });
     DRZG_CUDA(cudaGetLastError());
     DRZG_CUDA(cudaStreamSynchronize(st_));

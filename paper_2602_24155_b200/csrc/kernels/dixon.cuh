@@ -561,6 +561,81 @@ __global__ void merge_kernel(int8_t* pool, long long slot_stride, int side, int 
   }
 }
 
+// the same merge with four side rows per thread (one 32-bit word of each
+// member's plane per load: 128-byte warp accesses) and the digit planes in
+// registers (LD a compile-time count); the multiply-high balanced division
+// applies while |sum| < 2^22, i.e. up to 2^14 members a group (more: exact
+// 64-bit division)
+template <int LD>
+__global__ void __launch_bounds__(128) merge4_kernel(int8_t* pool, long long slot_stride, int side, int sidep, FastQ fq,
+                                                     const int* gptr, const int* members) {
+  const int words = (side + 3) / 4;
+  const int nrb = (words + blockDim.x - 1) / blockDim.x;
+  const int grp = blockIdx.x / nrb;
+  const int wi = (blockIdx.x % nrb) * blockDim.x + threadIdx.x;
+  if (wi >= words) return;
+  const int m0 = gptr[grp], m1 = gptr[grp + 1];
+  int acc[LD][4];
+#pragma unroll
+  for (int t = 0; t < LD; ++t)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[t][j] = 0;
+  for (int m = m0; m < m1; ++m) {
+    const int8_t* w = pool + (size_t)members[m] * slot_stride + 4 * (size_t)wi;
+    uint32_t wd[LD];
+#pragma unroll
+    for (int t = 0; t < LD; ++t) wd[t] = *reinterpret_cast<const uint32_t*>(w + (size_t)t * sidep);
+#pragma unroll
+    for (int t = 0; t < LD; ++t)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[t][j] += sbyte(wd[t], j);
+  }
+  int8_t* out = pool + (size_t)members[m0] * slot_stride + 4 * (size_t)wi;
+  const bool fast = m1 - m0 <= (1 << 14);
+  int carry[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int t = 0; t < LD; ++t) {
+    int dg[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int v2 = acc[t][j] + carry[j];
+      if (fast) {
+        dg[j] = fq.balq(v2, carry[j]);
+      } else {
+        int r;
+        int qt = fq.divfloor(v2, r);
+        if (r > (fq.q >> 1)) r -= fq.q, ++qt;
+        dg[j] = r;
+        carry[j] = qt;
+      }
+    }
+    *reinterpret_cast<uint32_t*>(out + (size_t)t * sidep) =
+        __byte_perm(__byte_perm((uint32_t)dg[0], (uint32_t)dg[1], 0x0040), __byte_perm((uint32_t)dg[2], (uint32_t)dg[3], 0x0040),
+                    0x5410);
+  }
+}
+// combine_states over `ngroups` groups of slots (CSR gptr/members): the
+// register version for Ld <= 16, else the plane loop
+inline void launch_merge(int8_t* pool, long long slot_stride, int side, int sidep, int Ld, const FastQ& fq,
+                         const int* gptr, const int* members, int ngroups, cudaStream_t st) {
+  const int words = (side + 3) / 4;
+  const dim3 g4((unsigned)((words + 127) / 128) * ngroups);
+  switch (Ld) {
+#define DRZG_MERGE_CASE(L) \
+  case L:                  \
+    merge4_kernel<L><<<g4, 128, 0, st>>>(pool, slot_stride, side, sidep, fq, gptr, members); \
+    return;
+    DRZG_MERGE_CASE(1) DRZG_MERGE_CASE(2) DRZG_MERGE_CASE(3) DRZG_MERGE_CASE(4) DRZG_MERGE_CASE(5) DRZG_MERGE_CASE(6)
+    DRZG_MERGE_CASE(7) DRZG_MERGE_CASE(8) DRZG_MERGE_CASE(9) DRZG_MERGE_CASE(10) DRZG_MERGE_CASE(11) DRZG_MERGE_CASE(12)
+    DRZG_MERGE_CASE(13) DRZG_MERGE_CASE(14) DRZG_MERGE_CASE(15) DRZG_MERGE_CASE(16)
+#undef DRZG_MERGE_CASE
+    default:
+      break;
+  }
+  const dim3 gm((unsigned)((side + 127) / 128) * ngroups);
+  merge_kernel<<<gm, 128, 0, st>>>(pool, slot_stride, side, sidep, Ld, fq.q, gptr, members);
+}
+
 // floor: G[col][t][rank(mon_g + u - 1)] += w[t][g]; mon table is side x nv
 __global__ void floor_kernel(const int8_t* pool, long long slot_stride, int side, int sidep, int Ld, int nv,
                              const int* slot, const int* col, const int* u, const int* mon, const unsigned long long* btab,
