@@ -874,7 +874,7 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
       mv += By;
       const int Bn = count_ge(y + 1);
       if (Bn < By) {
-        dim3 gF((By - Bn + dev::kFlushStates - 1) / dev::kFlushStates, (T.side + dev::kFlushRows - 1) / dev::kFlushRows);
+        dim3 gF((By - (Bn & ~3) + dev::kFlushStates - 1) / dev::kFlushStates, (T.side + dev::kFlushRows - 1) / dev::kFlushRows);
         size_t fsm = (size_t)T.dp.Ld * dev::kFlushRows * dev::kFlushStates;
         timed(&clock.epi_ms, [&] { dev::flush_kernel<<<gF, 256, fsm, st_>>>(a, Bn, By); });
       }

@@ -477,28 +477,41 @@ inline void launch_epilogue(const StepArgs& a, dim3 grid, cudaStream_t st) {
 // W -> slot pool for the batch columns [s_lo, s_hi) whose chunk ends here:
 // 32 states x 64 side rows per block, transposed through shared memory
 __global__ void __launch_bounds__(256) flush_kernel(StepArgs a, int s_lo, int s_hi) {
-  extern __shared__ int8_t ft[];  // Ld x kFlushRows x kFlushStates
-  const int g0 = blockIdx.y * kFlushRows, s0 = s_lo + blockIdx.x * kFlushStates;
+  // the block's 32 states start at a multiple of 4 at or below s_lo (word
+  // loads); states below s_lo continue their chunk and are not written
+  extern __shared__ __align__(16) int8_t ft[];  // Ld x kFlushRows x kFlushStates: [t][g][state]
+  const int g0 = blockIdx.y * kFlushRows, s0 = (s_lo & ~3) + blockIdx.x * kFlushStates;
   const size_t wplane = (size_t)a.sidep * a.P;
-  for (int e = threadIdx.x; e < a.Ld * kFlushRows * kFlushStates; e += 256) {
-    int sl = e % kFlushStates, gl = (e / kFlushStates) % kFlushRows, t = e / (kFlushStates * kFlushRows);
-    int g = g0 + gl, s = s0 + sl;
-    ft[e] = (g < a.side && s < s_hi) ? a.W[(size_t)t * wplane + (size_t)g * a.P + s] : (int8_t)0;
+  // W -> shared: one 4-state word per load (a warp reads 4 rows of 32 states)
+  for (int e = threadIdx.x; e < a.Ld * kFlushRows * (kFlushStates / 4); e += 256) {
+    const int sq = e % (kFlushStates / 4), gl = (e / (kFlushStates / 4)) % kFlushRows,
+              t = e / ((kFlushStates / 4) * kFlushRows);
+    const int g = g0 + gl, s = s0 + 4 * sq;
+    uint32_t wd = 0;
+    if (g < a.side && s < a.P) wd = *reinterpret_cast<const uint32_t*>(a.W + (size_t)t * wplane + (size_t)g * a.P + s);
+    reinterpret_cast<uint32_t*>(ft)[e] = wd;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;  // lane = state
-  const int s = s0 + lane;
-  if (s >= s_hi) return;
-  int8_t* dst = a.pool + (size_t)a.slot[s] * a.slot_stride;
-  for (int t = grp; t < a.Ld; t += 8) {
-    for (int w = 0; w < kFlushRows / 4; ++w) {
-      int g = g0 + w * 4;
-      if (g >= a.side) break;
-      uint32_t word = 0;
+  // shared -> slots: a thread takes 4 side rows x 4 states, transposes them
+  // (4 x 4 bytes) and writes each state's 4 rows as one word; a warp writes 16
+  // consecutive words (64 bytes) of a slot row per state
+  for (int e = threadIdx.x; e < a.Ld * (kFlushRows / 4) * (kFlushStates / 4); e += 256) {
+    const int g4 = e % (kFlushRows / 4), sq = (e / (kFlushRows / 4)) % (kFlushStates / 4),
+              t = e / ((kFlushRows / 4) * (kFlushStates / 4));
+    const int g = g0 + 4 * g4;
+    if (g >= a.side) continue;
+    const uint32_t* rows = reinterpret_cast<const uint32_t*>(ft) + ((size_t)t * kFlushRows + 4 * g4) * (kFlushStates / 4) + sq;
+    const uint32_t w0 = rows[0], w1 = rows[kFlushStates / 4], w2 = rows[2 * (kFlushStates / 4)],
+                   w3 = rows[3 * (kFlushStates / 4)];
+    const uint32_t lo01 = __byte_perm(w0, w1, 0x5140), hi01 = __byte_perm(w0, w1, 0x7362);
+    const uint32_t lo23 = __byte_perm(w2, w3, 0x5140), hi23 = __byte_perm(w2, w3, 0x7362);
+    const uint32_t st4[4] = {__byte_perm(lo01, lo23, 0x5410), __byte_perm(lo01, lo23, 0x7632),
+                             __byte_perm(hi01, hi23, 0x5410), __byte_perm(hi01, hi23, 0x7632)};
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        word |= (uint32_t)(uint8_t)ft[((size_t)t * kFlushRows + w * 4 + b) * kFlushStates + lane] << (8 * b);
-      *reinterpret_cast<uint32_t*>(dst + (size_t)t * a.sidep + g) = word;
+    for (int j = 0; j < 4; ++j) {
+      const int s = s0 + 4 * sq + j;
+      if (s < s_lo || s >= s_hi) continue;
+      *reinterpret_cast<uint32_t*>(a.pool + (size_t)a.slot[s] * a.slot_stride + (size_t)t * a.sidep + g) = st4[j];
     }
   }
 }
