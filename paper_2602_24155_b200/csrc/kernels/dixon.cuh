@@ -72,24 +72,37 @@ __global__ void __launch_bounds__(kGatherThreads) gather_kernel(StepArgs a) {
     // transposing load: a lane takes rows 4 g4 .. 4 g4 + 3 of four states
     // (one quad), 4 x 4 bytes, and stores them as four words of [g][state];
     // a warp reads 32 contiguous bytes of each of its 4 quads' 16 states
-    for (int e = tid; e < groups * 32 * 2; e += kGatherThreads) {
-      const int qh = e / (groups * 32), rest = e - qh * groups * 32;
-      const int gq = rest >> 5, lane = rest & 31;
-      const int g4 = gq * 8 + (lane >> 2), q = (lane & 3) + 4 * qh;
-      if (g4 >= words) continue;
-      uint32_t w[4];
+    // (kGU work items per thread per pass: their 4 kGU loads are all in
+    // flight before any is used -- the phase is latency-bound otherwise)
+    constexpr int kGU = 4;
+    const int nitems = groups * 32 * 2;
+    for (int e0 = tid; e0 < nitems; e0 += kGatherThreads * kGU) {
+      uint32_t w[kGU][4];
+      int g4s[kGU], qs[kGU];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const long long bs = base[q * 4 + k];
-        w[k] = bs >= 0 ? __ldg(reinterpret_cast<const uint32_t*>(a.pool + bs + (size_t)t * sidep) + g4) : 0u;
+      for (int u = 0; u < kGU; ++u) {
+        const int e = e0 + u * kGatherThreads;
+        const int qh = e / (groups * 32), rest = e - qh * groups * 32;
+        const int gq = rest >> 5, lane = rest & 31;
+        g4s[u] = e < nitems ? gq * 8 + (lane >> 2) : words;
+        qs[u] = (lane & 3) + 4 * qh;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const long long bs = g4s[u] < words ? base[qs[u] * 4 + k] : -1;
+          w[u][k] = bs >= 0 ? __ldg(reinterpret_cast<const uint32_t*>(a.pool + bs + (size_t)t * sidep) + g4s[u]) : 0u;
+        }
       }
-      const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140), hi01 = __byte_perm(w[0], w[1], 0x7362);
-      const uint32_t lo23 = __byte_perm(w[2], w[3], 0x5140), hi23 = __byte_perm(w[2], w[3], 0x7362);
-      int8_t* dst = planes + (size_t)(4 * g4) * kGatherPitch + 4 * q;
-      *reinterpret_cast<uint32_t*>(dst) = __byte_perm(lo01, lo23, 0x5410);
-      *reinterpret_cast<uint32_t*>(dst + kGatherPitch) = __byte_perm(lo01, lo23, 0x7632);
-      *reinterpret_cast<uint32_t*>(dst + 2 * kGatherPitch) = __byte_perm(hi01, hi23, 0x5410);
-      *reinterpret_cast<uint32_t*>(dst + 3 * kGatherPitch) = __byte_perm(hi01, hi23, 0x7632);
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        if (g4s[u] >= words) continue;
+        const uint32_t lo01 = __byte_perm(w[u][0], w[u][1], 0x5140), hi01 = __byte_perm(w[u][0], w[u][1], 0x7362);
+        const uint32_t lo23 = __byte_perm(w[u][2], w[u][3], 0x5140), hi23 = __byte_perm(w[u][2], w[u][3], 0x7362);
+        int8_t* dst = planes + (size_t)(4 * g4s[u]) * kGatherPitch + 4 * qs[u];
+        *reinterpret_cast<uint32_t*>(dst) = __byte_perm(lo01, lo23, 0x5410);
+        *reinterpret_cast<uint32_t*>(dst + kGatherPitch) = __byte_perm(lo01, lo23, 0x7632);
+        *reinterpret_cast<uint32_t*>(dst + 2 * kGatherPitch) = __byte_perm(hi01, hi23, 0x5410);
+        *reinterpret_cast<uint32_t*>(dst + 3 * kGatherPitch) = __byte_perm(hi01, hi23, 0x7632);
+      }
     }
     __syncthreads();
     const int uv = uniform_v;
