@@ -119,7 +119,7 @@ std::string frob_json_body(const FrobResult& fr) {
      << ",\"times\":{\"tables\":" << fr.t.tables << ",\"seeds\":" << fr.t.seeds << ",\"device\":" << fr.t.device
      << ",\"final\":" << fr.t.final << ",\"total\":" << fr.t.total << "}"
      << ",\"kernels\":{\"gemm_ms\":" << fr.clk.gemm_ms << ",\"carry_ms\":" << fr.clk.carry_ms
-     << ",\"gather_ms\":" << fr.clk.gather_ms << ",\"epilogue_ms\":" << fr.clk.epi_ms
+     << ",\"gather_ms\":" << fr.clk.gather_ms << ",\"epilogue_ms\":" << fr.clk.epi_ms << ",\"flush_ms\":" << fr.clk.flush_ms
      << ",\"other_ms\":" << fr.clk.other_ms << ",\"gemm_launches\":" << fr.clk.gemm_launches
      << ",\"gemm_macs\":" << fr.clk.gemm_macs << ",\"carry_launches\":" << fr.clk.carry_launches
      << ",\"carry_macs\":" << fr.clk.carry_macs << ",\"device_ms\":" << fr.clk.device_ms << ",\"peak_live_states\":" << fr.clk.peak_live << "}"

@@ -846,7 +846,9 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
       chunk_steps_ = 0;
       dim3 gF((nb + dev::kFlushStates - 1) / dev::kFlushStates, (T.side + dev::kFlushRows - 1) / dev::kFlushRows);
       size_t fsm = (size_t)T.dp.Ld * dev::kFlushRows * dev::kFlushStates;
+      const double e0f = clock.epi_ms;
       timed(&clock.epi_ms, [&] { dev::flush_kernel<<<gF, 256, fsm, st_>>>(a, 0, nb); });
+      clock.flush_ms += clock.epi_ms - e0f;
       DRZG_CUDA(cudaGetLastError());
       mv += steps;
       continue;
@@ -876,7 +878,9 @@ i64 ReductionEngine::run_sweep(const std::vector<i64>& ks) {
       if (Bn < By) {
         dim3 gF((By - (Bn & ~3) + dev::kFlushStates - 1) / dev::kFlushStates, (T.side + dev::kFlushRows - 1) / dev::kFlushRows);
         size_t fsm = (size_t)T.dp.Ld * dev::kFlushRows * dev::kFlushStates;
+        const double e0f = clock.epi_ms;
         timed(&clock.epi_ms, [&] { dev::flush_kernel<<<gF, 256, fsm, st_>>>(a, Bn, By); });
+        clock.flush_ms += clock.epi_ms - e0f;
       }
       By = Bn;
       DRZG_CUDA(cudaGetLastError());

@@ -87,6 +87,7 @@ struct Ledger {
 struct KernelClock {
   bool on = false;
   double gemm_ms = 0, carry_ms = 0, gather_ms = 0, epi_ms = 0, other_ms = 0;
+  double flush_ms = 0;  // of epi_ms: the chunk-end W -> slot transposes
   i64 gemm_launches = 0;
   double device_ms = 0;  // CUDA-event time of the whole device-resident run
   i64 peak_live = 0;     // most state slots live at once
