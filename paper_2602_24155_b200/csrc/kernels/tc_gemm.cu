@@ -715,11 +715,14 @@ __device__ __forceinline__ uint64_t sw128_mn_desc_1atom(uint32_t addr) {
 // leader's tempty barrier.  Each CTA drains its own TMEM lanes (its 128 rows,
 // all 256 states).  Carry tiles run over the union of the two 128-row tiles'
 // nonzero K blocks.
+#ifndef DRZG_F2_EPI_WARPS
+#define DRZG_F2_EPI_WARPS 12
+#endif
 namespace f2 {
 // 12 epilogue warps (3 per TMEM lane quarter, each a third of the 256 state
 // columns): the epilogues, not the MMAs, bound the dataflow solve, and 2
 // epilogue warps per scheduler could not hide their latencies
-constexpr int EPI_WARPS = 12;
+constexpr int EPI_WARPS = DRZG_F2_EPI_WARPS;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr int STAGES = 6;
 constexpr int A_BYTES = BM * BK;        // 16 KB: this CTA's 128 rows
