@@ -1796,10 +1796,8 @@ void dixon_fused(const int8_t* C, const int8_t* Jd, const FusedArgs& fa, cudaStr
   const int ns = fa.chunk ? 32 : ns_env ? std::atoi(ns_env) : (fa.N <= 32 * sms ? 32 : 64);
   // two 64-state blocks in flight per CTA once every CTA has two or more
   // (DRZG_FUSED_PP=0 keeps one block per CTA)
-  static const bool pp_on = [] {
-    const char* e = std::getenv("DRZG_FUSED_PP");
-    return !(e && std::string(e) == "0");
-  }();
+  const char* pp_env = std::getenv("DRZG_FUSED_PP");  // per launch: the path tests switch it
+  const bool pp_on = !(pp_env && std::string(pp_env) == "0");
   if (pp_on && !fa.chunk && !ns_env && fa.N >= 2 * 64 * sms &&
       tc::fz::smem_bytes_pp(fa.nLp / 128, 64) <= 227 * 1024) {
     launch_fused_pp<64>(mc, mj, fa, sms, st);

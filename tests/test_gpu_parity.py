@@ -125,6 +125,9 @@ PATH_ENVS = [
     {"DRZG_FUSED_NS": "32"},
     {"DRZG_FUSED_NS": "64"},
     {"DRZG_FUSED_NS": "128"},
+    {"DRZG_FUSED_PP": "0"},          # one block per CTA in the large one-launch solves
+    {"DRZG_CHUNK": "1"},             # whole chunks in one launch, T_x in the CTA
+    {"DRZG_FLOW2": "0"},             # the single-CTA dataflow kernel
     {"DRZG_FUSED": "0", "DRZG_FLOW": "0"},
     {"DRZG_FUSED": "0", "DRZG_FLOW": "0", "DRZG_SPARSE_CARRY": "0"},
     {"DRZG_GEMM": "dp4a"},
