@@ -1,5 +1,6 @@
 // Device-resident reduction engine (see engine.cuh).
 #include <algorithm>
+#include <tuple>
 #include <functional>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -93,26 +94,47 @@ SysOrder order_system(const RuvTables& T, bool search, bool group_tx) {
   for (int i = 0; i < nL; ++i) best.pos_m[i] = best.pos_r[i] = i;
   best.blocks = blocks_of(best.pos_m, best.pos_r).first;
   if (search) {
+    // every variable order (and its reverse) scored on host threads (the
+    // fourfold's 1440 candidates took ~0.5 s on one); the first best in
+    // enumeration order wins, as it did sequentially
     const auto& Lm = monos(nv, T.L).mons;
-    std::vector<int> vp(nv);
-    for (int i = 0; i < nv; ++i) vp[i] = i;
-    do {
-      for (int sgn = -1; sgn <= 1; sgn += 2) {
-        std::vector<double> key(nL);
-        for (int m = 0; m < nL; ++m) {
-          double k = 0;
-          for (int i = 0; i < nv; ++i) k = k * 64 + sgn * Lm[m][vp[i]];
-          key[m] = k;
-        }
-        std::vector<int> pm = sort_pos(key), pr = col_pos(pm);
-        long long nb = blocks_of(pm, pr).first;
-        if (nb < best.blocks) {
-          best.blocks = nb;
-          best.pos_m = std::move(pm);
-          best.pos_r = std::move(pr);
-        }
+    std::vector<std::vector<int>> perms;
+    {
+      std::vector<int> vp(nv);
+      for (int i = 0; i < nv; ++i) vp[i] = i;
+      do perms.push_back(vp);
+      while (std::next_permutation(vp.begin(), vp.end()));
+    }
+    const int ncand = 2 * (int)perms.size();
+    std::vector<long long> score(ncand);
+    auto eval = [&](int c) {
+      const std::vector<int>& vp = perms[c / 2];
+      const int sgn = (c & 1) ? 1 : -1;
+      std::vector<double> key(nL);
+      for (int m = 0; m < nL; ++m) {
+        double k = 0;
+        for (int i = 0; i < nv; ++i) k = k * 64 + sgn * Lm[m][vp[i]];
+        key[m] = k;
       }
-    } while (std::next_permutation(vp.begin(), vp.end()));
+      std::vector<int> pm = sort_pos(key), pr = col_pos(pm);
+      return std::make_tuple(blocks_of(pm, pr).first, std::move(pm), std::move(pr));
+    };
+    const int nth = std::max(1, std::min<int>((int)call_cores(), ncand / 8));
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nth; ++t)
+      pool.emplace_back([&, t] {
+        for (int c = t; c < ncand; c += nth) score[c] = std::get<0>(eval(c));
+      });
+    for (auto& th : pool) th.join();
+    int bestc = -1;
+    for (int c = 0; c < ncand; ++c)
+      if (score[c] < best.blocks && (bestc < 0 || score[c] < score[bestc])) bestc = c;
+    if (bestc >= 0) {
+      auto r = eval(bestc);
+      best.blocks = std::get<0>(r);
+      best.pos_m = std::move(std::get<1>(r));
+      best.pos_r = std::move(std::get<2>(r));
+    }
   }
   if (group_tx) {
     // solution indices feeding one side row made adjacent (each r feeds
