@@ -965,6 +965,28 @@ __global__ void __launch_bounds__(f2::THREADS, 1)
           if (v[0] == 0x7fffffff) fa.counters[0] = v[1];  // keep the loads
         }
       } else if (fa.debug == 2) {
+      } else if (fa.debug == 3) {
+        // the epilogue arithmetic without its global memory (inputs zero,
+        // results kept alive): separates the two costs
+        uint32_t sink = 0;
+        for (int c = cbeg; c < BN; c += cstep) {
+          int v[32];
+          tmem_ld32(tb + (uint32_t)c, v);
+#pragma unroll
+          for (int x = 0; x < 2; ++x) {
+            if (digit) {
+              uint32_t w4[4];
+              digits16(epi.fq, epi.fast, v + 16 * x, w4);
+              sink ^= w4[0] ^ w4[1] ^ w4[2] ^ w4[3];
+            } else {
+              const uint32_t z[4] = {0, 0, 0, 0};
+              uint32_t in4[4], h4[4];
+              carry16(epi.fq, epi.fast, k != 0, z, z, z, v + 16 * x, in4, h4);
+              sink ^= in4[0] ^ in4[1] ^ in4[2] ^ in4[3] ^ h4[0] ^ h4[1] ^ h4[2] ^ h4[3];
+            }
+          }
+        }
+        if (sink == 0x12345678u) fa.counters[0] = (int)sink;
       } else if (digit)
         epi_digit_tile(epi, k, m, mok, n0, cbeg, BN, tb, cstep);
       else
