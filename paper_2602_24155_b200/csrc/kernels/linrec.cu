@@ -58,23 +58,70 @@ __device__ __forceinline__ U192 shfl_down192(const U192& v, int off) {
   return r;
 }
 
-// v / beta and v % beta for a 192-bit v and 64-bit beta
-__device__ __forceinline__ unsigned long long divmod192(U192& v, unsigned long long beta) {
-  unsigned __int128 cur = v.w2;
-  unsigned long long q2 = (unsigned long long)(cur / beta);
-  cur = ((cur % beta) << 64) | v.w1;
-  unsigned long long q1 = (unsigned long long)(cur / beta);
-  cur = ((cur % beta) << 64) | v.w0;
-  unsigned long long q0 = (unsigned long long)(cur / beta);
-  unsigned long long r = (unsigned long long)(cur % beta);
-  v.w2 = q2;
-  v.w1 = q1;
-  v.w0 = q0;
-  return r;
+// Division by a per-call constant with a precomputed reciprocal (Moller and
+// Granlund's 2-by-1 division, "Improved division by invariant integers",
+// 2011): the divisor normalised to dn = d << s (top bit set) and
+// v = floor((2^128 - 1) / dn) - 2^64, computed once on the host.  A 128-by-64
+// step is two multiplies and two corrections instead of a software 128-bit
+// division; the per-row digit normalisation is a serial chain of these.
+struct Div64 {
+  unsigned long long dn, v;
+  int s;
+};
+
+inline Div64 make_div64(unsigned long long d) {
+  Div64 D{};
+  D.s = __builtin_clzll(d);
+  D.dn = d << D.s;
+  const unsigned __int128 all = ~(unsigned __int128)0;
+  D.v = (unsigned long long)(all / D.dn - ((unsigned __int128)1 << 64));
+  return D;
+}
+
+// (u1, u0) = q dn + r for u1 < dn; returns q, r through rr
+__device__ __forceinline__ unsigned long long div2by1(unsigned long long u1, unsigned long long u0, const Div64& D,
+                                                      unsigned long long& rr) {
+  unsigned long long q0 = D.v * u1, q1 = __umul64hi(D.v, u1);
+  q0 += u0;
+  q1 += u1 + (q0 < u0 ? 1ull : 0ull);
+  q1 += 1;
+  unsigned long long r = u0 - q1 * D.dn;
+  if (r > q0) {
+    q1 -= 1;
+    r += D.dn;
+  }
+  if (r >= D.dn) {
+    q1 += 1;
+    r -= D.dn;
+  }
+  rr = r;
+  return q1;
+}
+
+// v / d and v % d for a 192-bit v (v <- quotient; the remainder returned)
+__device__ __forceinline__ unsigned long long divmod192(U192& v, const Div64& D) {
+  const int s = D.s;
+  const unsigned long long n3 = s ? v.w2 >> (64 - s) : 0ull;
+  const unsigned long long n2 = s ? (v.w2 << s) | (v.w1 >> (64 - s)) : v.w2;
+  const unsigned long long n1 = s ? (v.w1 << s) | (v.w0 >> (64 - s)) : v.w1;
+  const unsigned long long n0 = v.w0 << s;
+  unsigned long long r = n3;
+  v.w2 = div2by1(r, n2, D, r);
+  v.w1 = div2by1(r, n1, D, r);
+  v.w0 = div2by1(r, n0, D, r);
+  return r >> s;
+}
+
+// x mod d for a 64-bit x
+__device__ __forceinline__ unsigned long long mod64(unsigned long long x, const Div64& D) {
+  const int s = D.s;
+  unsigned long long r;
+  div2by1(s ? x >> (64 - s) : 0ull, x << s, D, r);
+  return r >> s;
 }
 
 // canonical base-beta digits of sum_s beta^s acc[s] mod p^M
-__device__ __forceinline__ void normalise(U192* acc, int limbs, unsigned long long beta, unsigned long long top_mod,
+__device__ __forceinline__ void normalise(U192* acc, int limbs, const Div64& beta, const Div64& top_mod,
                                           unsigned long long* out) {
   U192 carry{0, 0, 0};
   for (int s = 0; s < limbs; ++s) {
@@ -83,7 +130,7 @@ __device__ __forceinline__ void normalise(U192* acc, int limbs, unsigned long lo
     out[s] = divmod192(v, beta);
     carry = v;
   }
-  out[limbs - 1] %= top_mod;
+  out[limbs - 1] = mod64(out[limbs - 1], top_mod);
 }
 
 struct LinrecArgs {
@@ -92,7 +139,7 @@ struct LinrecArgs {
   const unsigned long long* w;  // limbs x side (input of this factor)
   unsigned long long* y;        // limbs x side (output)
   int side, limbs;
-  unsigned long long beta, top_mod;
+  Div64 beta, top_mod;          // base and top-digit modulus, preinverted
   unsigned long long t;         // factor index
   // CSR variant
   const int* a_ptr;
@@ -104,7 +151,7 @@ struct LinrecArgs {
 };
 
 template <int L>
-__device__ __forceinline__ void normalise_t(U192 (&acc)[L], unsigned long long beta, unsigned long long top_mod,
+__device__ __forceinline__ void normalise_t(U192 (&acc)[L], const Div64& beta, const Div64& top_mod,
                                             unsigned long long (&out)[L]) {
   U192 carry{0, 0, 0};
 #pragma unroll
@@ -114,7 +161,7 @@ __device__ __forceinline__ void normalise_t(U192 (&acc)[L], unsigned long long b
     out[s] = divmod192(v, beta);
     carry = v;
   }
-  out[L - 1] %= top_mod;
+  out[L - 1] = mod64(out[L - 1], top_mod);
 }
 template <int L>
 __device__ __forceinline__ void finish_row_t(const LinrecArgs& a, int i, U192 (&accA)[L], U192 (&accB)[L]) {
@@ -210,6 +257,139 @@ __global__ void __launch_bounds__(256) linrec_dense_kernel(LinrecArgs a) {
       add192(accB[s], shfl_down192(accB[s], off));
     }
   if (lane == 0) finish_row_t<L>(a, i, accA, accB);
+}
+
+// One factor over a FLAT partition of the side x side index space: warp w of W
+// streams the contiguous elements [E w / W, E (w+1) / W) of every plane of A
+// and B (E = side^2), one resident wave, so every warp moves the same bytes
+// and the reads are long sequential runs.  The vector is read through L1 (the
+// same columns for every warp).  A warp's range crosses at most a few row
+// boundaries; per row segment it shuffle-reduces its exact 192-bit partials,
+// and a row split between warps is finished by the last of them to arrive
+// (partials in `scratch`, an arrival counter per row, reset by the finisher).
+struct LinrecFlat {
+  U192* scratch;      // side x cmax x 2L partial sums
+  unsigned* cnt;      // side arrival counters (zero between launches)
+  int cmax;           // max warps sharing a row
+  float keep;         // fraction of A and B loads marked L2 evict_last
+};
+
+// a load of the matrix stream under an L2 policy: the fraction f.keep of the
+// lines (as many as the 126 MB L2 holds) stays resident across factors, the
+// rest streams evict_first, so consecutive factors re-read the kept part from
+// L2 rather than HBM
+__device__ __forceinline__ unsigned long long ld_policy(const unsigned long long* p, unsigned long long pol) {
+  unsigned long long v;
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+template <int L, int U, bool PF>
+__global__ void __launch_bounds__(256, L == 1 ? 3 : 2) linrec_flat_kernel(LinrecArgs a, LinrecFlat f) {
+  const int lane = threadIdx.x & 31;
+  const long long W = (long long)gridDim.x * (blockDim.x >> 5);
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long side = a.side, E = side * side;
+  long long e = E * w / W;
+  const long long e1 = E * (w + 1) / W;
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(pol) : "f"(f.keep));
+  while (e < e1) {
+    const long long r = e / side;
+    const long long rend = min(e1, (r + 1) * side);
+    const int c1 = (int)(rend - r * side);
+    U192 accA[L], accB[L];
+#pragma unroll
+    for (int s = 0; s < L; ++s) accA[s] = accB[s] = U192{0, 0, 0};
+    const unsigned long long* Ar = a.A + r * side;
+    const unsigned long long* Br = a.B + r * side;
+    // batches of 32 U columns, the last one predicated (zeros past the end):
+    // every batch has all its loads in flight at once; with PF the next
+    // batch's loads are issued before this batch's products
+    unsigned long long av[L][U], bv[L][U], xv[L][U];
+    auto load = [&](int j, unsigned long long (&ra)[L][U], unsigned long long (&rb)[L][U],
+                    unsigned long long (&rx)[L][U]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool in = j + 32 * u < c1;
+#pragma unroll
+        for (int t = 0; t < L; ++t) {
+          ra[t][u] = in ? ld_policy(Ar + t * E + j + 32 * u, pol) : 0ull;
+          rb[t][u] = in ? ld_policy(Br + t * E + j + 32 * u, pol) : 0ull;
+          rx[t][u] = in ? __ldg(a.w + t * side + j + 32 * u) : 0ull;
+        }
+      }
+    };
+    int j = (int)(e - r * side) + lane;
+    if (PF) load(j, av, bv, xv);
+    for (; j - lane < c1; j += 32 * U) {
+      unsigned long long na[L][U], nb[L][U], nx[L][U];
+      if (PF) {
+        load(j + 32 * U, na, nb, nx);
+      } else {
+        load(j, av, bv, xv);
+      }
+#pragma unroll
+      for (int t1 = 0; t1 < L; ++t1)
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int t2 = 0; t1 + t2 < L; ++t2) {
+            add_prod(accA[t1 + t2], av[t1][u], xv[t2][u]);
+            add_prod(accB[t1 + t2], bv[t1][u], xv[t2][u]);
+          }
+      if (PF) {
+#pragma unroll
+        for (int t = 0; t < L; ++t)
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            av[t][u] = na[t][u];
+            bv[t][u] = nb[t][u];
+            xv[t][u] = nx[t][u];
+          }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1)
+#pragma unroll
+      for (int s = 0; s < L; ++s) {
+        add192(accA[s], shfl_down192(accA[s], off));
+        add192(accB[s], shfl_down192(accB[s], off));
+      }
+    if (lane == 0) {
+      // warps holding the row's first and last elements
+      const long long wlo = ((r * side + 1) * W - 1) / E, whi = ((r + 1) * side * W - 1) / E;
+      if (wlo == whi) {
+        finish_row_t<L>(a, (int)r, accA, accB);
+      } else {
+        U192* base = f.scratch + (size_t)r * f.cmax * 2 * L;
+        U192* mine = base + (size_t)(w - wlo) * 2 * L;
+#pragma unroll
+        for (int s = 0; s < L; ++s) {
+          mine[s] = accA[s];
+          mine[L + s] = accB[s];
+        }
+        __threadfence();
+        const unsigned n = (unsigned)(whi - wlo + 1);
+        if (atomicAdd(f.cnt + r, 1u) == n - 1) {
+          __threadfence();
+#pragma unroll
+          for (int s = 0; s < L; ++s) accA[s] = accB[s] = U192{0, 0, 0};
+          for (unsigned k = 0; k < n; ++k) {
+            const unsigned long long* q = reinterpret_cast<const unsigned long long*>(base + (size_t)k * 2 * L);
+#pragma unroll
+            for (int s = 0; s < L; ++s) {
+              add192(accA[s], U192{__ldcg(q + 3 * s), __ldcg(q + 3 * s + 1), __ldcg(q + 3 * s + 2)});
+              add192(accB[s], U192{__ldcg(q + 3 * (L + s)), __ldcg(q + 3 * (L + s) + 1), __ldcg(q + 3 * (L + s) + 2)});
+            }
+          }
+          finish_row_t<L>(a, (int)r, accA, accB);
+          f.cnt[r] = 0;
+        }
+      }
+    }
+    e = rend;
+  }
 }
 
 __global__ void linrec_csr_kernel(LinrecArgs a) {
@@ -343,8 +523,8 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
   a.B = (const unsigned long long*)dB;
   a.side = side;
   a.limbs = pl.limbs;
-  a.beta = pl.beta;
-  a.top_mod = pl.top_mod;
+  a.beta = dev::make_div64(pl.beta);
+  a.top_mod = dev::make_div64(pl.top_mod);
   if (csr) {
     a.a_ptr = csr->a_ptr;
     a.a_col = csr->a_col;
@@ -405,8 +585,77 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
     check(cudaFreeAsync(tmp, st), "cudaFreeAsync");
     return;
   }
+  // DRZG_LINREC_FLAT: 0 = a warp per row, 1 = flat partition for large
+  // sides (default), 2 = flat at every side, 3 = flat with the next batch's
+  // loads in flight during the products (slower: 52 vs 44 us at side 3003)
+  static const int flat_mode = [] {
+    const char* e = std::getenv("DRZG_LINREC_FLAT");
+    return e ? std::atoi(e) : 1;
+  }();
+  // the flat partition wins once the matrices stream from HBM (side 3003:
+  // 37 vs 47 us a factor, 1 limb); below that a warp per row finishes the
+  // rows' serial digit normalisation in parallel (side 220: 6 vs 12 us)
+  const bool flat = flat_mode == 2 || (flat_mode == 1 && (long long)side * side >= (1LL << 20));
   uint64_t* cur = dw;
   uint64_t* nxt = tmp;
+  if (!csr && flat) {
+    // one resident wave of warps over the flat index space, at least 512
+    // elements a warp (the per-segment reduction amortised)
+    const int L = pl.limbs;
+    const bool pf = flat_mode == 3;
+    using KF = void (*)(dev::LinrecArgs, dev::LinrecFlat);
+    KF kfn = L == 1 ? (pf ? dev::linrec_flat_kernel<1, 4, true> : dev::linrec_flat_kernel<1, 8, false>)
+             : L == 2 ? (pf ? dev::linrec_flat_kernel<2, 2, true> : dev::linrec_flat_kernel<2, 4, false>)
+             : L == 3 ? (pf ? dev::linrec_flat_kernel<3, 1, true> : dev::linrec_flat_kernel<3, 2, false>)
+                      : (pf ? dev::linrec_flat_kernel<4, 1, true> : dev::linrec_flat_kernel<4, 2, false>);
+    int dev = 0, sms = 0, per_sm = 0;
+    check(cudaGetDevice(&dev), "device");
+    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kfn, 256, 0), "occupancy");
+    DRZG_REQUIRE(per_sm >= 1, "linrec: flat kernel does not fit an SM");
+    const long long E = (long long)side * side;
+    const long long blocks = std::max(1LL, std::min((long long)sms * per_sm, E / (512LL * 8)));
+    const long long W = blocks * 8;
+    // most warps sharing one row: a warp holds at least floor(E / W) elements
+    const long long per_warp = E / W;
+    const int cmax = per_warp == 0 ? (int)W : (int)std::min<long long>(W, (side + per_warp - 1) / per_warp + 1);
+    dev::LinrecFlat f{};
+    const size_t scratch_bytes = (size_t)side * cmax * 2 * L * sizeof(dev::U192);
+    check(cudaMallocAsync(&f.scratch, scratch_bytes, st), "cudaMallocAsync");
+    check(cudaMallocAsync(&f.cnt, (size_t)side * sizeof(unsigned), st), "cudaMallocAsync");
+    check(cudaMemsetAsync(f.cnt, 0, (size_t)side * sizeof(unsigned), st), "memset");
+    f.cmax = cmax;
+    {
+      int l2 = 0;
+      check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev), "l2");
+      const double mat = 2.0 * L * (double)E * 8;
+      static const double keep_scale = [] {
+        const char* e = std::getenv("DRZG_LINREC_KEEP");
+        return e ? std::atof(e) : 0.6;
+      }();
+      f.keep = (float)std::max(0.01, std::min(1.0, keep_scale * l2 / mat));
+    }
+    for (int64_t t = tmax; t >= 0; --t) {
+      a.w = (const unsigned long long*)cur;
+      a.y = (unsigned long long*)nxt;
+      a.t = (unsigned long long)t;
+      kfn<<<(unsigned)blocks, 256, 0, st>>>(a, f);
+      std::swap(cur, nxt);
+    }
+    check(cudaGetLastError(), "linrec launch");
+    if (kernel_ms) {
+      check(cudaEventRecord(e1, st), "event");
+      check(cudaEventSynchronize(e1), "event");
+      check(cudaEventElapsedTime(kernel_ms, e0, e1), "event");
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    if (cur != dw) check(cudaMemcpyAsync(dw, cur, vec * 8, cudaMemcpyDeviceToDevice, st), "copy back");
+    check(cudaFreeAsync(f.scratch, st), "cudaFreeAsync");
+    check(cudaFreeAsync(f.cnt, st), "cudaFreeAsync");
+    check(cudaFreeAsync(tmp, st), "cudaFreeAsync");
+    return;
+  }
   for (int64_t t = tmax; t >= 0; --t) {
     a.w = (const unsigned long long*)cur;
     a.y = (unsigned long long*)nxt;

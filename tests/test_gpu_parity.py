@@ -53,6 +53,34 @@ def test_linrec_edge_cases():
     assert not z.any()
 
 
+@pytest.mark.parametrize("p,M,side,tmax", [
+    (7, 20, 3003, 2),   # fourfold side, 1 limb: rows shared by 2-3 warps of the flat partition
+    (7, 24, 3003, 1),   # fourfold side, 2 limbs
+    (7, 49, 455, 3),    # 3 limbs
+    (11, 17, 221, 4),   # odd side, few warps
+    (13, 13, 1, 3),     # one entry
+])
+def test_linrec_eval_large_sides_match_oracle(p, M, side, tmax):
+    """the flat-partition kernel at the BASELINE sizes against the C restatement
+    of linalg.hpp:337-410 (oracle/linrec_oracle.c) on seeded inputs"""
+    from oracle import refapi
+    sp = drzg.stripe_plan(p, M)
+    L, beta = sp.limbs, int(sp.beta)
+    top = p ** (M - sp.limb_exp * (L - 1))
+    rng = np.random.default_rng(side * 1000 + M)
+
+    def planes(n):
+        x = rng.integers(0, min(beta, 2**62), size=(L, n), dtype=np.uint64)
+        x[L - 1] %= np.uint64(top)
+        return x.ravel()
+
+    A, B, w = planes(side * side), planes(side * side), planes(side)
+    got, ctr = drzg.linrec_eval(p, M, side, A, B, tmax, w)
+    want = refapi.oracle_linrec_eval(p, M, side, A, B, tmax, w)
+    assert ctr == tmax + 1
+    assert (got == want).all()
+
+
 CHUNK_CASES = [
     # (golden file, M, u, pole, v, k)
     ("fermat_cubic_curve_f7.json", 6, [3, 7, 7], 6, [1, 1, 1], 3),
