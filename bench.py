@@ -348,6 +348,40 @@ def roofline_of(kern, nL, peak, config):
                          "ms": kern["epilogue_ms"], "share_of_kernel_time": kern["epilogue_ms"] / ksum if ksum else None}}
 
 
+def matvec_stepping(drzg, torch):
+    """north_star (a): achieved HBM GB/s of the reference-shaped linrec_eval
+    (linalg.hpp:337-410) on the device, drzg_linrec_eval_device with the inputs
+    resident, CUDA events around tmax + 1 = 21 factors, best of 3; algorithmic
+    bytes = A and B once per factor (2 side^2 8 limbs); at side 3003 the
+    matrices (144 / 289 MB) exceed the 126 MB L2"""
+    hbm = measured_peaks().get("hbm_gbs")
+    out = []
+    for p, M, side in [(7, 20, 3003), (7, 24, 3003), (13, 13, 495)]:
+        sp = drzg.stripe_plan(p, M)
+        L = sp.limbs
+        g = torch.Generator(device="cuda").manual_seed(1)
+        hi = min(int(sp.beta), 2**62)
+        A = torch.randint(0, hi, (L * side * side,), dtype=torch.int64, device="cuda", generator=g)
+        B = torch.randint(0, hi, (L * side * side,), dtype=torch.int64, device="cuda", generator=g)
+        w = torch.randint(0, hi, (L * side,), dtype=torch.int64, device="cuda", generator=g)
+        if L > 1:
+            top = p ** (M - sp.limb_exp * (L - 1))
+            for X in (A, B, w):
+                X.view(L, -1)[L - 1] %= top
+        drzg.linrec_eval_device(p, M, side, A.data_ptr(), B.data_ptr(), 2, w.data_ptr())
+        torch.cuda.synchronize()
+        best = min(drzg.linrec_eval_device(p, M, side, A.data_ptr(), B.data_ptr(), 20, w.data_ptr(), timed=True)
+                   for _ in range(3))
+        per = best / 21
+        gbs = 2 * side * side * 8 * L / (per / 1e3) / 1e9
+        out.append({"p": p, "M": M, "side": side, "limbs": L, "us_per_factor": round(per * 1e3, 2),
+                    "alg_GBps": round(gbs, 1), "frac_hbm": round(gbs / hbm, 3) if hbm else None,
+                    "kernel": "linrec_flat_kernel" if side * side >= (1 << 20) else "linrec_dense_kernel"})
+        del A, B, w
+    torch.cuda.empty_cache()
+    return {"cases": out, "peak_GBps": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
+
+
 def fourfold_leg(drzg, torch, local, peak):
     """ONE complete zeta function of the metric's own hypersurface (configs[4])
     under clock sampling, after a one-column warm-up; then column 0 once more
@@ -619,6 +653,10 @@ def main():
     }
     if dist_leg is not None:
         line["fourfold"] = dist_leg
+    try:
+        line["matvec_stepping"] = matvec_stepping(drzg, torch)
+    except Exception as e:
+        line["matvec_stepping"] = {"error": str(e)}
     leg = dist_leg is None and (args.fourfold_leg == "on" or (args.fourfold_leg == "auto" and world == 1 and
                                                                args.config == "k3"))
     if leg:
