@@ -376,7 +376,7 @@ def matvec_stepping(drzg, torch):
         gbs = 2 * side * side * 8 * L / (per / 1e3) / 1e9
         out.append({"p": p, "M": M, "side": side, "limbs": L, "us_per_factor": round(per * 1e3, 2),
                     "alg_GBps": round(gbs, 1), "frac_hbm": round(gbs / hbm, 3) if hbm else None,
-                    "kernel": "linrec_flat_kernel" if side * side >= (1 << 20) else "linrec_dense_kernel"})
+                    "kernel": "linrec_flat_kernel" if side * side >= (1 << 20) else "linrec_resident_kernel"})
         del A, B, w
     torch.cuda.empty_cache()
     return {"cases": out, "peak_GBps": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}

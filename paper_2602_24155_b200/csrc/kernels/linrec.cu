@@ -420,6 +420,72 @@ __global__ void linrec_csr_kernel(LinrecArgs a) {
 }
 
 
+// Small sides, all factors in ONE cooperative launch with the matrices
+// resident in shared memory: CTA c owns rows [c R, c R + R) (a warp per row)
+// and loads its rows of A and B into shared memory once; each factor then
+// reads only the vector (L side words, from L2) and synchronises the grid, so
+// a factor costs a grid barrier instead of a launch plus an L2 pass over the
+// matrices.  Same exact accumulation and normalisation as the other kernels.
+template <int L>
+__global__ void __launch_bounds__(256) linrec_resident_kernel(LinrecArgs a, unsigned long long* buf0,
+                                                               unsigned long long* buf1, long long tmax, int R) {
+  extern __shared__ unsigned long long sm[];  // [R][L][side] A, [R][L][side] B, [L][side] w
+  cg::grid_group grid = cg::this_grid();
+  const int side = a.side;
+  const size_t nn = (size_t)side * side;
+  const int r0 = blockIdx.x * R;
+  const int rows = max(0, min(R, side - r0));
+  unsigned long long* sA = sm;
+  unsigned long long* sB = sm + (size_t)R * L * side;
+  unsigned long long* sw = sB + (size_t)R * L * side;
+  for (int k = threadIdx.x; k < rows * L * side; k += blockDim.x) {
+    const int rr = k / (L * side), rem = k % (L * side), t = rem / side, j = rem % side;
+    sA[k] = a.A[t * nn + (size_t)(r0 + rr) * side + j];
+    sB[k] = a.B[t * nn + (size_t)(r0 + rr) * side + j];
+  }
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  for (long long t = tmax; t >= 0; --t) {
+    const unsigned long long* w = ((tmax - t) & 1) ? buf1 : buf0;
+    unsigned long long* y = ((tmax - t) & 1) ? buf0 : buf1;
+    for (int k = threadIdx.x; k < L * side; k += blockDim.x) sw[k] = __ldcg(w + k);
+    __syncthreads();
+    if (wi < rows) {
+      U192 accA[L], accB[L];
+#pragma unroll
+      for (int s = 0; s < L; ++s) accA[s] = accB[s] = U192{0, 0, 0};
+      const unsigned long long* ra = sA + (size_t)wi * L * side;
+      const unsigned long long* rb = sB + (size_t)wi * L * side;
+      for (int j = lane; j < side; j += 32) {
+#pragma unroll
+        for (int t1 = 0; t1 < L; ++t1) {
+          const unsigned long long av = ra[t1 * side + j], bv = rb[t1 * side + j];
+#pragma unroll
+          for (int t2 = 0; t1 + t2 < L; ++t2) {
+            const unsigned long long x = sw[t2 * side + j];
+            add_prod(accA[t1 + t2], av, x);
+            add_prod(accB[t1 + t2], bv, x);
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1)
+#pragma unroll
+        for (int s = 0; s < L; ++s) {
+          add192(accA[s], shfl_down192(accA[s], off));
+          add192(accB[s], shfl_down192(accB[s], off));
+        }
+      if (lane == 0) {
+        LinrecArgs b = a;
+        b.y = y;
+        b.t = (unsigned long long)t;
+        finish_row_t<L>(b, r0 + wi, accA, accB);
+      }
+    }
+    __threadfence();
+    grid.sync();
+  }
+}
+
 // All factors of a dense linrec_eval in ONE cooperative launch: every warp owns
 // rows i = warp_global, + total warps, ...; the grid synchronises between
 // factors (each factor needs the whole previous vector).  A and B stream with
@@ -549,12 +615,58 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
     check(cudaEventCreate(&e1), "event");
     check(cudaEventRecord(e0, st), "event");
   }
-  static const bool persistent = [] {
+  const bool persistent = [] {
     // opt-in: one cooperative launch for all factors measured slower than a
     // launch per factor (side 3003: 115 vs 60 us per factor; side 220-495 equal)
     const char* e = std::getenv("DRZG_LINREC_PERSISTENT");
     return e && std::string(e) == "1";
   }();
+  // matrices resident in shared memory for sides whose rows spread over the
+  // SMs fit (DRZG_LINREC_RESIDENT=0 disables)
+  const bool resident_ok = [] {
+    const char* e = std::getenv("DRZG_LINREC_RESIDENT");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!csr && !persistent && resident_ok && (long long)side * side < (1LL << 20)) {
+    const int L = pl.limbs;
+    using KR = void (*)(dev::LinrecArgs, unsigned long long*, unsigned long long*, long long, int);
+    KR kr = L == 1 ? dev::linrec_resident_kernel<1>
+            : L == 2 ? dev::linrec_resident_kernel<2>
+            : L == 3 ? dev::linrec_resident_kernel<3> : dev::linrec_resident_kernel<4>;
+    int dev = 0, sms = 0, optin = 0;
+    check(cudaGetDevice(&dev), "device");
+    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem optin");
+    const int R = std::min(8, (side + sms - 1) / sms);  // rows a CTA (a warp each)
+    const int blocks = (side + R - 1) / R;
+    const size_t rsmem = ((size_t)2 * R * L * side + (size_t)L * side) * 8;
+    int per_sm = 0;
+    if (rsmem <= (size_t)optin) {
+      raise_smem_limit(kr, rsmem);
+      check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)kr, 32 * R, rsmem), "occupancy");
+    }
+    if (per_sm >= 1 && blocks <= sms * per_sm) {
+      unsigned long long* b0 = (unsigned long long*)dw;
+      unsigned long long* b1 = (unsigned long long*)tmp;
+      long long tm = (long long)tmax;
+      int rr = R;
+      void* args[] = {&a, &b0, &b1, &tm, &rr};
+      check(cudaLaunchCooperativeKernel((const void*)kr, dim3(blocks), dim3(32 * R), args, rsmem, st),
+            "linrec resident launch");
+      check(cudaGetLastError(), "linrec launch");
+      // factor f (0-based) writes buf1 when f is even: tmax + 1 factors
+      if (((tmax + 1) & 1) == 1) check(cudaMemcpyAsync(dw, tmp, vec * 8, cudaMemcpyDeviceToDevice, st), "copy back");
+      if (kernel_ms) {
+        check(cudaEventRecord(e1, st), "event");
+        check(cudaEventSynchronize(e1), "event");
+        check(cudaEventElapsedTime(kernel_ms, e0, e1), "event");
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
+      check(cudaFreeAsync(tmp, st), "cudaFreeAsync");
+      return;
+    }
+  }
   if (!csr && persistent) {
     // one cooperative launch for every factor (grid-wide sync between factors)
     int dev = 0, sms = 0, per_sm = 0;
@@ -588,7 +700,7 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
   // DRZG_LINREC_FLAT: 0 = a warp per row, 1 = flat partition for large
   // sides (default), 2 = flat at every side, 3 = flat with the next batch's
   // loads in flight during the products (slower: 52 vs 44 us at side 3003)
-  static const int flat_mode = [] {
+  const int flat_mode = [] {
     const char* e = std::getenv("DRZG_LINREC_FLAT");
     return e ? std::atoi(e) : 1;
   }();
@@ -629,7 +741,7 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
       int l2 = 0;
       check(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev), "l2");
       const double mat = 2.0 * L * (double)E * 8;
-      static const double keep_scale = [] {
+      const double keep_scale = [] {
         const char* e = std::getenv("DRZG_LINREC_KEEP");
         return e ? std::atof(e) : 0.6;
       }();

@@ -19,8 +19,19 @@ def _arr(xs):
     return np.array([int(x) for x in xs], dtype=np.uint64)
 
 
+# the linrec_eval kernels: matrices resident in shared memory (small sides,
+# default), a warp per row, the flat partition (large sides, default) and the
+# flat partition forced at every side
+LINREC_ENVS = [{}, {"DRZG_LINREC_RESIDENT": "0"}, {"DRZG_LINREC_RESIDENT": "0", "DRZG_LINREC_FLAT": "0"},
+               {"DRZG_LINREC_FLAT": "2"}]
+_env_id = lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default"
+
+
+@pytest.mark.parametrize("env", LINREC_ENVS, ids=_env_id)
 @pytest.mark.parametrize("idx", range(10))
-def test_linrec_eval_matches_reference(idx):
+def test_linrec_eval_matches_reference(idx, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     c = golden("linrec_cases.json")["cases"][idx]
     out, ctr = drzg.linrec_eval(c["p"], c["M"], c["side"], _arr(c["A"]), _arr(c["B"]), c["tmax"], _arr(c["w"]))
     assert (out == _arr(c["out"])).all()
@@ -60,10 +71,13 @@ def test_linrec_edge_cases():
     (11, 17, 221, 4),   # odd side, few warps
     (13, 13, 1, 3),     # one entry
 ])
-def test_linrec_eval_large_sides_match_oracle(p, M, side, tmax):
-    """the flat-partition kernel at the BASELINE sizes against the C restatement
+@pytest.mark.parametrize("env", LINREC_ENVS, ids=_env_id)
+def test_linrec_eval_large_sides_match_oracle(p, M, side, tmax, env, monkeypatch):
+    """every linrec_eval kernel at the BASELINE sizes against the C restatement
     of linalg.hpp:337-410 (oracle/linrec_oracle.c) on seeded inputs"""
     from oracle import refapi
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     sp = drzg.stripe_plan(p, M)
     L, beta = sp.limbs, int(sp.beta)
     top = p ** (M - sp.limb_exp * (L - 1))
