@@ -651,8 +651,15 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
       long long tm = (long long)tmax;
       int rr = R;
       void* args[] = {&a, &b0, &b1, &tm, &rr};
-      check(cudaLaunchCooperativeKernel((const void*)kr, dim3(blocks), dim3(32 * R), args, rsmem, st),
-            "linrec resident launch");
+      const cudaError_t le =
+          cudaLaunchCooperativeKernel((const void*)kr, dim3(blocks), dim3(32 * R), args, rsmem, st);
+      if (le == cudaErrorCooperativeLaunchTooLarge) {
+        // the SMs are not all available to this context (MPS limits): the
+        // per-factor kernels below do the same work
+        (void)cudaGetLastError();
+        goto per_factor;
+      }
+      check(le, "linrec resident launch");
       check(cudaGetLastError(), "linrec launch");
       // factor f (0-based) writes buf1 when f is even: tmax + 1 factors
       if (((tmax + 1) & 1) == 1) check(cudaMemcpyAsync(dw, tmp, vec * 8, cudaMemcpyDeviceToDevice, st), "copy back");
@@ -667,6 +674,7 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
       return;
     }
   }
+per_factor:
   if (!csr && persistent) {
     // one cooperative launch for every factor (grid-wide sync between factors)
     int dev = 0, sms = 0, per_sm = 0;
