@@ -2,13 +2,16 @@
 // detail::sparse_steps, reference linalg.hpp:257-410).
 //
 // w <- M(0) M(1) ... M(tmax) w,  M(t) = t A + B, on the reference's own
-// residue layout (limbs planes of base-beta u64 digits).  One launch per
-// factor; a warp owns one output row and streams A and B once per factor
-// (the HBM roofline for side >= ~700, 16 B per (i, j) per limb).  Products
-// are accumulated exactly in 192-bit per digit-plane sum (t1 + t2 < limbs;
-// higher planes vanish because p^M | beta^limbs), then normalised to base-beta
-// digits, the top digit reduced mod p^(M - e(limbs-1)), so the output is the
-// canonical residue the reference produces.
+// residue layout (limbs planes of base-beta u64 digits).  Three dense kernels:
+// linrec_flat_kernel for sides whose matrices stream from HBM (a flat,
+// balanced partition of the index space, a launch per factor),
+// linrec_resident_kernel for smaller sides (all factors in one cooperative
+// launch, the matrices in shared memory), linrec_dense_kernel (a warp per row)
+// as the fallback.  Products are accumulated exactly in 192-bit per
+// digit-plane sum (t1 + t2 < limbs; higher planes vanish because
+// p^M | beta^limbs), then normalised to base-beta digits with preinverted
+// divisions, the top digit reduced mod p^(M - e(limbs-1)), so the output is
+// the canonical residue the reference produces.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -486,73 +489,6 @@ __global__ void __launch_bounds__(256) linrec_resident_kernel(LinrecArgs a, unsi
   }
 }
 
-// All factors of a dense linrec_eval in ONE cooperative launch: every warp owns
-// rows i = warp_global, + total warps, ...; the grid synchronises between
-// factors (each factor needs the whole previous vector).  A and B stream with
-// 128-bit loads (two columns per lane per load, two loads in flight per matrix
-// and limb), the vector sits in shared memory, reloaded after every grid sync.
-// Same exact 192-bit accumulation and canonical normalisation as
-// linrec_dense_kernel, so the output is bit-identical.
-__global__ void __launch_bounds__(256) linrec_dense_persistent(LinrecArgs a, unsigned long long* buf0,
-                                                                 unsigned long long* buf1, long long tmax) {
-  extern __shared__ unsigned long long ws[];  // limbs x side
-  cg::grid_group grid = cg::this_grid();
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  const int gw = blockIdx.x * wpb + (threadIdx.x >> 5), nw = gridDim.x * wpb;
-  const size_t nn = (size_t)a.side * a.side;
-  const int side = a.side, L = a.limbs;
-  const bool even = (side & 1) == 0;
-  for (long long t = tmax; t >= 0; --t) {
-    const unsigned long long* w = ((tmax - t) & 1) ? buf1 : buf0;
-    unsigned long long* y = ((tmax - t) & 1) ? buf0 : buf1;
-    for (int k = threadIdx.x; k < L * side; k += blockDim.x) ws[k] = w[k];
-    __syncthreads();
-    LinrecArgs b = a;
-    b.y = y;
-    b.t = (unsigned long long)t;
-    for (int i = gw; i < side; i += nw) {
-      U192 accA[kMaxLimbs], accB[kMaxLimbs];
-      for (int s2 = 0; s2 < kMaxLimbs; ++s2) accA[s2] = accB[s2] = U192{0, 0, 0};
-      for (int t1 = 0; t1 < L; ++t1) {
-        const unsigned long long* ar = a.A + t1 * nn + (size_t)i * side;
-        const unsigned long long* br = a.B + t1 * nn + (size_t)i * side;
-        // rows start 16-byte aligned when side is even: two columns per load
-        if (even) {
-          for (int j = 2 * lane; j < side; j += 64) {
-            const ulonglong2 av = __ldg(reinterpret_cast<const ulonglong2*>(ar + j));
-            const ulonglong2 bv = __ldg(reinterpret_cast<const ulonglong2*>(br + j));
-            for (int t2 = 0; t1 + t2 < L; ++t2) {
-              const unsigned long long x0 = ws[t2 * side + j], x1 = ws[t2 * side + j + 1];
-              add_prod(accA[t1 + t2], av.x, x0);
-              add_prod(accA[t1 + t2], av.y, x1);
-              add_prod(accB[t1 + t2], bv.x, x0);
-              add_prod(accB[t1 + t2], bv.y, x1);
-            }
-          }
-        } else {
-          for (int j = lane; j < side; j += 32) {
-            const unsigned long long av = __ldg(ar + j), bv = __ldg(br + j);
-            for (int t2 = 0; t1 + t2 < L; ++t2) {
-              const unsigned long long x = ws[t2 * side + j];
-              add_prod(accA[t1 + t2], av, x);
-              add_prod(accB[t1 + t2], bv, x);
-            }
-          }
-        }
-      }
-      for (int off = 16; off; off >>= 1)
-        for (int s2 = 0; s2 < L; ++s2) {
-          add192(accA[s2], shfl_down192(accA[s2], off));
-          add192(accB[s2], shfl_down192(accB[s2], off));
-        }
-      if (lane == 0) finish_row(b, i, accA, accB);
-    }
-    __threadfence();
-    grid.sync();
-  }
-}
-
 }  // namespace dev
 
 namespace {
@@ -615,19 +551,13 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
     check(cudaEventCreate(&e1), "event");
     check(cudaEventRecord(e0, st), "event");
   }
-  const bool persistent = [] {
-    // opt-in: one cooperative launch for all factors measured slower than a
-    // launch per factor (side 3003: 115 vs 60 us per factor; side 220-495 equal)
-    const char* e = std::getenv("DRZG_LINREC_PERSISTENT");
-    return e && std::string(e) == "1";
-  }();
   // matrices resident in shared memory for sides whose rows spread over the
   // SMs fit (DRZG_LINREC_RESIDENT=0 disables)
   const bool resident_ok = [] {
     const char* e = std::getenv("DRZG_LINREC_RESIDENT");
     return !(e && std::string(e) == "0");
   }();
-  if (!csr && !persistent && resident_ok && (long long)side * side < (1LL << 20)) {
+  if (!csr && resident_ok && (long long)side * side < (1LL << 20)) {
     const int L = pl.limbs;
     using KR = void (*)(dev::LinrecArgs, unsigned long long*, unsigned long long*, long long, int);
     KR kr = L == 1 ? dev::linrec_resident_kernel<1>
@@ -675,36 +605,6 @@ void linrec_device(const LinrecPlan& pl, int side, const uint64_t* dA, const uin
     }
   }
 per_factor:
-  if (!csr && persistent) {
-    // one cooperative launch for every factor (grid-wide sync between factors)
-    int dev = 0, sms = 0, per_sm = 0;
-    check(cudaGetDevice(&dev), "device");
-    check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
-    raise_smem_limit(dev::linrec_dense_persistent, smem);
-    check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dev::linrec_dense_persistent, 256, smem), "occupancy");
-    DRZG_REQUIRE(per_sm >= 1, "linrec: persistent kernel does not fit an SM");
-    const int rows_per_block = 8;
-    const int blocks = std::max(1, std::min(sms * per_sm, (side + rows_per_block - 1) / rows_per_block));
-    unsigned long long* b0 = (unsigned long long*)dw;
-    unsigned long long* b1 = (unsigned long long*)tmp;
-    long long tm = (long long)tmax;
-    void* args[] = {&a, &b0, &b1, &tm};
-    check(cudaLaunchCooperativeKernel((const void*)dev::linrec_dense_persistent, dim3(blocks), dim3(256), args, smem, st),
-          "linrec cooperative launch");
-    // the result is in buf0 after an odd number of factors... (tmax + 1 factors:
-    // factor f (0-based) writes buf1 when f is even)
-    if (((tmax + 1) & 1) == 1) check(cudaMemcpyAsync(dw, tmp, vec * 8, cudaMemcpyDeviceToDevice, st), "copy back");
-    if (kernel_ms) {
-      check(cudaEventRecord(e1, st), "event");
-      check(cudaEventSynchronize(e1), "event");
-      check(cudaEventElapsedTime(kernel_ms, e0, e1), "event");
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-    }
-    check(cudaGetLastError(), "linrec launch");
-    check(cudaFreeAsync(tmp, st), "cudaFreeAsync");
-    return;
-  }
   // DRZG_LINREC_FLAT: 0 = a warp per row, 1 = flat partition for large
   // sides (default), 2 = flat at every side, 3 = flat with the next batch's
   // loads in flight during the products (slower: 52 vs 44 us at side 3003)
