@@ -20,6 +20,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../host/common.hpp"
@@ -44,6 +45,21 @@ __device__ __forceinline__ void add_prod(U192& acc, unsigned long long a, unsign
       : "+l"(acc.w0), "+l"(acc.w1), "+l"(acc.w2)
       : "l"(lo), "l"(hi));
 }
+
+// two-word accumulator, for plans whose row sums stay below 2^128
+// (limbs * side * (beta - 1)^2 < 2^127: both fourfold plans)
+struct U128 {
+  unsigned long long w0, w1;
+};
+__device__ __forceinline__ void add_prod(U128& acc, unsigned long long a, unsigned long long b) {
+  unsigned long long lo = a * b, hi = __umul64hi(a, b);
+  asm("add.cc.u64 %0, %0, %2;\n\t"
+      "addc.u64 %1, %1, %3;"
+      : "+l"(acc.w0), "+l"(acc.w1)
+      : "l"(lo), "l"(hi));
+}
+__device__ __forceinline__ U192 widen(const U128& v) { return U192{v.w0, v.w1, 0}; }
+__device__ __forceinline__ U192 widen(const U192& v) { return v; }
 
 __device__ __forceinline__ void add192(U192& a, const U192& b) {
   asm("add.cc.u64 %0, %0, %3;\n\t"
@@ -287,8 +303,9 @@ __device__ __forceinline__ unsigned long long ld_policy(const unsigned long long
   return v;
 }
 
-template <int L, int U, bool PF>
+template <int L, int U, bool PF, bool N2 = false>
 __global__ void __launch_bounds__(256, L == 1 ? 3 : 2) linrec_flat_kernel(LinrecArgs a, LinrecFlat f) {
+  using Acc = typename std::conditional<N2, U128, U192>::type;
   const int lane = threadIdx.x & 31;
   const long long W = (long long)gridDim.x * (blockDim.x >> 5);
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -301,9 +318,9 @@ __global__ void __launch_bounds__(256, L == 1 ? 3 : 2) linrec_flat_kernel(Linrec
     const long long r = e / side;
     const long long rend = min(e1, (r + 1) * side);
     const int c1 = (int)(rend - r * side);
-    U192 accA[L], accB[L];
+    Acc pA[L], pB[L];
 #pragma unroll
-    for (int s = 0; s < L; ++s) accA[s] = accB[s] = U192{0, 0, 0};
+    for (int s = 0; s < L; ++s) pA[s] = pB[s] = Acc{};
     const unsigned long long* Ar = a.A + r * side;
     const unsigned long long* Br = a.B + r * side;
     // batches of 32 U columns, the last one predicated (zeros past the end):
@@ -338,8 +355,8 @@ __global__ void __launch_bounds__(256, L == 1 ? 3 : 2) linrec_flat_kernel(Linrec
         for (int u = 0; u < U; ++u)
 #pragma unroll
           for (int t2 = 0; t1 + t2 < L; ++t2) {
-            add_prod(accA[t1 + t2], av[t1][u], xv[t2][u]);
-            add_prod(accB[t1 + t2], bv[t1][u], xv[t2][u]);
+            add_prod(pA[t1 + t2], av[t1][u], xv[t2][u]);
+            add_prod(pB[t1 + t2], bv[t1][u], xv[t2][u]);
           }
       if (PF) {
 #pragma unroll
@@ -351,6 +368,12 @@ __global__ void __launch_bounds__(256, L == 1 ? 3 : 2) linrec_flat_kernel(Linrec
             xv[t][u] = nx[t][u];
           }
       }
+    }
+    U192 accA[L], accB[L];
+#pragma unroll
+    for (int s = 0; s < L; ++s) {
+      accA[s] = widen(pA[s]);
+      accB[s] = widen(pB[s]);
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1)
@@ -624,8 +647,17 @@ per_factor:
     const int L = pl.limbs;
     const bool pf = flat_mode == 3;
     using KF = void (*)(dev::LinrecArgs, dev::LinrecFlat);
-    KF kfn = L == 1 ? (pf ? dev::linrec_flat_kernel<1, 4, true> : dev::linrec_flat_kernel<1, 8, false>)
-             : L == 2 ? (pf ? dev::linrec_flat_kernel<2, 2, true> : dev::linrec_flat_kernel<2, 4, false>)
+    // row sums below 2^128: two-word accumulators (DRZG_LINREC_N2=0 keeps three)
+    const bool n2 = [&] {
+      const char* e = std::getenv("DRZG_LINREC_N2");
+      if (e && std::string(e) == "0") return false;
+      const unsigned __int128 sq = (unsigned __int128)(pl.beta - 1) * (pl.beta - 1);
+      return sq < ((unsigned __int128)1 << 127) / ((unsigned __int128)L * (unsigned)side);
+    }();
+    KF kfn = L == 1 ? (pf ? dev::linrec_flat_kernel<1, 4, true>
+                       : n2 ? dev::linrec_flat_kernel<1, 8, false, true> : dev::linrec_flat_kernel<1, 8, false>)
+             : L == 2 ? (pf ? dev::linrec_flat_kernel<2, 2, true>
+                         : n2 ? dev::linrec_flat_kernel<2, 4, false, true> : dev::linrec_flat_kernel<2, 4, false>)
              : L == 3 ? (pf ? dev::linrec_flat_kernel<3, 1, true> : dev::linrec_flat_kernel<3, 2, false>)
                       : (pf ? dev::linrec_flat_kernel<4, 1, true> : dev::linrec_flat_kernel<4, 2, false>);
     int dev = 0, sms = 0, per_sm = 0;

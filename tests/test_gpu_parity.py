@@ -21,9 +21,10 @@ def _arr(xs):
 
 # the linrec_eval kernels: matrices resident in shared memory (small sides,
 # default), a warp per row, the flat partition (large sides, default) and the
-# flat partition forced at every side
+# flat partition forced at every side, with two-word row sums where they fit
+# (default) or three
 LINREC_ENVS = [{}, {"DRZG_LINREC_RESIDENT": "0"}, {"DRZG_LINREC_RESIDENT": "0", "DRZG_LINREC_FLAT": "0"},
-               {"DRZG_LINREC_FLAT": "2"}]
+               {"DRZG_LINREC_FLAT": "2"}, {"DRZG_LINREC_FLAT": "2", "DRZG_LINREC_N2": "0"}]
 _env_id = lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default"
 
 
