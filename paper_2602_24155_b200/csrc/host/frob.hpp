@@ -9,6 +9,7 @@
 #pragma once
 
 #include <map>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -131,7 +132,9 @@ struct PowerCache {
     out.push_back(one);
     HPoly fr = X.f;
     for (auto& c : fr.c) c %= m;
-    for (int j = 1; j < N; ++j) out.push_back(poly_mul_small_par(out.back(), fr, m, threads));
+    std::unique_ptr<ForkJoin> pool;
+    if (threads > 1) pool = std::make_unique<ForkJoin>(threads);
+    for (int j = 1; j < N; ++j) out.push_back(poly_mul_small_par(out.back(), fr, m, threads, pool.get()));
     return out;
   }
   void prime(const Hypersurface& X, int N, int s, int threads) {

@@ -57,8 +57,12 @@ inline HPoly poly_mul_small(const HPoly& a, const HPoly& f, u128 m) {
 // terms into its own targets, then the ranges' sums are reduced per target
 // (a target still receives at most |f terms| products in total, so the bound
 // above holds for the sum)
-inline HPoly poly_mul_small_par(const HPoly& a, const HPoly& f, u128 m, int threads) {
-  const int nth = std::max(1, std::min(threads, a.size() / 4096));
+// pool != nullptr: the parts run on its persistent threads (a power chain
+// multiplies ~N times; spawning threads per product cost more than the
+// product for the small early powers), and smaller operands split
+inline HPoly poly_mul_small_par(const HPoly& a, const HPoly& f, u128 m, int threads, ForkJoin* pool = nullptr) {
+  const int nth = std::max(1, std::min(pool ? std::min(threads, pool->size()) : threads,
+                                       a.size() / (pool ? 1024 : 4096)));
   if (nth == 1) return poly_mul_small(a, f, m);
   HPoly r(a.nv, a.deg + f.deg);
   auto ft = f.terms();
@@ -82,10 +86,14 @@ inline HPoly poly_mul_small_par(const HPoly& a, const HPoly& f, u128 m, int thre
     }
   };
   auto parallel = [&](auto& phase) {
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nth; ++t) pool.emplace_back([&, t] { phase(t); });
+    if (pool) {
+      pool->run(nth, [&](int t) { phase(t); });
+      return;
+    }
+    std::vector<std::thread> ths;
+    for (int t = 1; t < nth; ++t) ths.emplace_back([&, t] { phase(t); });
     phase(0);
-    for (auto& th : pool) th.join();
+    for (auto& th : ths) th.join();
   };
   parallel(run);
   parallel(reduce);

@@ -151,7 +151,9 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);  // best effort
       if (t == 0) {
         try {
+          const double tp0 = now_s();
           pc.prime(X, Nmax, smax, nexp);
+          if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] power series primed %.4f s\n", now_s() - tp0);
         } catch (...) {
           std::lock_guard<std::mutex> lk(smu);
           if (!serr) serr = std::current_exception();
