@@ -161,8 +161,11 @@ struct PowerCache {
   }
 };
 
+// the seeds of column `col` from the powers f^j, j in [j0, j1) (a column's
+// powers land in distinct poles p(m + j), so parts merge by moving buckets)
 inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const PrecisionPlan& plan,
-                                 const RuvTables& T, const HostMod& hm, PowerCache& pc, int col, int threads = 1) {
+                                 const RuvTables& T, const HostMod& hm, PowerCache& pc, int col, int threads = 1,
+                                 int j0 = 0, int j1 = 1 << 30) {
   ColumnSeeds out;
   out.col = col;
   int m = B.pole_of[col];
@@ -200,7 +203,7 @@ inline ColumnSeeds expand_column(const Hypersurface& X, const Basis& B, const Pr
   // v < p^M <= q^Ld; the 64-bit split covers q^Ld < 2^126 (Ld - c <= c)
   const bool fast_digits = !hm.wide && 2 * split.c >= dp.Ld;
   for (int j = 0; j < N; ++j) {
-    if (Dj[j] == 0) continue;
+    if (Dj[j] == 0 || j < j0 || j >= j1) continue;
     int P = (int)p * (m + j);
     const Z& kap = kappa.at(P);
     u128 kap128 = hm.wide ? 0 : kap.to_u128();

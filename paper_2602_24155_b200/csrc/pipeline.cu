@@ -126,6 +126,25 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     if (tb < (double)(1 << 18)) break;
     ++first;
   }
+  // more small columns than threads (K3: 21 on 16): each column in two
+  // parts of about equal work (powers [0, jm) and [jm, N)), so the last
+  // round of whole columns does not leave most threads idle
+  const bool halves = first == 0 && cols.size() > (size_t)nexp && !std::getenv("DRZG_EXPAND_WHOLE");
+  std::vector<int> jsplit(cols.size(), 1 << 30);
+  if (halves)
+    for (size_t i = 0; i < cols.size(); ++i) {
+      const int m = B.pole_of[cols[i]];
+      double tot = 0, acc = 0;
+      for (int j = 0; j < plan.N_m[m]; ++j) tot += (double)mono_count(X.nv(), X.d * j);
+      int jm = 0;
+      while (jm < plan.N_m[m] && acc + (double)mono_count(X.nv(), X.d * jm) <= tot / 2)
+        acc += (double)mono_count(X.nv(), X.d * jm++);
+      jsplit[i] = jm;
+    }
+  std::vector<ColumnSeeds> upper(cols.size());
+  std::vector<std::atomic<int>> parts_left(cols.size());
+  for (auto& a : parts_left) a = halves ? 2 : 1;
+  const size_t nitems = halves ? 2 * cols.size() : cols.size();
   std::atomic<size_t> next{first};
   std::atomic<bool> first_done{false};
   std::vector<std::thread> pool;
@@ -139,6 +158,32 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
       std::lock_guard<std::mutex> lk(smu);
       seeds[i] = std::move(cs);
       ready[i] = 1;
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(smu);
+      if (!serr) serr = std::current_exception();
+      ready[i] = 1;
+    }
+    scv.notify_all();
+  };
+  // work item k: column k / 2, lower (even k) or upper (odd k) powers
+  auto expand_item = [&](size_t k) {
+    if (!halves) {
+      expand_one(k, 1);
+      return;
+    }
+    const size_t i = k / 2;
+    try {
+      ColumnSeeds cs = (k & 1) ? expand_column(X, B, plan, T, hm, pc, cols[i], 1, jsplit[i])
+                               : expand_column(X, B, plan, T, hm, pc, cols[i], 1, 0, jsplit[i]);
+      std::lock_guard<std::mutex> lk(smu);
+      ColumnSeeds& dst = (k & 1) ? upper[i] : seeds[i];
+      dst = std::move(cs);
+      if (--parts_left[i] == 0) {
+        for (auto& kv : upper[i].by_pole) seeds[i].by_pole[kv.first] = std::move(kv.second);
+        seeds[i].nterms += upper[i].nterms;
+        upper[i] = ColumnSeeds();
+        ready[i] = 1;
+      }
     } catch (...) {
       std::lock_guard<std::mutex> lk(smu);
       if (!serr) serr = std::current_exception();
@@ -168,7 +213,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
         std::unique_lock<std::mutex> lk(smu);
         scv.wait(lk, [&] { return first_done.load() || serr; });
       }
-      for (size_t i = next++; i < cols.size(); i = next++) expand_one(i, 1);
+      for (size_t k = next++; k < nitems; k = next++) expand_item(k);
     });
   auto wait_column = [&](size_t i) -> ColumnSeeds& {
     std::unique_lock<std::mutex> lk(smu);
@@ -183,7 +228,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
   try {
     fin.prepare();
   } catch (...) {
-    next = cols.size();
+    next = nitems;
     join_pool();
     throw;
   }
@@ -310,7 +355,7 @@ FrobResult frobenius_matrix(const Hypersurface& X, const Basis& B, const Precisi
     out.clk = eng.clock;
     td0 = now_s();
   } catch (...) {
-    next = cols.size();
+    next = nitems;
     join_pool();
     throw;
   }
