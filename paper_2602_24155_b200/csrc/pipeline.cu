@@ -1,4 +1,5 @@
 // Frobenius assembly + zeta driver (see pipeline.cuh).
+#include <future>
 #include <sys/resource.h>
 #include <sys/syscall.h>
 #include <unistd.h>
@@ -445,7 +446,7 @@ i64 count_points_any(const Hypersurface& X, int r, i64 budget) {
 }  // namespace
 
 std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const std::vector<Z>& F, i64 b,
-                        const ZetaOptions& opt, ZetaOut& res) {
+                        const ZetaOptions& opt, ZetaOut& res, const int* fsplit_known) {
   res.hodge = hodge_numbers(X.n, X.d);
   Z cp_mod = Z::pow(X.p, (u64)(plan.M + X.n));
   const double tb0 = now_s();
@@ -508,7 +509,7 @@ std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const 
   if (X.d <= X.nv()) {
     const double tf0 = now_s();
     res.inv.fsplit_defined = true;
-    res.inv.fsplit = fedder_is_fsplit(X);
+    res.inv.fsplit = fsplit_known ? *fsplit_known != 0 : fedder_is_fsplit(X);
     if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] fsplit %.4f s\n", now_s() - tf0);
   }
   res.counts = checks;
@@ -526,6 +527,11 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
   PrecisionPlan plan = choose_precision(X.p, X.n, X.d, opt.overrides);
   if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] zeta setup %.4f s\n", now_s() - t0);
   ZetaOut res;
+  // Fedder's F-split test depends on f alone: on the host beside the
+  // Frobenius matrix instead of after it
+  std::future<bool> fs_future;
+  if (X.d <= X.nv()) fs_future = std::async(std::launch::async, [&X] { return fedder_is_fsplit(X); });
+  int fs_value = -1;
   for (;;) {
     FrobOptions fo;
     fo.policy = opt.policy;
@@ -538,7 +544,8 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device) {
     res.last = std::move(fr);
     // the reference's escalation ladder (zeta.hpp:472-535): more series
     // terms, then more digits, until the battery passes
-    const std::string why = finish_zeta(X, plan, F, b, opt, res);
+    if (fs_future.valid()) fs_value = fs_future.get() ? 1 : 0;
+    const std::string why = finish_zeta(X, plan, F, b, opt, res, fs_value >= 0 ? &fs_value : nullptr);
     if (why.empty()) break;
     res.reasons.push_back(why);
     if (std::getenv("DRZG_VERBOSE")) std::fprintf(stderr, "[drzg] escalate: %s\n", why.c_str());

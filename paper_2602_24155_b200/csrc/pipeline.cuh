@@ -75,8 +75,9 @@ ZetaOut run_zeta(const Hypersurface& X, const ZetaOptions& opt, int device);
 // sign tie-break by point counts, Newton >= Hodge, point-count checks.
 // Returns "" (res filled) or the reason the plan must escalate.  Used by the
 // multi-GPU path on the gathered F.
+// (fsplit_known: Fedder's F-split test already computed, 0 / 1, or null)
 std::string finish_zeta(const Hypersurface& X, const PrecisionPlan& plan, const std::vector<Z>& F, i64 b,
-                        const ZetaOptions& opt, ZetaOut& res);
+                        const ZetaOptions& opt, ZetaOut& res, const int* fsplit_known = nullptr);
 
 std::set<int> working_set_for(const Hypersurface& X, Policy pol);
 
